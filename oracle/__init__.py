@@ -1,0 +1,157 @@
+"""ctypes wrapper around the plain-C oracle (oracle/sem_oracle.c).
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / ``--impl reference`` leg may import this module.  It shares no
+code with the CUDA library (paper_1403_0968_b200/csrc) and never imports it.
+
+Each wrapper names the SURVEY.md §8(c) step (O1..O7) and the PAPER.md passage
+it follows; see the C source for the definitions.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sem_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+# Plain build: -O2, no -ffast-math, no FMA contraction (FP64 rounding order is
+# exactly the order written in the C source).
+GCC_CMD = ["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", "-ffp-contract=off",
+           "-fno-fast-math", _SRC, "-o", _LIB, "-lm"]
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(GCC_CMD)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        i64 = ctypes.c_int64
+        L.ora_gll.argtypes = [ctypes.c_int, P, P]
+        L.ora_deriv.argtypes = [ctypes.c_int, P, P]
+        L.ora_geom.argtypes = [ctypes.c_int, i64, P, P, P]
+        L.ora_ax.argtypes = [ctypes.c_int, i64, P, P, P]
+        L.ora_dssum.argtypes = [i64, P, P]
+        L.ora_multiplicity.argtypes = [i64, P, P]
+        L.ora_cg.argtypes = [ctypes.c_int, i64, P, P, P, P, P, ctypes.c_double,
+                             ctypes.c_int, P, P]
+        for f in (L.ora_gll, L.ora_deriv, L.ora_geom, L.ora_ax, L.ora_dssum,
+                  L.ora_multiplicity, L.ora_cg):
+            f.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def _check(rc, what):
+    if rc != 0:
+        raise OracleError(f"{what} failed with status {rc}")
+
+
+def gll(N: int):
+    """O1: GLL nodes xi and weights w."""
+    xi = np.zeros(N + 1)
+    w = np.zeros(N + 1)
+    _check(lib().ora_gll(N, _p(xi), _p(w)), "ora_gll")
+    return xi, w
+
+
+def deriv(N: int, xi=None):
+    """O2: D_im = phi'_m(xi_i), row-major [i, m]."""
+    if xi is None:
+        xi, _ = gll(N)
+    xi = np.ascontiguousarray(xi, dtype=np.float64)
+    D = np.zeros((N + 1, N + 1))
+    _check(lib().ora_deriv(N, _p(xi), _p(D)), "ora_deriv")
+    return D
+
+
+def geom(N: int, xyz: np.ndarray):
+    """O3: geometric factors G [E,6,n^3] (rr,rs,rt,ss,st,tt; w J folded) and
+    pointwise Jacobian J [E,n^3]."""
+    n3 = (N + 1) ** 3
+    xyz = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1, 3, n3)
+    E = xyz.shape[0]
+    G = np.zeros((E, 6, n3))
+    J = np.zeros((E, n3))
+    _check(lib().ora_geom(N, E, _p(xyz), _p(G), _p(J)), "ora_geom")
+    return G, J
+
+
+def ax(N: int, G: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """O4: local unassembled unmasked w = A_L u (eq:semOperator)."""
+    n3 = (N + 1) ** 3
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    E = G.size // (6 * n3)
+    u = np.ascontiguousarray(u, dtype=np.float64).reshape(-1)
+    assert u.size == E * n3
+    w = np.zeros(E * n3)
+    _check(lib().ora_ax(N, E, _p(G), _p(u), _p(w)), "ora_ax")
+    return w
+
+
+def dssum(glo: np.ndarray, v: np.ndarray) -> np.ndarray:
+    """O5: Q Q^T v, copies summed in ascending local order."""
+    glo = np.ascontiguousarray(glo, dtype=np.int64).reshape(-1)
+    out = np.array(v, dtype=np.float64).reshape(-1).copy()
+    assert out.size == glo.size
+    _check(lib().ora_dssum(glo.size, _p(glo), _p(out)), "ora_dssum")
+    return out
+
+
+def multiplicity(glo: np.ndarray) -> np.ndarray:
+    glo = np.ascontiguousarray(glo, dtype=np.int64).reshape(-1)
+    m = np.zeros(glo.size)
+    _check(lib().ora_multiplicity(glo.size, _p(glo), _p(m)), "ora_multiplicity")
+    return m
+
+
+def cg(N: int, glo, dirichlet, G, b, x0=None, tol=1e-8, maxit=1000):
+    """O7: CG (PCG of PAPER.md:672-673, identity preconditioner).
+    Returns (x, iters, rel_res, status) with status 0 = converged, 4 = maxit."""
+    n3 = (N + 1) ** 3
+    glo = np.ascontiguousarray(glo, dtype=np.int64).reshape(-1)
+    dirichlet = np.ascontiguousarray(dirichlet, dtype=np.uint8).reshape(-1)
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
+    E = glo.size // n3
+    x = np.zeros(E * n3) if x0 is None else np.array(x0, dtype=np.float64).reshape(-1).copy()
+    iters = ctypes.c_int(0)
+    rel = ctypes.c_double(0.0)
+    rc = lib().ora_cg(N, E, _p(glo), _p(dirichlet), _p(G), _p(b), _p(x), float(tol),
+                      int(maxit), ctypes.byref(iters), ctypes.byref(rel))
+    if rc not in (0, 4):
+        raise OracleError(f"ora_cg failed with status {rc}")
+    return x, iters.value, rel.value, rc
+
+
+def mass_rhs(N: int, glo, dirichlet, J, f):
+    """b = mask Q Q^T (W J f): lumped mass (diagonal J w_abc)
+    applied to nodal f, assembled and masked (reading G7)."""
+    n = N + 1
+    _, w = gll(N)
+    w3 = np.einsum("k,j,i->kji", w, w, w).reshape(-1)
+    J = np.asarray(J).reshape(-1, n ** 3)
+    bl = (J * w3[None, :]).reshape(-1) * np.asarray(f).reshape(-1)
+    b = dssum(glo, bl)
+    return b * (1.0 - np.asarray(dirichlet, dtype=np.float64).reshape(-1))

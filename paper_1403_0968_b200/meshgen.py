@@ -1,0 +1,154 @@
+"""Seeded synthetic input generator (meshes and fields), shared by the tests,
+the oracle leg and the CUDA leg.
+
+It holds none of the method's arithmetic: no GLL nodes, no differentiation, no
+geometric factors, no assembly.  The 1-D reference node positions ``r1d`` are
+an *argument* (tests pass the oracle's GLL nodes, the product path passes the
+library's), so the same recipe feeds both sides without either importing the
+other.
+
+Recipe: a Nekbone-shaped brick box of
+ex x ey x ez conforming hexahedra on [0,Lx]x[0,Ly]x[0,Lz]; GLL nodes mapped
+affinely into each element and then deformed by
+    x <- x + eps * min(L) * S(x) * (1, 0.5, -0.7),
+    S = sin(pi x/Lx) sin(pi y/Ly) sin(pi z/Lz)     (pre-deformation coordinates)
+so shared nodes get bit-identical coordinates in every element that holds
+them and the boundary stays planar.  Global ids follow the lexicographic
+global node grid (Fischer-style global-local numbering);
+homogeneous Dirichlet on every box face (reading G7).
+
+Local storage is element-major, node (i,j,k) at e*n^3 + i + n*j + n*n*k.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+@dataclass
+class Mesh:
+    N: int
+    xyz: np.ndarray         # [E, 3, n^3] float64
+    glo: np.ndarray         # [E, n^3] int64 global node ids (consistent across ranks)
+    dirichlet: np.ndarray   # [E, n^3] uint8, 1 = Dirichlet node
+    elems: tuple            # global element grid (ex, ey, ez)
+    lengths: tuple          # box lengths
+    parts: tuple = (1, 1, 1)
+    rank: int = 0
+    eidx: np.ndarray = field(default=None)   # [E, 3] global element (a, b, c)
+    nboundary: int = 0      # leading elements that touch a partition interface
+
+    @property
+    def nelem(self) -> int:
+        return int(self.glo.shape[0])
+
+    @property
+    def nlocal(self) -> int:
+        return int(self.glo.size)
+
+    @property
+    def nglobal(self) -> int:
+        ex, ey, ez = self.elems
+        N = self.N
+        return (ex * N + 1) * (ey * N + 1) * (ez * N + 1)
+
+
+def rank_block(elems, parts, rank):
+    """Element index ranges [lo, hi) per axis owned by ``rank`` (x fastest)."""
+    px, py, pz = parts
+    rx = rank % px
+    ry = (rank // px) % py
+    rz = rank // (px * py)
+    out = []
+    for e, p, r in zip(elems, (px, py, pz), (rx, ry, rz)):
+        lo = (e * r) // p
+        hi = (e * (r + 1)) // p
+        out.append((lo, hi))
+    return out
+
+
+def default_parts(nranks: int):
+    """3-D block partition minimising surface."""
+    table = {1: (1, 1, 1), 2: (1, 1, 2), 4: (1, 2, 2), 8: (2, 2, 2)}
+    if nranks in table:
+        return table[nranks]
+    return (1, 1, nranks)
+
+
+def box_mesh(N: int, r1d, elems=(2, 2, 2), lengths=(1.0, 1.0, 1.0), eps: float = 0.0,
+             parts=(1, 1, 1), rank: int = 0, boundary_first: bool = False) -> Mesh:
+    r1d = np.asarray(r1d, dtype=np.float64)
+    n = N + 1
+    assert r1d.shape == (n,), "r1d must hold the N+1 reference node positions"
+    ex, ey, ez = elems
+    Lx, Ly, Lz = (float(v) for v in lengths)
+    (ax0, ax1), (by0, by1), (cz0, cz1) = rank_block(elems, parts, rank)
+    a, b, c = np.meshgrid(np.arange(ax0, ax1), np.arange(by0, by1), np.arange(cz0, cz1),
+                          indexing="ij")
+    # element order: a fastest, then b, then c
+    a = a.transpose(2, 1, 0).reshape(-1)
+    b = b.transpose(2, 1, 0).reshape(-1)
+    c = c.transpose(2, 1, 0).reshape(-1)
+    eidx = np.stack([a, b, c], axis=1)
+    nb = 0
+    if boundary_first and tuple(parts) != (1, 1, 1):
+        touch = np.zeros(len(a), dtype=bool)
+        for v, lo, hi, e in ((a, ax0, ax1, ex), (b, by0, by1, ey), (c, cz0, cz1, ez)):
+            touch |= (v == lo) & (lo > 0)
+            touch |= (v == hi - 1) & (hi < e)
+        order = np.concatenate([np.nonzero(touch)[0], np.nonzero(~touch)[0]])
+        nb = int(touch.sum())
+        eidx = eidx[order]
+        a, b, c = eidx[:, 0], eidx[:, 1], eidx[:, 2]
+    # local node (i,j,k), i fastest
+    k, j, i = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    i = i.reshape(-1)
+    j = j.reshape(-1)
+    k = k.reshape(-1)
+    I = a[:, None] * N + i[None, :]
+    J = b[:, None] * N + j[None, :]
+    K = c[:, None] * N + k[None, :]
+    nx, ny = ex * N + 1, ey * N + 1
+    glo = (I + nx * (J + ny * K)).astype(np.int64)
+    dirichlet = ((I == 0) | (I == ex * N) | (J == 0) | (J == ey * N) |
+                 (K == 0) | (K == ez * N)).astype(np.uint8)
+    # affine placement: x = (a + (1 + r_i)/2) * hx  (exact at shared faces)
+    x = (a[:, None] + (1.0 + r1d[i])[None, :] / 2.0) * (Lx / ex)
+    y = (b[:, None] + (1.0 + r1d[j])[None, :] / 2.0) * (Ly / ey)
+    z = (c[:, None] + (1.0 + r1d[k])[None, :] / 2.0) * (Lz / ez)
+    if eps != 0.0:
+        S = np.sin(np.pi * x / Lx) * np.sin(np.pi * y / Ly) * np.sin(np.pi * z / Lz)
+        amp = eps * min(Lx, Ly, Lz)
+        x, y, z = x + amp * S, y + 0.5 * amp * S, z - 0.7 * amp * S
+    xyz = np.stack([x, y, z], axis=1)
+    return Mesh(N=N, xyz=np.ascontiguousarray(xyz), glo=np.ascontiguousarray(glo),
+                dirichlet=np.ascontiguousarray(dirichlet), elems=tuple(elems),
+                lengths=(Lx, Ly, Lz), parts=tuple(parts), rank=rank, eidx=eidx,
+                nboundary=nb)
+
+
+def random_field(n: int, seed: int) -> np.ndarray:
+    """u ~ U(-1, 1), numpy default_rng(seed)."""
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+
+
+def manufactured(mesh: Mesh):
+    """u* = prod sin(pi x_c / L_c) (vanishes on the box faces) and
+    f = -Laplace u* = pi^2 (1/Lx^2 + 1/Ly^2 + 1/Lz^2) u*, at the nodes."""
+    Lx, Ly, Lz = mesh.lengths
+    x, y, z = mesh.xyz[:, 0], mesh.xyz[:, 1], mesh.xyz[:, 2]
+    us = np.sin(np.pi * x / Lx) * np.sin(np.pi * y / Ly) * np.sin(np.pi * z / Lz)
+    f = math.pi ** 2 * (1 / Lx ** 2 + 1 / Ly ** 2 + 1 / Lz ** 2) * us
+    return us.reshape(-1), f.reshape(-1)
+
+
+def cube_poly(mesh: Mesh):
+    """u* = x(1-x) y(1-y) z(1-z) on the unit cube (degree 2 per direction) and
+    f = -Laplace u* = 2[y(1-y)z(1-z) + x(1-x)z(1-z) + x(1-x)y(1-y)]."""
+    x, y, z = mesh.xyz[:, 0], mesh.xyz[:, 1], mesh.xyz[:, 2]
+    gx, gy, gz = x * (1 - x), y * (1 - y), z * (1 - z)
+    us = gx * gy * gz
+    f = 2.0 * (gy * gz + gx * gz + gx * gy)
+    return us.reshape(-1), f.reshape(-1)
