@@ -1,0 +1,174 @@
+/*
+ * sem.h -- C ABI of libsem, the B200-native (sm_100a) hot path of the
+ * spectral-element Poisson benchmark of arXiv 1403.0968 (OCCA), Sec.
+ * "Spectral Element Methods", PAPER.md:578-784:
+ *
+ *   sem_ax     local matrix-free stiffness operator w = A_L u on order-N hexahedra
+ *              (eq:semOperator, with kappa = 1, alpha = 0;
+ *              tensor-product GLL basis :599-604; derivative sparsity :615-625;
+ *              chain rule and G^ = G^T G "precomputed for each elemental node"
+ *              :627-665)
+ *   sem_dssum  direct-stiffness summation w <- Q Q^T w over the global-local
+ *              numbering (Fischer 1991)
+ *   sem_mask   homogeneous Dirichlet mask (paper silent; reading G7)
+ *   sem_mass   lumped diagonal mass b = J w_abc f (discrete orthogonality,
+ *              PAPER.md:605-614) -- used to assemble right-hand sides
+ *   sem_cg     the (P)CG iteration that drives them (identity
+ *              preconditioner, reading G8)
+ *
+ * Conventions (all entry points):
+ *  - Every function returns an int status (SEM_OK = 0) and never throws or
+ *    aborts across the ABI.  sem_last_error() gives a message for the last
+ *    failure on a context; sem_strerror() names a status code.
+ *  - Vectors u, w, b, x, f are DEVICE pointers (CUDA global memory on the
+ *    context's device) of nlocal = E * (N+1)^3 doubles in "local" (E-vector)
+ *    storage: node (i,j,k) of element e at e*(N+1)^3 + i + (N+1)*j + (N+1)^2*k,
+ *    i (the r direction) fastest.  They must be 8-byte aligned.  The caller owns
+ *    them (PyTorch tensors in the Python binding).
+ *  - All device work is enqueued on the CUDA stream given to sem_setup and the
+ *    call returns without a host synchronisation, except sem_setup and sem_cg,
+ *    which synchronise that stream before returning.
+ *  - The caller owns the device workspace passed to sem_setup (size from
+ *    sem_workspace_bytes); it must stay allocated until sem_free.  The library
+ *    allocates no device memory of its own on one rank; with nranks > 1 it
+ *    allocates its small interface-exchange buffers and NCCL does its own.
+ *  - sem_setup, sem_dssum and sem_cg are COLLECTIVE when nranks > 1: every rank
+ *    must call them in the same order.
+ *  - Errors: SEM_EINVAL for a NULL pointer, N outside [1, SEM_NMAX], an empty or
+ *    malformed mesh (non-positive Jacobian, inconsistent Dirichlet flags across
+ *    copies of a global node, an element-interior node that is shared or
+ *    Dirichlet), or a misaligned pointer; SEM_ECUDA for a CUDA runtime failure
+ *    (the context is then unusable); SEM_ENCCL for an NCCL failure;
+ *    SEM_ENOCONV when sem_cg reached maxit with tol > 0 (x holds the last
+ *    iterate; not a failure for tol == 0); SEM_ESTATE for a NULL/freed context.
+ */
+#ifndef SEM_H
+#define SEM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SEM_NMAX 15
+
+enum sem_status {
+    SEM_OK = 0,
+    SEM_EINVAL = 1,
+    SEM_ECUDA = 2,
+    SEM_ENCCL = 3,
+    SEM_ENOCONV = 4,
+    SEM_ESTATE = 5
+};
+
+/* Host-side all-gather used ONLY during sem_setup when nranks > 1 (to find the
+ * global ids shared with each peer).  Must place the `bytes` bytes of every
+ * rank's `send` buffer into `recv` in rank order (recv holds nranks*bytes).
+ * Returns 0 on success.  The Python binding implements it with
+ * torch.distributed (gloo or nccl). */
+typedef int (*sem_allgather_fn)(void *user, const void *send, size_t bytes, void *recv);
+
+typedef struct {
+    int32_t nelem;             /* E, elements owned by this rank (> 0)                      */
+    const double *xyz;         /* HOST [E][3][(N+1)^3] coordinates of the GLL nodes
+                                  (isoparametric map x(r,s,t)), i fastest      */
+    const int64_t *glo;        /* HOST [E][(N+1)^3] global node ids (global-local numbering,
+                                  PAPER.md:667), consistent across ranks, >= 0               */
+    const uint8_t *dirichlet;  /* HOST [E][(N+1)^3] 1 = homogeneous Dirichlet node           */
+    int32_t nboundary;         /* the first nboundary elements touch a partition interface
+                                  (ordering hint for overlap; 0 = unknown)                   */
+    int32_t rank, nranks;      /* 0, 1 on one GPU                                            */
+    const void *nccl_id;       /* 128-byte ncclUniqueId (rank 0's), required if nranks > 1   */
+    sem_allgather_fn allgather;/* setup-time host all-gather, required if nranks > 1         */
+    void *allgather_user;
+    int32_t device;            /* CUDA device ordinal                                        */
+} sem_mesh;
+
+typedef struct sem_ctx sem_ctx;  /* opaque; created by sem_setup, destroyed by sem_free */
+
+/* Library version string. */
+const char *sem_version(void);
+
+/* The library's own 1-D GLL nodes xi[N+1] (ascending, xi_0 = -1, xi_N = 1) and
+ * weights w[N+1].  HOST arrays.  Pure function; no
+ * GPU needed.  Mesh generators use xi to place the GLL nodes. */
+int sem_gll(int N, double *xi, double *w);
+
+/* Bytes of device workspace sem_setup needs for this mesh and order.  Pure
+ * host query (looks only at nelem); no GPU needed. */
+int sem_workspace_bytes(const sem_mesh *mesh, int N, size_t *bytes);
+
+/* Build a context: GLL nodes and D (a0), geometric factors G^ with w J folded in
+ * on the GPU (a1), gather-scatter plan from glo (a2, :667),
+ * and for nranks > 1 the NCCL communicator and interface exchange lists.
+ * `workspace` is a DEVICE buffer of at least sem_workspace_bytes bytes, 256-byte
+ * aligned.  `cuda_stream` is a cudaStream_t (NULL = legacy default stream).
+ * Collective.  Synchronises the stream before returning. */
+int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t bytes,
+              void *cuda_stream, sem_ctx **out);
+
+/* nlocal = E (N+1)^3 on this rank; nglobal = number of distinct global ids on
+ * ALL ranks. */
+int sem_sizes(const sem_ctx *ctx, int64_t *nlocal, int64_t *nglobal);
+
+/* w = A_L u: local, unassembled, unmasked stiffness apply (eq:semOperator).
+ * u and w are DEVICE [nlocal] and must not alias.  Asynchronous. */
+int sem_ax(sem_ctx *ctx, const double *u, double *w);
+
+/* In place w <- Q Q^T w (copies of each global id summed in ascending local
+ * order, then summed across ranks in ascending rank order).  No mask.
+ * Collective.  Asynchronous. */
+int sem_dssum(sem_ctx *ctx, double *w);
+
+/* In place w <- mask .* w (zero at Dirichlet nodes).  Asynchronous. */
+int sem_mask(sem_ctx *ctx, double *w);
+
+/* b = B_L f with B_L = diag(w_i w_j w_k J) the lumped local mass
+ * (PAPER.md:605-614).  Unassembled; follow with sem_dssum / sem_mask to form a
+ * right-hand side.  f and b may alias.  Asynchronous. */
+int sem_mass(sem_ctx *ctx, const double *f, double *b);
+
+/* Solve mask Q Q^T A_L x = mask b by CG (recurrence and
+ * stopping rule in DESIGN.md / SURVEY.md §8(c) O7):
+ *   inner product (a,b)_c = sum over distinct non-Dirichlet global nodes;
+ *   stop before iteration k when k == maxit or sqrt(rho_k) <= tol sqrt(rho_0).
+ * b: DEVICE, continuous (already assembled); x: DEVICE, in = x0, out = solution.
+ * iters / rel_res (HOST, may be NULL) receive the iteration count and
+ * sqrt(rho_k / rho_0).  Collective.  Synchronises the stream.  Returns
+ * SEM_ENOCONV if maxit was reached with tol > 0. */
+int sem_cg(sem_ctx *ctx, const double *b, double *x, double tol, int maxit,
+           int *iters, double *rel_res);
+
+/* Size of an ncclUniqueId (128) and a fresh one, for rank 0 to broadcast to
+ * the other ranks before sem_setup (HOST buffer of sem_nccl_id_bytes()). */
+int sem_nccl_id_bytes(void);
+int sem_nccl_get_unique_id(void *id_out);
+
+/* Device timing per kernel class, for the benchmark's roofline report.
+ * sem_profile(ctx, 1) resets the accumulators and brackets every later launch
+ * with a pair of CUDA events on the context stream (host-side cost only);
+ * sem_profile(ctx, 0) stops.  sem_profile_read synchronises the stream and
+ * returns, for class `which` (0 = sem_ax kernel, 1 = fused CG Ax kernel K1,
+ * 2 = gather-scatter, 3 = CG r-update/dot kernel, 4 = other), the summed
+ * device milliseconds, the number of launches that did work (CG launches after
+ * the stopping decision are excluded) and their ALGORITHMIC bytes (DESIGN.md:
+ * Ax 64 B/node; K1 96 B/node, 72 at k = 0; r-update 24 B/node; gather-scatter
+ * 16 B per surface copy + 8 B per non-Dirichlet group for (w,p)). */
+int sem_profile(sem_ctx *ctx, int enable);
+int sem_profile_read(sem_ctx *ctx, int which, double *ms, int64_t *launches, double *bytes);
+
+/* Number of kernels this context has launched so far (all entry points). */
+int64_t sem_launch_count(const sem_ctx *ctx);
+
+/* Destroy the context (the caller still owns workspace and vectors). */
+void sem_free(sem_ctx *ctx);
+
+const char *sem_strerror(int code);
+const char *sem_last_error(const sem_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEM_H */

@@ -1,0 +1,715 @@
+// sem_host.cpp -- host orchestration behind the C ABI of include/sem.h.
+//
+// a0  GLL nodes/weights and the differentiation matrix (own implementation:
+//     simultaneous Newton on all N+1 nodes with a Legendre Vandermonde, and the
+//     barycentric form of D; it shares nothing with oracle/).
+// a2  gather-scatter plan from the global-local numbering.
+// a9  CG driver: device-resident scalars, no per-iteration host sync, exact
+//     iteration count via a sticky device flag polled once per chunk.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/sem.h"
+#include "sem_internal.h"
+#include "sem_comm.h"
+
+using namespace sem;
+
+// kernel classes for sem_profile_read (documented in include/sem.h)
+enum { kProfAx = 0, kProfAxCg = 1, kProfGs = 2, kProfRr = 3, kProfOther = 4, kProfClasses = 5 };
+
+struct sem_ctx {
+    int N = 0, n = 0, n3 = 0;
+    int64_t E = 0, L = 0, nglobal = 0;
+    int rank = 0, nranks = 1, device = 0;
+    cudaStream_t stream = nullptr;
+    DevMesh dm{};
+    CgVecs cv{};
+    int nb_ax = 0;
+    CgState *host_state = nullptr;   // pinned, 2 slots for double-buffered polling
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int64_t launches = 0;
+    bool broken = false;
+    // optional per-kernel-class device timing (bench roofline), see sem_profile
+    bool prof = false;
+    struct Rec { cudaEvent_t a, b; int cls; int k; double bytes; };
+    std::vector<Rec> recs;               // pending (not yet folded)
+    std::vector<cudaEvent_t> evpool;
+    double prof_ms[kProfClasses] = {0};
+    double prof_bytes[kProfClasses] = {0};
+    int64_t prof_n[kProfClasses] = {0};
+    std::string err;
+    Comm *comm = nullptr;            // nranks > 1 only
+};
+
+static thread_local std::string g_err;
+
+static int fail(sem_ctx *c, int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    g_err = buf;
+    return code;
+}
+
+struct sem_ctx;
+static cudaEvent_t prof_event(sem_ctx *ctx);
+static void prof_fold(sem_ctx *ctx, int iters);
+
+#define CU(call)                                                                     \
+    do {                                                                             \
+        cudaError_t e_ = (call);                                                     \
+        if (e_ != cudaSuccess) {                                                     \
+            if (ctx) ctx->broken = true;                                             \
+            return fail(ctx, SEM_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                         \
+        }                                                                            \
+    } while (0)
+
+#define LAUNCH(call) LAUNCHP(kProfOther, 0.0, -1, call)
+
+// Launch with optional device timing: class `cls`, algorithmic bytes `by`,
+// CG iteration `kk` (-1 outside CG; CG launches at k >= iters are no-ops and
+// are dropped when the solve is folded).
+#define LAUNCHP(cls, by, kk, call)                                                   \
+    do {                                                                             \
+        ctx->launches++;                                                             \
+        cudaEvent_t a_ = nullptr, b_ = nullptr;                                      \
+        if (ctx->prof) {                                                             \
+            a_ = prof_event(ctx);                                                    \
+            b_ = prof_event(ctx);                                                    \
+            CU(cudaEventRecord(a_, ctx->stream));                                    \
+        }                                                                            \
+        CU(call);                                                                    \
+        if (ctx->prof) {                                                             \
+            CU(cudaEventRecord(b_, ctx->stream));                                    \
+            ctx->recs.push_back({a_, b_, (cls), (kk), (by)});                        \
+        }                                                                            \
+    } while (0)
+
+static cudaEvent_t prof_event(sem_ctx *ctx) {
+    cudaEvent_t e = nullptr;
+    if (!ctx->evpool.empty()) {
+        e = ctx->evpool.back();
+        ctx->evpool.pop_back();
+    } else if (cudaEventCreate(&e) != cudaSuccess) {
+        e = nullptr;
+    }
+    return e;
+}
+
+// Fold completed records into the accumulators (stream must be synchronised).
+// iters >= 0: records of a CG solve; launches with k >= iters were no-ops.
+static void prof_fold(sem_ctx *ctx, int iters) {
+    for (auto &r : ctx->recs) {
+        float ms = 0.f;
+        bool keep = (r.k < 0) || (iters >= 0 && r.k < iters);
+        if (keep && cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+            ctx->prof_ms[r.cls] += ms;
+            ctx->prof_bytes[r.cls] += r.bytes;
+            ctx->prof_n[r.cls] += 1;
+        }
+        ctx->evpool.push_back(r.a);
+        ctx->evpool.push_back(r.b);
+    }
+    ctx->recs.clear();
+}
+
+// ---------------------------------------------------------------------------
+// a0: GLL nodes/weights and D
+// ---------------------------------------------------------------------------
+extern "C" int sem_gll(int N, double *xi, double *w) {
+    if (N < 1 || N > 64 || !xi || !w) return fail(nullptr, SEM_EINVAL, "sem_gll: bad arguments");
+    const int n = N + 1;
+    std::vector<double> x(n), xold(n), P(n * (N + 1));
+    // initial guess: Chebyshev-Gauss-Lobatto points, ascending
+    for (int i = 0; i < n; ++i) x[i] = -std::cos(M_PI * i / N);
+    // Newton on (1 - x^2) P'_N(x) for all nodes at once, using
+    // (1 - x^2) P'_N = N (P_{N-1} - x P_N) and d/dx of that = -N (N+1) P_N:
+    //   x <- x - (x P_N - P_{N-1}) / ((N+1) P_N)
+    for (int it = 0; it < 200; ++it) {
+        for (int i = 0; i < n; ++i) {
+            double p0 = 1.0, p1 = x[i];
+            for (int k = 2; k <= N; ++k) {
+                double p2 = ((2 * k - 1) * x[i] * p1 - (k - 1) * p0) / k;
+                p0 = p1;
+                p1 = p2;
+            }
+            // p1 = P_N, p0 = P_{N-1}  (for N == 1: p1 = x, p0 = 1)
+            P[i] = p1;
+            xold[i] = x[i];
+            x[i] = xold[i] - (xold[i] * p1 - p0) / ((N + 1) * p1);
+        }
+        double d = 0.0;
+        for (int i = 0; i < n; ++i) d = std::max(d, std::fabs(x[i] - xold[i]));
+        if (d < 4e-16) break;
+    }
+    // exact endpoints and mirror symmetry
+    x[0] = -1.0;
+    x[N] = 1.0;
+    for (int i = 1; i < n / 2; ++i) {
+        double a = 0.5 * (x[N - i] - x[i]);
+        x[i] = -a;
+        x[N - i] = a;
+    }
+    if (N % 2 == 0) x[N / 2] = 0.0;
+    for (int i = 0; i < n; ++i) {
+        double p0 = 1.0, p1 = x[i];
+        for (int k = 2; k <= N; ++k) {
+            double p2 = ((2 * k - 1) * x[i] * p1 - (k - 1) * p0) / k;
+            p0 = p1;
+            p1 = p2;
+        }
+        xi[i] = x[i];
+        w[i] = 2.0 / (N * (N + 1.0) * p1 * p1);
+    }
+    return SEM_OK;
+}
+
+// Barycentric differentiation matrix: D_ij = (lam_j / lam_i) / (x_i - x_j),
+// lam_j = 1 / prod_{k != j} (x_j - x_k); D_ii = -sum_{j != i} D_ij.
+static void diff_matrix(int N, const double *x, double *D) {
+    const int n = N + 1;
+    std::vector<double> lam(n);
+    for (int j = 0; j < n; ++j) {
+        double p = 1.0;
+        for (int k = 0; k < n; ++k)
+            if (k != j) p *= (x[j] - x[k]);
+        lam[j] = 1.0 / p;
+    }
+    for (int i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < n; ++j) {
+            if (j == i) continue;
+            double v = (lam[j] / lam[i]) / (x[i] - x[j]);
+            D[i * n + j] = v;
+            s += v;
+        }
+        D[i * n + i] = -s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// workspace layout
+// ---------------------------------------------------------------------------
+namespace {
+struct Layout {
+    size_t G, BM, r, p, w, D, gs_off, gs_idx, owner, partials, rr_all, pap_all, st, total;
+    int64_t nsurf_cap, partial_cap;
+};
+
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+Layout make_layout(int N, int64_t E, int nranks) {
+    Layout Lo{};
+    const int64_t n = N + 1, n3 = n * n * n, L = E * n3;
+    const int64_t ni = (n >= 2) ? (n - 2) : 0;
+    Lo.nsurf_cap = E * (n3 - ni * ni * ni);
+    const int nb_ax = ax_blocks(N, E);
+    const int64_t nb_gs = (Lo.nsurf_cap + kGsThreads - 1) / kGsThreads + 1;
+    Lo.partial_cap = std::max<int64_t>(nb_ax + nb_gs, kRrBlocks) + 16;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        size_t at = o;
+        o = align256(o + bytes);
+        return at;
+    };
+    Lo.G = take(sizeof(double) * 6 * L);
+    Lo.BM = take(sizeof(double) * L);
+    Lo.r = take(sizeof(double) * L);
+    Lo.p = take(sizeof(double) * L);
+    Lo.w = take(sizeof(double) * L);
+    Lo.D = take(sizeof(double) * (n * n + n));
+    Lo.gs_off = take(sizeof(int32_t) * (Lo.nsurf_cap + 1));
+    Lo.gs_idx = take(sizeof(int32_t) * Lo.nsurf_cap);
+    Lo.owner = take(sizeof(uint32_t) * ((L + 31) / 32));
+    Lo.partials = take(sizeof(double) * Lo.partial_cap);
+    Lo.rr_all = take(sizeof(double) * kRing * nranks);
+    Lo.pap_all = take(sizeof(double) * kRing * nranks);
+    Lo.st = take(sizeof(CgState));
+    Lo.total = o;
+    return Lo;
+}
+}  // namespace
+
+static int check_mesh(const sem_mesh *m, int N) {
+    if (!m) return fail(nullptr, SEM_EINVAL, "mesh is NULL");
+    if (N < 1 || N > SEM_NMAX) return fail(nullptr, SEM_EINVAL, "N=%d outside [1,%d]", N, SEM_NMAX);
+    if (m->nelem <= 0) return fail(nullptr, SEM_EINVAL, "nelem=%d must be > 0", m->nelem);
+    if (m->nranks < 1 || m->nranks > kMaxRanks || m->rank < 0 || m->rank >= m->nranks)
+        return fail(nullptr, SEM_EINVAL, "bad rank %d / nranks %d", m->rank, m->nranks);
+    const int64_t n3 = int64_t(N + 1) * (N + 1) * (N + 1);
+    if (int64_t(m->nelem) * n3 >= (int64_t(1) << 31))
+        return fail(nullptr, SEM_EINVAL, "nlocal >= 2^31 not supported");
+    return SEM_OK;
+}
+
+extern "C" int sem_workspace_bytes(const sem_mesh *m, int N, size_t *bytes) {
+    int rc = check_mesh(m, N);
+    if (rc) return rc;
+    if (!bytes) return fail(nullptr, SEM_EINVAL, "bytes is NULL");
+    *bytes = make_layout(N, m->nelem, m->nranks).total;
+    return SEM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// a2: gather-scatter plan (host)
+// ---------------------------------------------------------------------------
+namespace {
+struct HostPlan {
+    std::vector<int32_t> off, idx;
+    int32_t ngroups = 0, ndir = 0;
+    std::vector<uint32_t> owner;
+    int64_t ndistinct = 0;
+    // for multi-rank: distinct surface global ids (ascending) and their group
+    std::vector<int64_t> surf_ids;
+    std::vector<int32_t> surf_group;
+};
+
+// order[] = local indices sorted by (glo, local index) -- counting sort when the
+// id range is compact, std::sort otherwise.
+std::vector<int32_t> sort_by_glo(const int64_t *glo, int64_t L, int64_t gmin, int64_t gmax) {
+    std::vector<int32_t> order(L);
+    const int64_t range = gmax - gmin + 1;
+    if (range <= 4 * L + 1024) {
+        std::vector<int32_t> cnt(range + 1, 0);
+        for (int64_t l = 0; l < L; ++l) cnt[glo[l] - gmin + 1]++;
+        for (int64_t g = 0; g < range; ++g) cnt[g + 1] += cnt[g];
+        for (int64_t l = 0; l < L; ++l) order[cnt[glo[l] - gmin]++] = (int32_t)l;
+    } else {
+        for (int64_t l = 0; l < L; ++l) order[l] = (int32_t)l;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int32_t a, int32_t b) { return glo[a] < glo[b]; });
+    }
+    return order;
+}
+
+int build_plan(const sem_mesh *m, int N, HostPlan &hp, std::string &err) {
+    const int n = N + 1, n3 = n * n * n;
+    const int64_t L = int64_t(m->nelem) * n3;
+    const int64_t *glo = m->glo;
+    const uint8_t *dir = m->dirichlet;
+    int64_t gmin = glo[0], gmax = glo[0];
+    for (int64_t l = 0; l < L; ++l) {
+        if (glo[l] < 0) { err = "negative global id"; return SEM_EINVAL; }
+        gmin = std::min(gmin, glo[l]);
+        gmax = std::max(gmax, glo[l]);
+    }
+    std::vector<uint8_t> surf(n3);
+    for (int q = 0; q < n3; ++q) {
+        int i = q % n, j = (q / n) % n, k = q / (n * n);
+        surf[q] = (i == 0 || i == N || j == 0 || j == N || k == 0 || k == N);
+    }
+    std::vector<int32_t> order = sort_by_glo(glo, L, gmin, gmax);
+    struct G { int32_t a, b; uint8_t d; int32_t first; };
+    std::vector<G> groups;
+    hp.owner.assign((L + 31) / 32, 0u);
+    int64_t a = 0;
+    hp.ndistinct = 0;
+    while (a < L) {
+        int64_t b = a + 1;
+        const int64_t g = glo[order[a]];
+        while (b < L && glo[order[b]] == g) ++b;
+        hp.ndistinct++;
+        const uint8_t d0 = dir[order[a]] ? 1 : 0;
+        bool any_interior = false;
+        for (int64_t t = a; t < b; ++t) {
+            if ((dir[order[t]] ? 1 : 0) != d0) {
+                err = "inconsistent Dirichlet flags across copies of global id " + std::to_string(g);
+                return SEM_EINVAL;
+            }
+            if (!surf[order[t] % n3]) any_interior = true;
+        }
+        if (any_interior) {
+            if (b - a > 1) {
+                err = "element-interior node shared (global id " + std::to_string(g) + ")";
+                return SEM_EINVAL;
+            }
+            if (d0) {
+                err = "element-interior node marked Dirichlet (global id " + std::to_string(g) + ")";
+                return SEM_EINVAL;
+            }
+        } else {
+            groups.push_back({(int32_t)a, (int32_t)b, d0, order[a]});
+        }
+        if (!d0) {
+            const int32_t o = order[a];  // lowest local index owns the node
+            hp.owner[o >> 5] |= 1u << (o & 31);
+        }
+        a = b;
+    }
+    // Dirichlet groups first, then by multiplicity, then by first local index
+    std::stable_sort(groups.begin(), groups.end(), [](const G &x, const G &y) {
+        if (x.d != y.d) return x.d > y.d;
+        const int mx = x.b - x.a, my = y.b - y.a;
+        if (mx != my) return mx < my;
+        return x.first < y.first;
+    });
+    hp.ngroups = (int32_t)groups.size();
+    hp.off.resize(groups.size() + 1);
+    hp.idx.clear();
+    hp.ndir = 0;
+    hp.off[0] = 0;
+    for (size_t q = 0; q < groups.size(); ++q) {
+        for (int32_t t = groups[q].a; t < groups[q].b; ++t) hp.idx.push_back(order[t]);
+        hp.off[q + 1] = (int32_t)hp.idx.size();
+        if (groups[q].d) hp.ndir++;
+    }
+    // surface ids (for the inter-rank exchange)
+    hp.surf_ids.resize(groups.size());
+    hp.surf_group.resize(groups.size());
+    {
+        std::vector<std::pair<int64_t, int32_t>> sg(groups.size());
+        for (size_t q = 0; q < groups.size(); ++q) sg[q] = {glo[hp.idx[hp.off[q]]], (int32_t)q};
+        std::sort(sg.begin(), sg.end());
+        for (size_t q = 0; q < sg.size(); ++q) {
+            hp.surf_ids[q] = sg[q].first;
+            hp.surf_group[q] = sg[q].second;
+        }
+    }
+    return SEM_OK;
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// setup / teardown
+// ---------------------------------------------------------------------------
+extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t bytes,
+                         void *cuda_stream, sem_ctx **out) {
+    sem_ctx *ctx = nullptr;
+    int rc = check_mesh(mesh, N);
+    if (rc) return rc;
+    if (!out || !workspace || !mesh->xyz || !mesh->glo || !mesh->dirichlet)
+        return fail(nullptr, SEM_EINVAL, "NULL argument to sem_setup");
+    if (reinterpret_cast<uintptr_t>(workspace) % 256)
+        return fail(nullptr, SEM_EINVAL, "workspace must be 256-byte aligned");
+    if (mesh->nranks > 1 && (!mesh->nccl_id || !mesh->allgather))
+        return fail(nullptr, SEM_EINVAL, "nranks > 1 needs nccl_id and allgather");
+    const Layout Lo = make_layout(N, mesh->nelem, mesh->nranks);
+    if (bytes < Lo.total)
+        return fail(nullptr, SEM_EINVAL, "workspace too small: %zu < %zu", bytes, Lo.total);
+    *out = nullptr;
+
+    HostPlan hp;
+    std::string perr;
+    rc = build_plan(mesh, N, hp, perr);
+    if (rc) return fail(nullptr, rc, "%s", perr.c_str());
+
+    ctx = new (std::nothrow) sem_ctx;
+    if (!ctx) return fail(nullptr, SEM_EINVAL, "out of host memory");
+    ctx->N = N;
+    ctx->n = N + 1;
+    ctx->n3 = ctx->n * ctx->n * ctx->n;
+    ctx->E = mesh->nelem;
+    ctx->L = ctx->E * ctx->n3;
+    ctx->rank = mesh->rank;
+    ctx->nranks = mesh->nranks;
+    ctx->device = mesh->device;
+    ctx->stream = (cudaStream_t)cuda_stream;
+    ctx->nglobal = hp.ndistinct;
+    auto bail = [&](int code) {
+        sem_free(ctx);
+        return code;
+    };
+    {
+        cudaError_t e = cudaSetDevice(mesh->device);
+        if (e != cudaSuccess) {
+            fail(nullptr, SEM_ECUDA, "cudaSetDevice(%d): %s", mesh->device, cudaGetErrorString(e));
+            return bail(SEM_ECUDA);
+        }
+    }
+    char *ws = static_cast<char *>(workspace);
+    DevMesh &dm = ctx->dm;
+    dm.N = N;
+    dm.n = ctx->n;
+    dm.n3 = ctx->n3;
+    dm.E = ctx->E;
+    dm.L = ctx->L;
+    dm.D = reinterpret_cast<double *>(ws + Lo.D);
+    dm.G = reinterpret_cast<double *>(ws + Lo.G);
+    dm.BM = reinterpret_cast<double *>(ws + Lo.BM);
+    dm.gs_off = reinterpret_cast<int32_t *>(ws + Lo.gs_off);
+    dm.gs_idx = reinterpret_cast<int32_t *>(ws + Lo.gs_idx);
+    dm.ngroups = hp.ngroups;
+    dm.ndir = hp.ndir;
+    dm.nsurf = (int32_t)hp.idx.size();
+    dm.owner = reinterpret_cast<uint32_t *>(ws + Lo.owner);
+    dm.rank = ctx->rank;
+    dm.nranks = ctx->nranks;
+    CgVecs &cv = ctx->cv;
+    cv.r = reinterpret_cast<double *>(ws + Lo.r);
+    cv.p = reinterpret_cast<double *>(ws + Lo.p);
+    cv.w = reinterpret_cast<double *>(ws + Lo.w);
+    cv.partials = reinterpret_cast<double *>(ws + Lo.partials);
+    cv.rr_all = reinterpret_cast<double *>(ws + Lo.rr_all);
+    cv.pap_all = reinterpret_cast<double *>(ws + Lo.pap_all);
+    cv.st = reinterpret_cast<CgState *>(ws + Lo.st);
+    ctx->nb_ax = ax_blocks(N, ctx->E);
+
+    rc = [&]() -> int {
+        const int n = ctx->n;
+        std::vector<double> xw(n), wq(n), Dh(n * n + n);
+        sem_gll(N, xw.data(), wq.data());
+        diff_matrix(N, xw.data(), Dh.data());
+        for (int i = 0; i < n; ++i) Dh[n * n + i] = wq[i];
+        cudaStream_t s = ctx->stream;
+        CU(cudaHostAlloc(&ctx->host_state, 2 * sizeof(CgState), cudaHostAllocDefault));
+        CU(cudaEventCreateWithFlags(&ctx->ev[0], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&ctx->ev[1], cudaEventDisableTiming));
+        CU(cudaMemcpyAsync((void *)dm.D, Dh.data(), sizeof(double) * Dh.size(),
+                           cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync((void *)dm.gs_off, hp.off.data(), sizeof(int32_t) * hp.off.size(),
+                           cudaMemcpyHostToDevice, s));
+        if (!hp.idx.empty())
+            CU(cudaMemcpyAsync((void *)dm.gs_idx, hp.idx.data(), sizeof(int32_t) * hp.idx.size(),
+                               cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync((void *)dm.owner, hp.owner.data(), sizeof(uint32_t) * hp.owner.size(),
+                           cudaMemcpyHostToDevice, s));
+        CU(cudaMemsetAsync(cv.st, 0, sizeof(CgState), s));
+        CU(cudaMemsetAsync(cv.rr_all, 0, sizeof(double) * kRing * ctx->nranks, s));
+        CU(cudaMemsetAsync(cv.pap_all, 0, sizeof(double) * kRing * ctx->nranks, s));
+        // xyz -> device (temporarily in r|p|w, exactly 3L doubles), then G^, B
+        double *xyz_d = cv.r;
+        int *bad_d = reinterpret_cast<int *>(cv.partials);
+        CU(cudaMemcpyAsync(xyz_d, mesh->xyz, sizeof(double) * 3 * ctx->L, cudaMemcpyHostToDevice, s));
+        CU(cudaMemsetAsync(bad_d, 0, sizeof(int), s));
+        LAUNCH(launch_geom(dm, xyz_d, const_cast<double *>(dm.G), const_cast<double *>(dm.BM),
+                           bad_d, s));
+        int bad = 0;
+        CU(cudaMemcpyAsync(&bad, bad_d, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        if (bad) return fail(ctx, SEM_EINVAL, "non-positive Jacobian in the mesh");
+        if (ctx->nranks > 1) {
+            std::string cerr;
+            int crc = comm_setup(ctx->comm, mesh, hp.surf_ids, hp.surf_group, hp.off, hp.idx,
+                                 ctx->nglobal, s, cerr);
+            if (crc) return fail(ctx, crc, "%s", cerr.c_str());
+        }
+        return SEM_OK;
+    }();
+    if (rc) {
+        g_err = ctx->err;
+        return bail(rc);
+    }
+    *out = ctx;
+    return SEM_OK;
+}
+
+extern "C" void sem_free(sem_ctx *ctx) {
+    if (!ctx) return;
+    if (ctx->comm) comm_free(ctx->comm);
+    if (ctx->host_state) cudaFreeHost(ctx->host_state);
+    for (auto &r : ctx->recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : ctx->evpool) cudaEventDestroy(e);
+    for (auto &e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    delete ctx;
+}
+
+extern "C" int sem_sizes(const sem_ctx *ctx, int64_t *nlocal, int64_t *nglobal) {
+    if (!ctx) return fail(nullptr, SEM_ESTATE, "NULL context");
+    if (nlocal) *nlocal = ctx->L;
+    if (nglobal) *nglobal = ctx->nglobal;
+    return SEM_OK;
+}
+
+extern "C" int64_t sem_launch_count(const sem_ctx *ctx) { return ctx ? ctx->launches : -1; }
+
+#define CHECK_CTX()                                                                  \
+    do {                                                                             \
+        if (!ctx) return fail(nullptr, SEM_ESTATE, "NULL context");                  \
+        if (ctx->broken) return fail(ctx, SEM_ECUDA, "context unusable after a CUDA error"); \
+    } while (0)
+
+static bool aligned8(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
+
+extern "C" int sem_ax(sem_ctx *ctx, const double *u, double *w) {
+    CHECK_CTX();
+    if (!u || !w || !aligned8(u) || !aligned8(w)) return fail(ctx, SEM_EINVAL, "sem_ax: bad pointer");
+    if (u == w) return fail(ctx, SEM_EINVAL, "sem_ax: u and w must not alias");
+    LAUNCHP(kProfAx, 64.0 * ctx->L, -1, launch_ax(ctx->dm, u, w, ctx->stream));
+    return SEM_OK;
+}
+
+static int dssum_impl(sem_ctx *ctx, double *w, int mode, int k) {
+    if (ctx->nranks == 1) {
+        const double by = 16.0 * ctx->dm.nsurf + (mode == 2 ? 8.0 * (ctx->dm.ngroups - ctx->dm.ndir) : 0.0);
+        LAUNCHP(kProfGs, by, mode == 2 ? k : -1,
+                launch_gs(ctx->dm, w, mode, &ctx->cv, k, ctx->nb_ax, ctx->stream));
+        return SEM_OK;
+    }
+    std::string cerr;
+    int64_t nl = 0;
+    int rc = comm_dssum(ctx->comm, ctx->dm, w, mode, &ctx->cv, k, ctx->nb_ax, ctx->stream, nl, cerr);
+    ctx->launches += nl;
+    if (rc) {
+        if (rc == SEM_ECUDA) ctx->broken = true;
+        return fail(ctx, rc, "%s", cerr.c_str());
+    }
+    return SEM_OK;
+}
+
+extern "C" int sem_dssum(sem_ctx *ctx, double *w) {
+    CHECK_CTX();
+    if (!w || !aligned8(w)) return fail(ctx, SEM_EINVAL, "sem_dssum: bad pointer");
+    return dssum_impl(ctx, w, 0, 0);
+}
+
+extern "C" int sem_mask(sem_ctx *ctx, double *w) {
+    CHECK_CTX();
+    if (!w || !aligned8(w)) return fail(ctx, SEM_EINVAL, "sem_mask: bad pointer");
+    if (ctx->dm.ndir > 0) LAUNCH(launch_mask(ctx->dm, w, ctx->stream));
+    return SEM_OK;
+}
+
+extern "C" int sem_mass(sem_ctx *ctx, const double *f, double *b) {
+    CHECK_CTX();
+    if (!f || !b || !aligned8(f) || !aligned8(b)) return fail(ctx, SEM_EINVAL, "sem_mass: bad pointer");
+    LAUNCH(launch_mass(ctx->dm, f, b, ctx->stream));
+    return SEM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// a9: CG driver
+// ---------------------------------------------------------------------------
+static int allgather_scalar(sem_ctx *ctx, double *slot_base) {
+    if (ctx->nranks == 1) return SEM_OK;
+    std::string cerr;
+    int rc = comm_allgather_scalar(ctx->comm, slot_base, ctx->stream, cerr);
+    if (rc) return fail(ctx, rc, "%s", cerr.c_str());
+    return SEM_OK;
+}
+
+extern "C" int sem_cg(sem_ctx *ctx, const double *b, double *x, double tol, int maxit,
+                      int *iters, double *rel_res) {
+    CHECK_CTX();
+    if (!b || !x || !aligned8(b) || !aligned8(x)) return fail(ctx, SEM_EINVAL, "sem_cg: bad pointer");
+    if (!(tol >= 0.0) || maxit < 0) return fail(ctx, SEM_EINVAL, "sem_cg: tol >= 0 and maxit >= 0 required");
+    cudaStream_t s = ctx->stream;
+    CgVecs &v = ctx->cv;
+    v.b = b;
+    v.x = x;
+    const int P = ctx->nranks;
+    int rc;
+    // tol / maxit into the device state (the init kernel resets the rest)
+    {
+        CgState h{};
+        h.tol = tol;
+        h.maxit = maxit;
+        CU(cudaMemcpyAsync(&v.st->tol, &h.tol, sizeof(double), cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(&v.st->maxit, &h.maxit, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    }
+    // r = mask (b - Q Q^T A_L x0)
+    LAUNCH(launch_ax(ctx->dm, x, v.w, s));
+    if ((rc = dssum_impl(ctx, v.w, 1, 0))) return rc;
+    LAUNCH(launch_cg_init(ctx->dm, v, s));
+    if (ctx->dm.ndir > 0) LAUNCH(launch_mask(ctx->dm, v.r, s));
+    LAUNCH(launch_rr(ctx->dm, v, 0, false, s));
+    if ((rc = allgather_scalar(ctx, v.rr_all + 0 * P))) return rc;
+
+    // iterations, enqueued in chunks; the device flag is polled one chunk behind
+    const int chunk = 8;
+    int k = 0, c = 0;
+    bool finished = false;
+    while (!finished) {
+        for (int q = 0; q < chunk && k <= maxit; ++q, ++k) {
+            LAUNCHP(kProfAxCg, (k == 0 ? 72.0 : 96.0) * ctx->L, k, launch_ax_cg(ctx->dm, v, k, s));
+            if (k == maxit) continue;  // K1(maxit) only evaluates the stopping rule
+            if ((rc = dssum_impl(ctx, v.w, 2, k))) return rc;
+            if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P))) return rc;
+            LAUNCHP(kProfRr, 24.0 * ctx->L, k, launch_rr(ctx->dm, v, k, true, s));
+            if ((rc = allgather_scalar(ctx, v.rr_all + ((k + 1) & 3) * P))) return rc;
+        }
+        CU(cudaMemcpyAsync(&ctx->host_state[c & 1], v.st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
+        CU(cudaEventRecord(ctx->ev[c & 1], s));
+        if (k > maxit) {  // everything that can run has been enqueued
+            CU(cudaEventSynchronize(ctx->ev[c & 1]));
+            finished = true;
+            break;
+        }
+        if (c > 0) {
+            CU(cudaEventSynchronize(ctx->ev[(c - 1) & 1]));
+            if (ctx->host_state[(c - 1) & 1].done) finished = true;
+        }
+        ++c;
+    }
+    LAUNCH(launch_cg_finish(ctx->dm, v, s));
+    CU(cudaMemcpyAsync(&ctx->host_state[0], v.st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    const CgState &hs = ctx->host_state[0];
+    if (!hs.done) return fail(ctx, SEM_ECUDA, "sem_cg: device did not reach a stopping decision");
+    if (ctx->prof) prof_fold(ctx, hs.iters);
+    if (iters) *iters = hs.iters;
+    if (rel_res) *rel_res = hs.rel_res;
+    if (!hs.converged && tol > 0.0) {
+        fail(ctx, SEM_ENOCONV, "sem_cg: maxit=%d reached, rel_res=%.3e > tol=%.3e", maxit, hs.rel_res, tol);
+        return SEM_ENOCONV;
+    }
+    return SEM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// profiling (benchmark roofline)
+// ---------------------------------------------------------------------------
+extern "C" int sem_profile(sem_ctx *ctx, int enable) {
+    CHECK_CTX();
+    if (!ctx->recs.empty()) {
+        CU(cudaStreamSynchronize(ctx->stream));
+        prof_fold(ctx, -1);
+    }
+    ctx->prof = enable != 0;
+    for (int c = 0; c < kProfClasses; ++c) {
+        ctx->prof_ms[c] = 0.0;
+        ctx->prof_bytes[c] = 0.0;
+        ctx->prof_n[c] = 0;
+    }
+    return SEM_OK;
+}
+
+extern "C" int sem_profile_read(sem_ctx *ctx, int which, double *ms, int64_t *launches,
+                                double *bytes) {
+    CHECK_CTX();
+    if (which < 0 || which >= kProfClasses) return fail(ctx, SEM_EINVAL, "bad kernel class");
+    if (!ctx->recs.empty()) {
+        CU(cudaStreamSynchronize(ctx->stream));
+        prof_fold(ctx, -1);
+    }
+    if (ms) *ms = ctx->prof_ms[which];
+    if (launches) *launches = ctx->prof_n[which];
+    if (bytes) *bytes = ctx->prof_bytes[which];
+    return SEM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// errors / version
+// ---------------------------------------------------------------------------
+extern "C" const char *sem_strerror(int code) {
+    switch (code) {
+    case SEM_OK: return "SEM_OK";
+    case SEM_EINVAL: return "SEM_EINVAL: invalid argument or mesh";
+    case SEM_ECUDA: return "SEM_ECUDA: CUDA runtime failure";
+    case SEM_ENCCL: return "SEM_ENCCL: NCCL failure";
+    case SEM_ENOCONV: return "SEM_ENOCONV: maxit reached before tol";
+    case SEM_ESTATE: return "SEM_ESTATE: bad context state";
+    default: return "unknown status";
+    }
+}
+
+extern "C" const char *sem_last_error(const sem_ctx *ctx) {
+    if (ctx && !ctx->err.empty()) return ctx->err.c_str();
+    return g_err.c_str();
+}
+
+extern "C" const char *sem_version(void) { return "libsem 0.1 (sm_100a, fp64)"; }

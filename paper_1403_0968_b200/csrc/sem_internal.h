@@ -1,0 +1,74 @@
+// sem_internal.h -- internal types shared by the host orchestration
+// (sem_host.cpp) and the sm_100a kernels (sem_kernels.cu).  Not part of the ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sem {
+
+constexpr int kRing = 4;        // scalar ring depth (iteration k uses slot k & 3)
+constexpr int kMaxRanks = 64;
+
+// Device-resident CG state (one per context, in the workspace).
+struct CgState {
+    double rho0;                // (r0, r0)_c, written by K1 at k = 0
+    double tol;
+    int32_t maxit;
+    int32_t done;               // sticky: 1 once the stopping rule fired
+    int32_t iters;              // iteration count at which it fired
+    int32_t converged;          // 1 if sqrt(rho) <= tol sqrt(rho0) (or rho0 == 0)
+    double rel_res;             // sqrt(rho_k / rho0)
+    double alpha[kRing];        // alpha_k in slot k & 3
+    uint32_t ticket[4];         // last-block-done counters: 0 = gs/pap, 1 = rr
+};
+
+// Everything a kernel needs to know about the discretisation on this rank.
+struct DevMesh {
+    int N, n, n3;
+    int64_t E, L;
+    const double *D;            // [n][n] row-major, D[i*n+m] = phi'_m(xi_i)
+    const double *G;            // [E][6][n3] rr rs rt ss st tt (w J folded in)
+    const double *BM;           // [L] lumped mass w_i w_j w_k J
+    // gather-scatter plan over element-SURFACE nodes: groups of local copies of
+    // one global id, Dirichlet groups first ([0, ndir)), copies in ascending
+    // local order.
+    const int32_t *gs_off;      // [ngroups + 1]
+    const int32_t *gs_idx;      // [nsurf]
+    int32_t ngroups, ndir, nsurf;
+    const uint32_t *owner;      // [ceil(L/32)] bit l: this copy counts once in (.,.)_c
+    int rank, nranks;
+};
+
+struct CgVecs {
+    const double *b;
+    double *x, *r, *p, *w;
+    double *partials;           // [kPartialCap] per-block partial sums
+    double *rr_all;             // [kRing][nranks] rank partials of (r,r)_c
+    double *pap_all;            // [kRing][nranks] rank partials of (w,p)_c
+    CgState *st;
+};
+
+constexpr int kRrBlocks = 148 * 4;     // grid of the r-update / (r,r) kernel
+constexpr int kRrThreads = 256;
+constexpr int kGsThreads = 256;
+
+// ---- launchers (sem_kernels.cu); all return cudaGetLastError() ----
+int ax_blocks(int N, int64_t E);      // grid size of the Ax kernels for E elements
+cudaError_t launch_geom(const DevMesh &m, const double *xyz, double *G, double *BM,
+                        int *bad, cudaStream_t s);
+cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t s);
+cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, int k, cudaStream_t s);
+// mode: 0 = plain dssum, 1 = dssum + mask, 2 = dssum + mask + (w,p) partial +
+// last-block reduction into pap_all[k & 3][rank] (also folds the Ax partials)
+cudaError_t launch_gs(const DevMesh &m, double *w, int mode, const CgVecs *v, int k,
+                      int nb_ax, cudaStream_t s);
+cudaError_t launch_mask(const DevMesh &m, double *w, cudaStream_t s);
+cudaError_t launch_mass(const DevMesh &m, const double *f, double *b, cudaStream_t s);
+cudaError_t launch_cg_init(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+// update: r -= alpha_k w then (r,r)_c partial into rr_all[(k+1) & 3][rank];
+// !update (init): (r,r)_c of r into rr_all[0][rank]
+cudaError_t launch_rr(const DevMesh &m, const CgVecs &v, int k, bool update, cudaStream_t s);
+cudaError_t launch_cg_finish(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+
+}  // namespace sem

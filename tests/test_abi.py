@@ -1,0 +1,160 @@
+"""CPU-side checks of the C ABI (no GPU): libsem.so loads, exports every entry
+point include/sem.h declares, host-only calls work, and setup rejects
+malformed meshes before touching the GPU."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1403_0968_b200 import meshgen, sem
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    names = set()
+    for fn in os.listdir(os.path.join(ROOT, "include")):
+        if not fn.endswith(".h"):
+            continue
+        src = open(os.path.join(ROOT, "include", fn)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for mm in re.finditer(r"^[A-Za-z_][\w\s\*]*?\b(sem_\w+)\s*\(", src, flags=re.M):
+            names.add(mm.group(1))
+    return names
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_1403_0968_b200 import _build
+    _build.build()
+    return sem.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    names = declared_functions()
+    assert {"sem_setup", "sem_ax", "sem_dssum", "sem_cg", "sem_mask", "sem_free"} <= names
+    for nm in sorted(names):
+        assert hasattr(L, nm), f"libsem.so does not export {nm}"
+    assert set(sem.EXPORTS) >= names
+    assert b"sm_100a" in L.sem_version()
+
+
+def test_cuda_objects_target_sm100a(L):
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", sem.LIB_PATH], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_library_gll_matches_closed_forms_and_oracle(L, oracle):
+    for N in range(1, 16):
+        xi, w = sem.gll(N)
+        xo, wo = oracle.gll(N)
+        np.testing.assert_allclose(xi, xo, rtol=0, atol=2e-15)
+        np.testing.assert_allclose(w, wo, rtol=0, atol=2e-15)
+        assert abs(w.sum() - 2.0) < 1e-14
+    xi, w = sem.gll(4)
+    np.testing.assert_allclose(xi, [-1, -np.sqrt(3 / 7), 0, np.sqrt(3 / 7), 1], atol=1e-16)
+    np.testing.assert_allclose(w, [0.1, 49 / 90, 32 / 45, 49 / 90, 0.1], atol=3e-16)
+
+
+def test_gll_rejects_bad_order(L):
+    with pytest.raises(sem.SemError) as ei:
+        sem.gll(0)
+    assert ei.value.code == sem.SEM_EINVAL
+
+
+def _mesh_struct(m, nranks=1):
+    s = sem.SemMesh()
+    s.nelem = m.nelem
+    s.xyz = m.xyz.ctypes.data
+    s.glo = m.glo.ctypes.data
+    s.dirichlet = m.dirichlet.ctypes.data
+    s.rank, s.nranks = 0, nranks
+    s.allgather = sem.ALLGATHER_FN()
+    return s
+
+
+def test_workspace_bytes_and_validation(L):
+    N = 7
+    xi, _ = sem.gll(N)
+    m = meshgen.box_mesh(N, xi, elems=(16, 16, 16))
+    s = _mesh_struct(m)
+    nb = ctypes.c_size_t(0)
+    assert L.sem_workspace_bytes(ctypes.byref(s), N, ctypes.byref(nb)) == 0
+    Lloc = m.nlocal
+    # G (6L) + B (L) + r, p, w (3L) doubles dominate
+    assert 80 * Lloc <= nb.value <= 100 * Lloc
+    assert L.sem_workspace_bytes(ctypes.byref(s), 0, ctypes.byref(nb)) == sem.SEM_EINVAL
+    assert L.sem_workspace_bytes(ctypes.byref(s), 16, ctypes.byref(nb)) == sem.SEM_EINVAL
+    s.nelem = 0
+    assert L.sem_workspace_bytes(ctypes.byref(s), N, ctypes.byref(nb)) == sem.SEM_EINVAL
+
+
+def _setup_rc(L, m, N):
+    s = _mesh_struct(m)
+    ws = ctypes.create_string_buffer(1024)  # never reached: validation fails first
+    ctx = ctypes.c_void_p()
+    nb = ctypes.c_size_t(0)
+    L.sem_workspace_bytes(ctypes.byref(s), N, ctypes.byref(nb))
+    rc = L.sem_setup(ctypes.byref(s), N, ctypes.c_void_p(256), nb.value, None, ctypes.byref(ctx))
+    return rc, L.sem_last_error(None).decode()
+
+
+def test_setup_rejects_malformed_meshes(L):
+    N = 3
+    xi, _ = sem.gll(N)
+    m = meshgen.box_mesh(N, xi, elems=(2, 2, 1))
+    # inconsistent Dirichlet flag on one copy of a shared node
+    bad = meshgen.box_mesh(N, xi, elems=(2, 2, 1))
+    g = bad.glo.reshape(-1)
+    ids, cnt = np.unique(g, return_counts=True)
+    shared = ids[cnt > 1][0]
+    first = np.nonzero(g == shared)[0][0]
+    bad.dirichlet.reshape(-1)[first] ^= 1
+    rc, msg = _setup_rc(L, bad, N)
+    assert rc == sem.SEM_EINVAL and "Dirichlet" in msg
+    # an element-interior node shared between two elements
+    bad2 = meshgen.box_mesh(N, xi, elems=(2, 2, 1))
+    n = N + 1
+    q_int = 1 + n + n * n
+    bad2.glo[1, q_int] = bad2.glo[0, q_int]
+    rc, msg = _setup_rc(L, bad2, N)
+    assert rc == sem.SEM_EINVAL and "interior" in msg
+    # negative id
+    bad3 = meshgen.box_mesh(N, xi, elems=(2, 2, 1))
+    bad3.glo[0, 0] = -5
+    rc, msg = _setup_rc(L, bad3, N)
+    assert rc == sem.SEM_EINVAL
+    # misaligned workspace
+    s = _mesh_struct(m)
+    ctx = ctypes.c_void_p()
+    assert L.sem_setup(ctypes.byref(s), N, ctypes.c_void_p(8), 1 << 30, None,
+                       ctypes.byref(ctx)) == sem.SEM_EINVAL
+
+
+def test_null_context_calls(L):
+    assert L.sem_ax(None, None, None) == sem.SEM_ESTATE
+    assert L.sem_dssum(None, None) == sem.SEM_ESTATE
+    assert L.sem_cg(None, None, None, 1e-8, 10, None, None) == sem.SEM_ESTATE
+    assert L.sem_launch_count(None) == -1
+    L.sem_free(None)
+    for c in range(6):
+        assert L.sem_strerror(c)
+
+
+def test_nccl_id_host_call(L):
+    assert L.sem_nccl_id_bytes() == 128
+
+
+def test_no_cpu_fallback_without_gpu(L):
+    """On a box without a GPU the product path must fail loudly."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    N = 2
+    xi, _ = sem.gll(N)
+    m = meshgen.box_mesh(N, xi, elems=(1, 1, 1))
+    with pytest.raises(Exception):
+        sem.Context(m, N, device=0)
