@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""Benchmark of the SEM Poisson hot path (arXiv 1403.0968) on B200.
+
+One STEP = one full CG solve (Ax + DSSUM + mask + fused CG vector updates and
+dot products) to rel. tol 1e-8 from x0 = 0 on config c3:
+4096 hexahedra (16^3) of order N=7 per GPU, eps=0.05 deformed box, manufactured
+sin right-hand side.  N GPUs = weak scaling (c5): each rank owns a 16^3-element
+unit cube of the global box, ranks exchange interface partial sums over NCCL.
+
+value = CG GDOF/s = (local DOF on all ranks) x (CG iterations) / time / 1e9,
+with local DOF = E (N+1)^3 (SURVEY.md reading G13).  The line also carries CG
+iterations/s, the Ax-only GDOF/s, the roofline of the dominant kernel, an
+end-to-end number through the public API with host buffers, the plain-C oracle
+timed on a bounded sample of the same workload, and SM clocks under load.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "Ax GDOF/s and % of HBM roofline; CG iterations/s at 1/2/4/8 B200"
+L2_BYTES = 126 * 2 ** 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["sem", "reference"], default="sem")
+    ap.add_argument("--N", type=int, default=7)
+    ap.add_argument("--elems", type=int, nargs=3, default=[16, 16, 16], help="elements per rank")
+    ap.add_argument("--eps", type=float, default=0.05)
+    ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--maxit", type=int, default=5000)
+    ap.add_argument("--ax-reps", type=int, default=200)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-its", type=int, default=100,
+                    help="oracle CG iterations timed for cpu_baseline (bounded sample)")
+    ap.add_argument("--ref-its", type=int, default=3,
+                    help="oracle CG iterations per --impl reference step")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    --set full summary (profiles/ncu_summary_*.json), or None."""
+    d = os.path.join(ROOT, "profiles")
+    if not os.path.isdir(d):
+        return None
+    files = sorted(f for f in os.listdir(d) if f.startswith("ncu_summary") and f.endswith(".json"))
+    if not files:
+        return None
+    try:
+        s = json.load(open(os.path.join(d, files[-1])))
+        return s.get("dominant", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_info():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def rank_mesh(args, rank, world, r1d):
+    from paper_1403_0968_b200 import meshgen
+    parts = meshgen.default_parts(world)
+    elems = tuple(e * p for e, p in zip(args.elems, parts))
+    lengths = tuple(float(p) for p in parts)
+    return meshgen.box_mesh(args.N, r1d, elems=elems, lengths=lengths, eps=args.eps,
+                            parts=parts, rank=rank, boundary_first=world > 1), parts
+
+
+def workload_name(args, world):
+    E = args.elems[0] * args.elems[1] * args.elems[2]
+    return (f"c3/c5: {E} hex elements ({'x'.join(map(str, args.elems))}) of order N={args.N} "
+            f"per GPU, eps={args.eps} deformed box, full CG to {args.tol:g} from x0=0")
+
+
+def oracle_sample(args, its_per_call, calls):
+    """Time the plain-C oracle's CG (tol = 0, fixed iterations) on rank 0's c3
+    mesh.  Returns (seconds per call list, L)."""
+    import oracle
+    from paper_1403_0968_b200 import meshgen
+    xi, _ = oracle.gll(args.N)
+    m, _ = rank_mesh(args, 0, 1, xi)
+    G, J = oracle.geom(args.N, m.xyz)
+    _, f = meshgen.manufactured(m)
+    b = oracle.mass_rhs(args.N, m.glo, m.dirichlet, J, f)
+    times = []
+    for _ in range(calls):
+        t0 = time.perf_counter()
+        oracle.cg(args.N, m.glo, m.dirichlet, G, b, tol=0.0, maxit=its_per_call)
+        times.append(time.perf_counter() - t0)
+    return times, m.nlocal
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    steps, warm = args.steps, args.warmup
+    times, L = oracle_sample(args, args.ref_its, steps + warm)
+    t = sum(times[warm:])
+    value = L * args.ref_its * steps / t / 1e9
+    sample = (f"oracle (plain C, 1 thread) CG, {args.ref_its} iterations (tol=0) per step on the "
+              f"c3 mesh of rank 0 ({L} local DOF); setup untimed")
+    out = {"metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": steps,
+           "warmup": warm, "ms_per_step": 1e3 * t / steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": workload_name(args, world), "N": args.N,
+                      "elements_per_gpu": args.elems[0] * args.elems[1] * args.elems[2]},
+           "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": 1, "kind": "oracle",
+                            "sample": sample, "cpu": cpu_info()},
+           "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1403_0968_b200 import meshgen, sem
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    xi, _ = sem.gll(args.N)
+    m, parts = rank_mesh(args, rank, world, xi)
+    ctx = sem.Context(m, args.N, device=local_rank, group=group)
+    L = ctx.nlocal
+    L_all = L * world
+    _, f = meshgen.manufactured(m)
+    b = ctx.rhs(torch.from_numpy(f).to(dev))
+    x = torch.zeros_like(b)
+    stream = torch.cuda.current_stream()
+
+    # ---- warm-up ----
+    its = None
+    for _ in range(max(args.warmup, 1)):
+        x.zero_()
+        _, its, rel, ok = ctx.cg(b, x, tol=args.tol, maxit=args.maxit)
+    assert ok, f"CG did not converge: rel_res={rel}"
+
+    # ---- timed region: K full CG solves, inputs resident in HBM ----
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    launches0 = ctx.launch_count
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    iters = []
+    for _ in range(args.steps):
+        x.zero_()
+        _, it, rel, ok = ctx.cg(b, x, tol=args.tol, maxit=args.maxit)
+        iters.append(it)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    gpu_launches = ctx.launch_count - launches0
+    clocks = sampler.stop()
+    assert len(set(iters)) == 1, f"non-deterministic iteration counts {iters}"
+    its = iters[0]
+    t = ms / 1e3
+    value = L_all * its * args.steps / t / 1e9
+    cg_its_per_s = its * args.steps / t
+
+    # ---- per-kernel device time: the same solves again, each launch bracketed
+    # by CUDA events on the library stream (kept out of the timed region) ----
+    prof_steps = max(1, min(3, args.steps))
+    ctx.profile(True)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(prof_steps):
+        x.zero_()
+        ctx.cg(b, x, tol=args.tol, maxit=args.maxit)
+    p1.record(stream)
+    torch.cuda.synchronize()
+    prof_ms = p0.elapsed_time(p1)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+
+    # dominant kernel roofline (K1 = fused CG Ax kernel), algorithmic bytes
+    peak, peak_src = peaks()
+    k1_ms, k1_n, k1_bytes = prof["ax_cg"]
+    achieved = (k1_bytes / k1_n) / (k1_ms / k1_n / 1e3) / 1e9 if k1_n else None
+    traffic = ncu_traffic()
+    shares = {k: v[0] / prof_ms for k, v in prof.items() if v[1]}
+
+    # ---- Ax alone on the same mesh (64 B/node), for the Ax GDOF/s metric ----
+    u = torch.from_numpy(meshgen.random_field(L, 0)).to(dev)
+    w = torch.empty_like(u)
+    for _ in range(5):
+        ctx.ax(u, w)
+    ctx.profile(True)
+    torch.cuda.synchronize()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(args.ax_reps):
+        ctx.ax(u, w)
+    a1.record(stream)
+    torch.cuda.synchronize()
+    ax_ms = max_over_ranks(a0.elapsed_time(a1)) / args.ax_reps
+    pa = ctx.profile_read()["ax"]
+    ctx.profile(False)
+    ax_kernel_ms = pa[0] / pa[1]
+    ax = {"gdof_s": L_all / (ax_ms / 1e3) / 1e9, "ms_per_apply": ax_ms,
+          "kernel_ms": ax_kernel_ms,
+          "achieved_gbs": 64.0 * L / (ax_kernel_ms / 1e3) / 1e9,
+          "frac": 64.0 * L / (ax_kernel_ms / 1e3) / 1e9 / peak,
+          "gflops": (12 * (args.N + 1) ** 4 + 15 * (args.N + 1) ** 3) * (L / (args.N + 1) ** 3)
+          / (ax_kernel_ms / 1e3) / 1e9,
+          "bytes_per_apply": 64 * L,
+          "l2_note": "working set 64 B/node; at c3 (134 MB) partly L2-resident"}
+
+    # ---- end to end through the public API with host buffers ----
+    b_host = b.cpu().pin_memory()
+    x_host = torch.empty_like(b_host).pin_memory()
+    b_dev = torch.empty_like(b)
+    for _ in range(2):
+        b_dev.copy_(b_host, non_blocking=True)
+        x.zero_()
+        ctx.cg(b_dev, x, tol=args.tol, maxit=args.maxit)
+        x_host.copy_(x, non_blocking=True)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0.record(stream)
+    e2e_steps = max(1, min(args.steps, 10))
+    for _ in range(e2e_steps):
+        b_dev.copy_(b_host, non_blocking=True)
+        x.zero_()
+        _, it2, _, _ = ctx.cg(b_dev, x, tol=args.tol, maxit=args.maxit)
+        x_host.copy_(x, non_blocking=True)
+    h1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(h0.elapsed_time(h1))
+    e2e = {"value": L_all * it2 * e2e_steps / (e2e_ms / 1e3) / 1e9, "unit": "GDOF/s",
+           "h2d_bytes_per_step": 8 * L, "d2h_bytes_per_step": 8 * L,
+           "ms_per_step": e2e_ms / e2e_steps}
+
+    # ---- oracle on the host cores (rank 0, N=1 only), bounded sample ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        times, Lc = oracle_sample(args, args.cpu_its, 1)
+        cpu = {"value": Lc * args.cpu_its / times[0] / 1e9, "unit": "GDOF/s", "cores": 1,
+               "kind": "oracle", "cpu": cpu_info(),
+               "sample": f"plain-C oracle CG, {args.cpu_its} iterations (tol=0) on the same c3 "
+                         f"mesh ({Lc} local DOF), 1 thread, {times[0]:.1f} s; setup untimed"}
+
+    if rank == 0:
+        ws = 16 * L + ctx.workspace.numel()
+        out = {
+            "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded deformed-box mesh, manufactured sin RHS)",
+            "cg_iters_per_s": cg_its_per_s,
+            "config": {"workload": workload_name(args, world), "N": args.N,
+                       "elements_per_gpu": m.nelem, "local_dof_per_gpu": L,
+                       "unique_dof_total": ctx.nglobal, "cg_iters": its, "tol": args.tol,
+                       "partition": "x".join(map(str, parts)),
+                       "parallelism": f"element partition over {world} GPU(s)",
+                       "l2": f"inputs larger than L2: {ws / 2**20:.0f} MiB resident working set "
+                             f"> {L2_BYTES / 2**20:.0f} MiB L2, streamed every iteration"},
+            "ax": ax,
+            "roofline": {"bound": "hbm", "kernel": "K1: ax_tma_kernel<N,CG=true> (fused x/p update + Ax + interior (w,p))",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if achieved else None, "traffic": traffic,
+                         "peak_source": peak_src,
+                         "bytes_per_node": "96 (x,r,p,G read; x,p,w write), 72 at k=0",
+                         "launches": k1_n, "avg_launch_us": 1e3 * k1_ms / k1_n if k1_n else None,
+                         "step_share": shares,
+                         "timing": f"CUDA events around every launch on the library stream over "
+                                   f"{prof_steps} extra solves after the timed region"},
+            "gpu_launches": gpu_launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+        }
+        print(json.dumps(out), flush=True)
+    ctx.free()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,460 @@
+// ax_tma.cu -- TMA-pipelined, persistent sm_100a kernel for the local stiffness
+// apply w = A_L u (eq:semOperator) and its fused CG variant
+// K1 (x += alpha_{k-1} p_{k-1}; p = r + beta_k p_{k-1}; w = A_L p; (w,p) over
+// element-interior nodes).  Used for N <= kTmaMaxN; larger N use ax_kernel.
+//
+// Design:
+//  * one CTA per SM (persistent); the CTA holds NG independent "groups" of GT
+//    threads; a group works on a UNIT of EPG consecutive elements at a time,
+//    thread (i,j) of element el owning the k-column of nodes (i,j,0..N).
+//  * every group double-buffers its units in shared memory: the group leader
+//    issues 1-D bulk copies (cp.async.bulk, TMA engine) of the unit's input
+//    vectors and its six geometric-factor blocks, completing on an mbarrier
+//    with expect_tx; while the group computes unit t, unit t+1 is in flight.
+//    G^ is streamed exactly once (L2 evict_first policy); nothing is re-read.
+//  * sum factorisation: u_r and u_s from the k-slice in shared memory (D rows
+//    of the thread in registers), u_t from the register column with D in
+//    constant memory (uniform index -> constant-bank operand); f_r, f_s are
+//    written over the thread's own (already consumed) G^ slots, f_t stays in
+//    registers; the transposed contraction reads f_r, f_s after one group
+//    barrier.  FP64 FMA throughout.
+#include <cstdio>
+
+#include "sem_internal.h"
+
+namespace sem {
+
+// ---------------------------------------------------------------------------
+// D in constant memory, one block per order N (values depend on N only).
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int d_off(int N) {
+    int o = 0;
+    for (int q = 1; q < N; ++q) o += (q + 1) * (q + 1);
+    return o;
+}
+constexpr int kDConstTotal = d_off(16);
+__constant__ double c_D[kDConstTotal];
+
+cudaError_t upload_const_D(int N, const double *D_host) {
+    return cudaMemcpyToSymbol(c_D, D_host, sizeof(double) * (N + 1) * (N + 1),
+                              sizeof(double) * d_off(N), cudaMemcpyHostToDevice);
+}
+
+// ---------------------------------------------------------------------------
+// per-N configuration
+// ---------------------------------------------------------------------------
+template <int N>
+struct TmaCfg {
+    static constexpr int n = N + 1, n2 = n * n, n3 = n2 * n;
+    // elements per unit (packs small elements into ~64-128 threads)
+    static constexpr int EPG = (N == 1) ? 16 : (N == 2) ? 7 : (N == 3) ? 4 : (N == 4) ? 5
+                             : (N == 5) ? 3 : (N == 6) ? 2 : 1;
+    static constexpr int GT = ((EPG * n2 + 31) / 32) * 32;   // threads per group
+    static constexpr int VL = ((EPG * n3 + 2 + 1) / 2) * 2;  // vector slot (doubles)
+};
+
+template <int N, bool CG>
+struct TmaLayout {
+    using C = TmaCfg<N>;
+    static constexpr int NV = CG ? 3 : 1;                           // r,p,x | u
+    static constexpr int STAGE = NV * C::VL + 6 * C::EPG * C::n3;   // doubles
+    static constexpr int SMEM_MAX = 227 * 1024 - 1024;
+    static constexpr int NG_FIT = SMEM_MAX / (2 * STAGE * 8);
+    static constexpr int NG = NG_FIT > 4 ? 4 : NG_FIT;              // groups per CTA
+    static constexpr int NT = NG * C::GT;
+    static constexpr size_t SMEM = size_t(NG) * 2 * STAGE * 8 + 128;
+};
+
+// ---------------------------------------------------------------------------
+// PTX helpers (mbarrier + bulk copy)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void group_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// 16-byte aligned superset [a0, a1) (in doubles) of the E-vector range
+// [first, first + nd) for a bulk copy; element data then starts at smem slot
+// + (first - a0).  When the superset would run past the end L of the caller's
+// buffer, a1 is pulled back and the last double(s) are copied by plain loads
+// (no over-read).
+struct VecRange {
+    int64_t a0, a1;
+};
+__device__ __forceinline__ VecRange vec_range(int64_t first, int64_t nd, int64_t L) {
+    VecRange r;
+    r.a0 = first & ~int64_t(1);
+    r.a1 = (first + nd + 1) & ~int64_t(1);
+    if (r.a1 > L) r.a1 -= 2;
+    return r;
+}
+
+struct TmaArgs {
+    int64_t E;
+    const double *G;
+    // plain: u -> w.  CG: r, p (in/out), x (in/out) -> w
+    const double *u;
+    const double *r;
+    double *p, *x, *w;
+    double *partials;
+    const double *rr_all;
+    CgState *st;
+    int k, nranks;
+};
+
+template <int N, bool CG>
+__global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs a) {
+    using C = TmaCfg<N>;
+    using Lo = TmaLayout<N, CG>;
+    constexpr int n = C::n, n2 = C::n2, n3 = C::n3, EPG = C::EPG, GT = C::GT, VL = C::VL;
+    constexpr int NG = Lo::NG, NV = Lo::NV, STAGE = Lo::STAGE;
+    constexpr int DO = d_off(N);
+    extern __shared__ __align__(128) double smem[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + size_t(NG) * 2 * STAGE);  // [NG][2]
+    __shared__ double sred[(Lo::NT + 31) / 32];
+
+    // ---- CG prologue: stopping rule, beta, alpha_prev (uniform) ----
+    double beta = 0.0, alpha_prev = 0.0;
+    if constexpr (CG) {
+        CgState *st = a.st;
+        if (*(volatile int32_t *)&st->done) return;
+        const int k = a.k;
+        double rho = 0.0;
+        for (int q = 0; q < a.nranks; ++q) rho += __ldcg(a.rr_all + (k & 3) * a.nranks + q);
+        const double rho0 = (k == 0) ? rho : st->rho0;
+        bool done;
+        if (k == 0 && rho0 == 0.0) done = true;
+        else done = !(k < st->maxit && sqrt(rho) > st->tol * sqrt(rho0));
+        if (done) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                st->rho0 = rho0;
+                st->iters = k;
+                st->rel_res = (rho0 == 0.0) ? 0.0 : sqrt(rho) / sqrt(rho0);
+                st->converged = (rho0 == 0.0) || !(sqrt(rho) > st->tol * sqrt(rho0));
+                __threadfence();
+                st->done = 1;
+            }
+            return;
+        }
+        if (k == 0) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) st->rho0 = rho0;
+        } else {
+            double rho_old = 0.0;
+            for (int q = 0; q < a.nranks; ++q)
+                rho_old += __ldcg(a.rr_all + ((k - 1) & 3) * a.nranks + q);
+            beta = rho / rho_old;
+            alpha_prev = st->alpha[(k - 1) & 3];
+        }
+    }
+
+    const int tid = threadIdx.x;
+    const int g = tid / GT;                 // group
+    const int gt = tid - g * GT;            // thread in group
+    const int el = gt / n2;                 // element within unit
+    const int ij = gt - el * n2;
+    const int i = ij % n, j = ij / n;
+    const bool lane_on = el < EPG;
+    const bool leader = (gt == 0);
+    double *stage0 = smem + size_t(g) * 2 * STAGE;
+    uint64_t *gbar = bars + 2 * g;
+
+    const int64_t nunits = (a.E + EPG - 1) / EPG;
+    const int64_t TG = int64_t(gridDim.x) * NG;
+    const int64_t u0 = int64_t(blockIdx.x) * NG + g;
+    const int64_t L = a.E * n3;
+
+    if (leader) {
+        mbar_init(gbar + 0, 1);
+        mbar_init(gbar + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const uint64_t pol_g = policy_evict_first();
+    const uint64_t pol_v = CG ? policy_evict_last() : policy_evict_first();
+    int shift_s[2] = {0, 0};
+
+    // Leader: issue the copies of unit `unit` into stage s.  Plain-load tails
+    // are stored BEFORE the mbarrier arrive (release), the bulk copies after
+    // expect_tx; the group observes all of it through the mbarrier phase.
+    auto issue_unit = [&](int64_t unit, int s) {
+        double *sb = stage0 + size_t(s) * STAGE;
+        const int64_t e0 = unit * EPG;
+        const int64_t ne = (a.E - e0 < EPG) ? (a.E - e0) : EPG;
+        const int64_t first = e0 * n3, nd = ne * n3;
+        const VecRange vr = vec_range(first, nd, L);
+        const double *vsrc[3];
+        if constexpr (CG) {
+            vsrc[0] = a.r;
+            vsrc[1] = a.p;
+            vsrc[2] = a.x;
+        } else {
+            vsrc[0] = a.u;
+        }
+        for (int v = 0; v < NV; ++v)
+            for (int64_t q = vr.a1; q < first + nd; ++q) sb[v * VL + (q - vr.a0)] = __ldg(vsrc[v] + q);
+        const uint32_t vb = (uint32_t)((vr.a1 - vr.a0) * 8);
+        const uint32_t gb = (uint32_t)(ne * 6 * n3 * 8);
+        mbar_expect_tx(gbar + s, NV * vb + gb);
+        for (int v = 0; v < NV; ++v) bulk_g2s(sb + v * VL, vsrc[v] + vr.a0, vb, gbar + s, pol_v);
+        bulk_g2s(sb + NV * VL, a.G + e0 * 6 * n3, gb, gbar + s, pol_g);
+    };
+
+    if (leader) {
+        if (u0 < nunits) issue_unit(u0, 0);
+        if (u0 + TG < nunits) issue_unit(u0 + TG, 1);
+    }
+
+    // thread-varying D entries in registers
+    double Dri[n], Drj[n], Dci[n], Dcj[n];
+#pragma unroll
+    for (int m = 0; m < n; ++m) {
+        Dri[m] = c_D[DO + i * n + m];
+        Drj[m] = c_D[DO + j * n + m];
+        Dci[m] = c_D[DO + m * n + i];
+        Dcj[m] = c_D[DO + m * n + j];
+    }
+
+    double pap = 0.0;
+    int t = 0;
+    for (int64_t unit = u0; unit < nunits; unit += TG, ++t) {
+        const int s = t & 1;
+        double *sb = stage0 + size_t(s) * STAGE;
+        const int64_t e0 = unit * EPG;
+        const int64_t e = e0 + el;
+        const bool on = lane_on && (e < a.E);
+        const int sh = (int)((e0 * n3) & 1);  // element data offset in each vector slot
+        mbar_wait(gbar + s, (t >> 1) & 1);
+
+        double *su;     // Ax input in smem (u, or p after the CG update)
+        double col[n];  // input column (i,j,0..N)
+        const int64_t gbase = e * n3 + ij;
+        if constexpr (CG) {
+            double *sr = sb + 0 * VL + sh + el * n3;
+            double *sp = sb + 1 * VL + sh + el * n3;
+            double *sx = sb + 2 * VL + sh + el * n3;
+            su = sp;
+            if (on) {
+#pragma unroll
+                for (int k = 0; k < n; ++k) {
+                    const int q = k * n2 + ij;
+                    const double rl = sr[q];
+                    double pl;
+                    if (a.k == 0) {
+                        pl = rl;
+                    } else {
+                        const double po = sp[q];
+                        a.x[gbase + k * n2] = sx[q] + alpha_prev * po;
+                        pl = rl + beta * po;
+                    }
+                    sp[q] = pl;
+                    a.p[gbase + k * n2] = pl;
+                    col[k] = pl;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < n; ++k) col[k] = 0.0;
+            }
+            group_bar(1 + g, GT);  // p visible to the group
+        } else {
+            su = sb + sh + el * n3;
+#pragma unroll
+            for (int k = 0; k < n; ++k) col[k] = on ? su[k * n2 + ij] : 0.0;
+        }
+        double *sG = sb + NV * VL + el * 6 * n3;
+
+        // ---- phase A: gradient, geometric factors ----
+        double ft[n];
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+            const double *uk = su + k * n2;
+            double ur = 0.0, us = 0.0, ut = 0.0;
+#pragma unroll
+            for (int m = 0; m < n; ++m) {
+                ur = fma(Dri[m], uk[j * n + m], ur);
+                us = fma(Drj[m], uk[m * n + i], us);
+                ut = fma(c_D[DO + k * n + m], col[m], ut);
+            }
+            const int q = k * n2 + ij;
+            double fr = 0.0, fs = 0.0, f3 = 0.0;
+            if (on) {
+                const double g0 = sG[0 * n3 + q], g1 = sG[1 * n3 + q], g2 = sG[2 * n3 + q];
+                const double g3 = sG[3 * n3 + q], g4 = sG[4 * n3 + q], g5 = sG[5 * n3 + q];
+                fr = g0 * ur + g1 * us + g2 * ut;
+                fs = g1 * ur + g3 * us + g4 * ut;
+                f3 = g2 * ur + g4 * us + g5 * ut;
+                sG[0 * n3 + q] = fr;   // own node's slots, already consumed
+                sG[1 * n3 + q] = fs;
+            }
+            ft[k] = f3;
+        }
+        group_bar(1 + g, GT);
+
+        // ---- phase B: transposed contraction, epilogue ----
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+            const double *frk = sG + 0 * n3 + k * n2;
+            const double *fsk = sG + 1 * n3 + k * n2;
+            double wr = 0.0, ws = 0.0, wt = 0.0;
+#pragma unroll
+            for (int m = 0; m < n; ++m) {
+                wr = fma(Dci[m], frk[j * n + m], wr);
+                ws = fma(Dcj[m], fsk[m * n + i], ws);
+                wt = fma(c_D[DO + m * n + k], ft[m], wt);
+            }
+            const double wv = wr + ws + wt;
+            if (on) {
+                a.w[gbase + k * n2] = wv;
+                if constexpr (CG) {
+                    if (k > 0 && k < N && i > 0 && i < N && j > 0 && j < N) pap = fma(wv, col[k], pap);
+                }
+            }
+        }
+        fence_proxy_async();     // generic smem writes before the next async refill
+        group_bar(1 + g, GT);    // stage s fully consumed
+        if (leader && unit + 2 * TG < nunits) issue_unit(unit + 2 * TG, s);
+    }
+
+    if constexpr (CG) {
+        // deterministic block reduction of the interior (w,p) partial
+        double v = pap;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        __syncthreads();
+        if ((tid & 31) == 0) sred[tid >> 5] = v;
+        __syncthreads();
+        if (tid == 0) {
+            double s = 0.0;
+            for (int q = 0; q < (Lo::NT + 31) / 32; ++q) s += sred[q];
+            a.partials[blockIdx.x] = s;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+#define SEM_TMA_DISPATCH(N_, ...)                                            \
+    switch (N_) {                                                            \
+    case 1: { constexpr int NN = 1; __VA_ARGS__; } break;                           \
+    case 2: { constexpr int NN = 2; __VA_ARGS__; } break;                           \
+    case 3: { constexpr int NN = 3; __VA_ARGS__; } break;                           \
+    case 4: { constexpr int NN = 4; __VA_ARGS__; } break;                           \
+    case 5: { constexpr int NN = 5; __VA_ARGS__; } break;                           \
+    case 6: { constexpr int NN = 6; __VA_ARGS__; } break;                           \
+    case 7: { constexpr int NN = 7; __VA_ARGS__; } break;                           \
+    case 8: { constexpr int NN = 8; __VA_ARGS__; } break;                           \
+    case 9: { constexpr int NN = 9; __VA_ARGS__; } break;                           \
+    case 10: { constexpr int NN = 10; __VA_ARGS__; } break;                         \
+    default: break;                                                          \
+    }
+
+bool tma_supported(int N) { return N >= 1 && N <= kTmaMaxN; }
+
+template <int N, bool CG>
+static int tma_grid(int64_t E, int nsm) {
+    using Lo = TmaLayout<N, CG>;
+    const int64_t nunits = (E + TmaCfg<N>::EPG - 1) / TmaCfg<N>::EPG;
+    int64_t need = (nunits + Lo::NG - 1) / Lo::NG;
+    return (int)(need < nsm ? (need < 1 ? 1 : need) : nsm);
+}
+
+int tma_blocks(int N, int64_t E, int nsm, bool cg) {
+    int nb = 0;
+    if (cg) {
+        SEM_TMA_DISPATCH(N, nb = tma_grid<NN, true>(E, nsm));
+    } else {
+        SEM_TMA_DISPATCH(N, nb = tma_grid<NN, false>(E, nsm));
+    }
+    return nb;
+}
+
+template <int N, bool CG>
+static cudaError_t tma_attr() {
+    using Lo = TmaLayout<N, CG>;
+    static_assert(Lo::NG >= 1, "stage does not fit in shared memory");
+    return cudaFuncSetAttribute(ax_tma_kernel<N, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)Lo::SMEM);
+}
+
+cudaError_t tma_prepare(int N) {
+    cudaError_t e = cudaSuccess;
+    SEM_TMA_DISPATCH(N, (e = tma_attr<NN, false>(), e = (e == cudaSuccess ? tma_attr<NN, true>() : e)));
+    return e;
+}
+
+cudaError_t launch_ax_tma(const DevMesh &m, const double *u, double *w, cudaStream_t s) {
+    TmaArgs a{};
+    a.E = m.E;
+    a.G = m.G;
+    a.u = u;
+    a.w = w;
+    SEM_TMA_DISPATCH(m.N, (ax_tma_kernel<NN, false><<<tma_grid<NN, false>(m.E, m.nsm),
+                                                      TmaLayout<NN, false>::NT,
+                                                      TmaLayout<NN, false>::SMEM, s>>>(a)));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, int k, cudaStream_t s) {
+    TmaArgs a{};
+    a.E = m.E;
+    a.G = m.G;
+    a.r = v.r;
+    a.p = v.p;
+    a.x = v.x;
+    a.w = v.w;
+    a.partials = v.partials;
+    a.rr_all = v.rr_all;
+    a.st = v.st;
+    a.k = k;
+    a.nranks = m.nranks;
+    SEM_TMA_DISPATCH(m.N, (ax_tma_kernel<NN, true><<<tma_grid<NN, true>(m.E, m.nsm),
+                                                     TmaLayout<NN, true>::NT,
+                                                     TmaLayout<NN, true>::SMEM, s>>>(a)));
+    return cudaGetLastError();
+}
+
+}  // namespace sem

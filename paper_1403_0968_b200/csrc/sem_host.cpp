@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -214,7 +215,9 @@ Layout make_layout(int N, int64_t E, int nranks) {
     const int64_t n = N + 1, n3 = n * n * n, L = E * n3;
     const int64_t ni = (n >= 2) ? (n - 2) : 0;
     Lo.nsurf_cap = E * (n3 - ni * ni * ni);
-    const int nb_ax = ax_blocks(N, E);
+    // partial slots for the Ax kernels: simple kernel blocks, or a persistent
+    // TMA grid (<= one CTA per SM, <= E)
+    const int nb_ax = std::max<int>(ax_blocks(N, E), (int)std::min<int64_t>(E, 1024));
     const int64_t nb_gs = (Lo.nsurf_cap + kGsThreads - 1) / kGsThreads + 1;
     Lo.partial_cap = std::max<int64_t>(nb_ax + nb_gs, kRrBlocks) + 16;
     size_t o = 0;
@@ -453,7 +456,14 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
     cv.rr_all = reinterpret_cast<double *>(ws + Lo.rr_all);
     cv.pap_all = reinterpret_cast<double *>(ws + Lo.pap_all);
     cv.st = reinterpret_cast<CgState *>(ws + Lo.st);
-    ctx->nb_ax = ax_blocks(N, ctx->E);
+    {
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, mesh->device);
+        dm.nsm = nsm;
+        const char *impl = getenv("SEM_AX_KERNEL");
+        dm.use_tma = tma_supported(N) && !(impl && strcmp(impl, "simple") == 0);
+    }
+    ctx->nb_ax = dm.use_tma ? tma_blocks(N, ctx->E, dm.nsm, true) : ax_blocks(N, ctx->E);
 
     rc = [&]() -> int {
         const int n = ctx->n;
@@ -463,6 +473,8 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         for (int i = 0; i < n; ++i) Dh[n * n + i] = wq[i];
         cudaStream_t s = ctx->stream;
         CU(cudaHostAlloc(&ctx->host_state, 2 * sizeof(CgState), cudaHostAllocDefault));
+        CU(upload_const_D(N, Dh.data()));
+        if (dm.use_tma) CU(tma_prepare(N));
         CU(cudaEventCreateWithFlags(&ctx->ev[0], cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&ctx->ev[1], cudaEventDisableTiming));
         CU(cudaMemcpyAsync((void *)dm.D, Dh.data(), sizeof(double) * Dh.size(),

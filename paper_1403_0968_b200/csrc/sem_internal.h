@@ -9,6 +9,7 @@ namespace sem {
 
 constexpr int kRing = 4;        // scalar ring depth (iteration k uses slot k & 3)
 constexpr int kMaxRanks = 64;
+constexpr int kTmaMaxN = 10;     // TMA-pipelined Ax kernel for N <= 10
 
 // Device-resident CG state (one per context, in the workspace).
 struct CgState {
@@ -38,6 +39,8 @@ struct DevMesh {
     int32_t ngroups, ndir, nsurf;
     const uint32_t *owner;      // [ceil(L/32)] bit l: this copy counts once in (.,.)_c
     int rank, nranks;
+    int nsm;                    // SM count of the device (persistent grids)
+    bool use_tma;               // TMA-pipelined Ax kernels (N <= kTmaMaxN)
 };
 
 struct CgVecs {
@@ -70,5 +73,13 @@ cudaError_t launch_cg_init(const DevMesh &m, const CgVecs &v, cudaStream_t s);
 // !update (init): (r,r)_c of r into rr_all[0][rank]
 cudaError_t launch_rr(const DevMesh &m, const CgVecs &v, int k, bool update, cudaStream_t s);
 cudaError_t launch_cg_finish(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+
+// ax_tma.cu
+bool tma_supported(int N);
+int tma_blocks(int N, int64_t E, int nsm, bool cg);
+cudaError_t tma_prepare(int N);
+cudaError_t upload_const_D(int N, const double *D_host);
+cudaError_t launch_ax_tma(const DevMesh &m, const double *u, double *w, cudaStream_t s);
+cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, int k, cudaStream_t s);
 
 }  // namespace sem

@@ -459,6 +459,7 @@ cudaError_t launch_geom(const DevMesh &m, const double *xyz, double *G, double *
 
 cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t s) {
     if (m.E == 0) return cudaSuccess;
+    if (m.use_tma) return launch_ax_tma(m, u, w, s);
     AxCgArgs none{};
     SEM_DISPATCH_N(m.N, (ax_kernel<NN, false><<<ax_blocks_t<NN>(m.E), AxCfg<NN>::NT, 0, s>>>(
                              m.E, m.D, m.G, u, w, none)));
@@ -466,6 +467,7 @@ cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t
 }
 
 cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, int k, cudaStream_t s) {
+    if (m.use_tma) return launch_ax_cg_tma(m, v, k, s);
     AxCgArgs a{v.r, v.x, v.p, v.w, v.partials, v.rr_all, v.st, k, m.nranks};
     SEM_DISPATCH_N(m.N, (ax_kernel<NN, true><<<ax_blocks_t<NN>(m.E), AxCfg<NN>::NT, 0, s>>>(
                              m.E, m.D, m.G, nullptr, v.w, a)));

@@ -28,6 +28,14 @@ def relerr(a, b):
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
+@pytest.fixture(params=["tma", "simple"])
+def impl(request, monkeypatch):
+    """Both Ax kernel paths: the TMA-pipelined persistent kernel (N <= 10) and
+    the simple one-block-per-element kernel (all N)."""
+    monkeypatch.setenv("SEM_AX_KERNEL", request.param)
+    return request.param
+
+
 def make(N, elems, eps, **kw):
     from paper_1403_0968_b200 import sem
     xi, _ = oracle.gll(N)
@@ -44,7 +52,7 @@ def T(a, dev):
 # --- Ax -------------------------------------------------------------------
 @pytest.mark.parametrize("N", range(1, 16))
 @pytest.mark.parametrize("eps", [0.0, 0.05])
-def test_ax_parity_all_orders(dev, N, eps):
+def test_ax_parity_all_orders(dev, impl, N, eps):
     # 3x2x1 = 6 elements: several blocks for small N, a ragged last block
     # whenever EPB does not divide 6
     m, G, J, ctx = make(N, (3, 2, 1), eps)
@@ -55,8 +63,9 @@ def test_ax_parity_all_orders(dev, N, eps):
     assert ctx.launch_count >= 4
 
 
-@pytest.mark.parametrize("N,elems", [(7, (8, 8, 8)), (3, (13, 7, 5)), (4, (9, 5, 3))])
-def test_ax_parity_many_elements(dev, N, elems):
+@pytest.mark.parametrize("N,elems", [(7, (8, 8, 8)), (3, (13, 7, 5)), (4, (9, 5, 3)),
+                                     (6, (7, 5, 3)), (2, (11, 9, 7)), (10, (3, 3, 3))])
+def test_ax_parity_many_elements(dev, impl, N, elems):
     m, G, J, ctx = make(N, elems, 0.05)
     u = meshgen.random_field(m.nlocal, 11)
     w = ctx.ax(T(u, dev)).cpu().numpy()
@@ -130,7 +139,7 @@ def _rhs(m, J, kind="sin"):
     return oracle.mass_rhs(m.N, m.glo, m.dirichlet, J, f)
 
 
-def test_cg_c1_twenty_iterations(dev):
+def test_cg_c1_twenty_iterations(dev, impl):
     """config c1: 2x2x2, N=4, 20 CG iterations (tol = 0) -> x_20 <= 1e-10."""
     m, G, J, ctx = make(4, (2, 2, 2), 0.05)
     b = _rhs(m, J)
@@ -145,7 +154,7 @@ def test_cg_c1_twenty_iterations(dev):
     (4, (2, 2, 2), 0.0, "sin"), (4, (2, 2, 2), 0.05, "sin"), (4, (2, 2, 2), 0.05, "rand"),
     (7, (8, 8, 8), 0.05, "sin"), (3, (5, 4, 3), 0.05, "rand"), (2, (3, 3, 3), 0.0, "rand"),
     (9, (2, 3, 2), 0.05, "sin")])
-def test_cg_iteration_parity(dev, N, elems, eps, kind):
+def test_cg_iteration_parity(dev, impl, N, elems, eps, kind):
     m, G, J, ctx = make(N, elems, eps)
     b = _rhs(m, J, kind)
     x, its, rel, ok = ctx.cg(T(b, dev), tol=1e-8, maxit=2000)
@@ -155,7 +164,7 @@ def test_cg_iteration_parity(dev, N, elems, eps, kind):
     assert relerr(x.cpu().numpy(), xr) <= 1e-10
 
 
-def test_cg_edge_cases(dev):
+def test_cg_edge_cases(dev, impl):
     m, G, J, ctx = make(3, (2, 2, 2), 0.05)
     b = _rhs(m, J)
     # zero RHS
