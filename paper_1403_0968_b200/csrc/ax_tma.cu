@@ -20,6 +20,7 @@
 //    barrier.  FP64 FMA throughout.
 #include <cstdio>
 
+#include "cg_device.cuh"
 #include "sem_internal.h"
 
 namespace sem {
@@ -138,11 +139,11 @@ struct TmaArgs {
     // plain: u -> w.  CG: r, p (in/out), x (in/out) -> w
     const double *u;
     const double *r;
-    double *p, *x, *w;
+    double *p, *w;
     double *partials;
     const double *rr_all;
     CgState *st;
-    int k, nranks;
+    int nranks;
 };
 
 template <int N, bool CG>
@@ -158,36 +159,15 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
 
     // ---- CG prologue: stopping rule, beta, alpha_prev (uniform) ----
     double beta = 0.0, alpha_prev = 0.0;
+    int kit = 0;
+    double *xg = nullptr;
     if constexpr (CG) {
-        CgState *st = a.st;
-        if (*(volatile int32_t *)&st->done) return;
-        const int k = a.k;
-        double rho = 0.0;
-        for (int q = 0; q < a.nranks; ++q) rho += __ldcg(a.rr_all + (k & 3) * a.nranks + q);
-        const double rho0 = (k == 0) ? rho : st->rho0;
-        bool done;
-        if (k == 0 && rho0 == 0.0) done = true;
-        else done = !(k < st->maxit && sqrt(rho) > st->tol * sqrt(rho0));
-        if (done) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) {
-                st->rho0 = rho0;
-                st->iters = k;
-                st->rel_res = (rho0 == 0.0) ? 0.0 : sqrt(rho) / sqrt(rho0);
-                st->converged = (rho0 == 0.0) || !(sqrt(rho) > st->tol * sqrt(rho0));
-                __threadfence();
-                st->done = 1;
-            }
-            return;
-        }
-        if (k == 0) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) st->rho0 = rho0;
-        } else {
-            double rho_old = 0.0;
-            for (int q = 0; q < a.nranks; ++q)
-                rho_old += __ldcg(a.rr_all + ((k - 1) & 3) * a.nranks + q);
-            beta = rho / rho_old;
-            alpha_prev = st->alpha[(k - 1) & 3];
-        }
+        const CgStep c = cg_k1_prologue(a.st, a.rr_all, a.nranks);
+        if (c.done) return;
+        beta = c.beta;
+        alpha_prev = c.alpha_prev;
+        kit = c.k;
+        xg = c.x;
     }
 
     const int tid = threadIdx.x;
@@ -215,7 +195,6 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
 
     const uint64_t pol_g = policy_evict_first();
     const uint64_t pol_v = CG ? policy_evict_last() : policy_evict_first();
-    int shift_s[2] = {0, 0};
 
     // Leader: issue the copies of unit `unit` into stage s.  Plain-load tails
     // are stored BEFORE the mbarrier arrive (release), the bulk copies after
@@ -230,7 +209,7 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
         if constexpr (CG) {
             vsrc[0] = a.r;
             vsrc[1] = a.p;
-            vsrc[2] = a.x;
+            vsrc[2] = xg;
         } else {
             vsrc[0] = a.u;
         }
@@ -283,11 +262,11 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
                     const int q = k * n2 + ij;
                     const double rl = sr[q];
                     double pl;
-                    if (a.k == 0) {
+                    if (kit == 0) {
                         pl = rl;
                     } else {
                         const double po = sp[q];
-                        a.x[gbase + k * n2] = sx[q] + alpha_prev * po;
+                        xg[gbase + k * n2] = sx[q] + alpha_prev * po;
                         pl = rl + beta * po;
                     }
                     sp[q] = pl;
@@ -438,18 +417,16 @@ cudaError_t launch_ax_tma(const DevMesh &m, const double *u, double *w, cudaStre
     return cudaGetLastError();
 }
 
-cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, int k, cudaStream_t s) {
+cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
     TmaArgs a{};
     a.E = m.E;
     a.G = m.G;
     a.r = v.r;
     a.p = v.p;
-    a.x = v.x;
     a.w = v.w;
     a.partials = v.partials;
     a.rr_all = v.rr_all;
     a.st = v.st;
-    a.k = k;
     a.nranks = m.nranks;
     SEM_TMA_DISPATCH(m.N, (ax_tma_kernel<NN, true><<<tma_grid<NN, true>(m.E, m.nsm),
                                                      TmaLayout<NN, true>::NT,

@@ -47,7 +47,14 @@ struct sem_ctx {
     int64_t prof_n[kProfClasses] = {0};
     std::string err;
     Comm *comm = nullptr;            // nranks > 1 only
+    // CUDA graph of kChunk CG iterations (captured on first use)
+    bool use_graph = true;
+    cudaStream_t cap_stream = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    int64_t graph_kernels = 0;
 };
+
+static constexpr int kChunk = 8;     // CG iterations per graph launch / poll (multiple of 4)
 
 static thread_local std::string g_err;
 
@@ -204,7 +211,7 @@ static void diff_matrix(int N, const double *x, double *D) {
 // ---------------------------------------------------------------------------
 namespace {
 struct Layout {
-    size_t G, BM, r, p, w, D, gs_off, gs_idx, owner, partials, rr_all, pap_all, st, total;
+    size_t G, BM, r, p, w, D, gs_idx, owner, partials, rr_all, pap_all, st, total;
     int64_t nsurf_cap, partial_cap;
 };
 
@@ -232,7 +239,6 @@ Layout make_layout(int N, int64_t E, int nranks) {
     Lo.p = take(sizeof(double) * L);
     Lo.w = take(sizeof(double) * L);
     Lo.D = take(sizeof(double) * (n * n + n));
-    Lo.gs_off = take(sizeof(int32_t) * (Lo.nsurf_cap + 1));
     Lo.gs_idx = take(sizeof(int32_t) * Lo.nsurf_cap);
     Lo.owner = take(sizeof(uint32_t) * ((L + 31) / 32));
     Lo.partials = take(sizeof(double) * Lo.partial_cap);
@@ -269,7 +275,9 @@ extern "C" int sem_workspace_bytes(const sem_mesh *m, int N, size_t *bytes) {
 // ---------------------------------------------------------------------------
 namespace {
 struct HostPlan {
-    std::vector<int32_t> off, idx;
+    std::vector<int32_t> off, idx;      // CSR: copies of group q = idx[off[q]..off[q+1])
+    std::vector<int32_t> cidx;          // the same copies, class-transposed (device layout)
+    GsClasses cls{};
     int32_t ngroups = 0, ndir = 0;
     std::vector<uint32_t> owner;
     int64_t ndistinct = 0;
@@ -367,6 +375,35 @@ int build_plan(const sem_mesh *m, int N, HostPlan &hp, std::string &err) {
         hp.off[q + 1] = (int32_t)hp.idx.size();
         if (groups[q].d) hp.ndir++;
     }
+    // class layout: runs of equal (dirichlet, multiplicity)
+    hp.cidx.assign(hp.idx.size(), 0);
+    hp.cls.n = 0;
+    {
+        size_t q = 0;
+        int32_t ioff = 0;
+        while (q < groups.size()) {
+            const int m = groups[q].b - groups[q].a;
+            const uint8_t d = groups[q].d;
+            size_t r = q;
+            while (r < groups.size() && groups[r].d == d && groups[r].b - groups[r].a == m) ++r;
+            if (hp.cls.n >= kMaxClasses) {
+                err = "too many distinct (Dirichlet, multiplicity) classes in the mesh";
+                return SEM_EINVAL;
+            }
+            const int c = hp.cls.n++;
+            const int32_t cnt = (int32_t)(r - q);
+            hp.cls.start[c] = (int32_t)q;
+            hp.cls.m[c] = m;
+            hp.cls.dir[c] = d;
+            hp.cls.idxoff[c] = ioff;
+            for (int32_t gq = 0; gq < cnt; ++gq)
+                for (int t = 0; t < m; ++t)
+                    hp.cidx[ioff + (int64_t)t * cnt + gq] = hp.idx[hp.off[q + gq] + t];
+            ioff += cnt * m;
+            q = r;
+        }
+        hp.cls.start[hp.cls.n] = (int32_t)groups.size();
+    }
     // surface ids (for the inter-rank exchange)
     hp.surf_ids.resize(groups.size());
     hp.surf_group.resize(groups.size());
@@ -440,7 +477,7 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
     dm.D = reinterpret_cast<double *>(ws + Lo.D);
     dm.G = reinterpret_cast<double *>(ws + Lo.G);
     dm.BM = reinterpret_cast<double *>(ws + Lo.BM);
-    dm.gs_off = reinterpret_cast<int32_t *>(ws + Lo.gs_off);
+    dm.cls = hp.cls;
     dm.gs_idx = reinterpret_cast<int32_t *>(ws + Lo.gs_idx);
     dm.ngroups = hp.ngroups;
     dm.ndir = hp.ndir;
@@ -462,6 +499,8 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         dm.nsm = nsm;
         const char *impl = getenv("SEM_AX_KERNEL");
         dm.use_tma = tma_supported(N) && !(impl && strcmp(impl, "simple") == 0);
+        const char *gr = getenv("SEM_CG_GRAPH");
+        ctx->use_graph = !(gr && strcmp(gr, "0") == 0);
     }
     ctx->nb_ax = dm.use_tma ? tma_blocks(N, ctx->E, dm.nsm, true) : ax_blocks(N, ctx->E);
 
@@ -479,10 +518,8 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         CU(cudaEventCreateWithFlags(&ctx->ev[1], cudaEventDisableTiming));
         CU(cudaMemcpyAsync((void *)dm.D, Dh.data(), sizeof(double) * Dh.size(),
                            cudaMemcpyHostToDevice, s));
-        CU(cudaMemcpyAsync((void *)dm.gs_off, hp.off.data(), sizeof(int32_t) * hp.off.size(),
-                           cudaMemcpyHostToDevice, s));
-        if (!hp.idx.empty())
-            CU(cudaMemcpyAsync((void *)dm.gs_idx, hp.idx.data(), sizeof(int32_t) * hp.idx.size(),
+        if (!hp.cidx.empty())
+            CU(cudaMemcpyAsync((void *)dm.gs_idx, hp.cidx.data(), sizeof(int32_t) * hp.cidx.size(),
                                cudaMemcpyHostToDevice, s));
         CU(cudaMemcpyAsync((void *)dm.owner, hp.owner.data(), sizeof(uint32_t) * hp.owner.size(),
                            cudaMemcpyHostToDevice, s));
@@ -518,6 +555,8 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
 
 extern "C" void sem_free(sem_ctx *ctx) {
     if (!ctx) return;
+    if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->comm) comm_free(ctx->comm);
     if (ctx->host_state) cudaFreeHost(ctx->host_state);
     for (auto &r : ctx->recs) {
@@ -555,16 +594,15 @@ extern "C" int sem_ax(sem_ctx *ctx, const double *u, double *w) {
     return SEM_OK;
 }
 
-static int dssum_impl(sem_ctx *ctx, double *w, int mode, int k) {
+static int dssum_impl(sem_ctx *ctx, double *w, int mode, int k, cudaStream_t s) {
     if (ctx->nranks == 1) {
         const double by = 16.0 * ctx->dm.nsurf + (mode == 2 ? 8.0 * (ctx->dm.ngroups - ctx->dm.ndir) : 0.0);
-        LAUNCHP(kProfGs, by, mode == 2 ? k : -1,
-                launch_gs(ctx->dm, w, mode, &ctx->cv, k, ctx->nb_ax, ctx->stream));
+        LAUNCHP(kProfGs, by, mode == 2 ? k : -1, launch_gs(ctx->dm, w, mode, &ctx->cv, ctx->nb_ax, s));
         return SEM_OK;
     }
     std::string cerr;
     int64_t nl = 0;
-    int rc = comm_dssum(ctx->comm, ctx->dm, w, mode, &ctx->cv, k, ctx->nb_ax, ctx->stream, nl, cerr);
+    int rc = comm_dssum(ctx->comm, ctx->dm, w, mode, &ctx->cv, ctx->nb_ax, s, nl, cerr);
     ctx->launches += nl;
     if (rc) {
         if (rc == SEM_ECUDA) ctx->broken = true;
@@ -576,7 +614,7 @@ static int dssum_impl(sem_ctx *ctx, double *w, int mode, int k) {
 extern "C" int sem_dssum(sem_ctx *ctx, double *w) {
     CHECK_CTX();
     if (!w || !aligned8(w)) return fail(ctx, SEM_EINVAL, "sem_dssum: bad pointer");
-    return dssum_impl(ctx, w, 0, 0);
+    return dssum_impl(ctx, w, 0, -1, ctx->stream);
 }
 
 extern "C" int sem_mask(sem_ctx *ctx, double *w) {
@@ -596,11 +634,50 @@ extern "C" int sem_mass(sem_ctx *ctx, const double *f, double *b) {
 // ---------------------------------------------------------------------------
 // a9: CG driver
 // ---------------------------------------------------------------------------
-static int allgather_scalar(sem_ctx *ctx, double *slot_base) {
+static int allgather_scalar(sem_ctx *ctx, double *slot_base, cudaStream_t s) {
     if (ctx->nranks == 1) return SEM_OK;
     std::string cerr;
-    int rc = comm_allgather_scalar(ctx->comm, slot_base, ctx->stream, cerr);
+    int rc = comm_allgather_scalar(ctx->comm, slot_base, s, cerr);
     if (rc) return fail(ctx, rc, "%s", cerr.c_str());
+    return SEM_OK;
+}
+
+// One CG iteration: K1 (x/p update + Ax + interior (w,p)), gather-scatter
+// with mask and surface (w,p) + alpha's reduction, [all-gather], r-update with
+// (r,r) + beta's reduction, [all-gather].  k: host count (all-gather slot k & 3
+// and profiling only; the kernels read k from the device state).
+static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
+    CgVecs &v = ctx->cv;
+    const int P = ctx->nranks;
+    int rc;
+    LAUNCHP(kProfAxCg, (k == 0 ? 72.0 : 96.0) * ctx->L, k, launch_ax_cg(ctx->dm, v, s));
+    if ((rc = dssum_impl(ctx, v.w, 2, k, s))) return rc;
+    if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P, s))) return rc;
+    LAUNCHP(kProfRr, 24.0 * ctx->L, k, launch_rr(ctx->dm, v, true, s));
+    if ((rc = allgather_scalar(ctx, v.rr_all + ((k + 1) & 3) * P, s))) return rc;
+    return SEM_OK;
+}
+
+// Capture kChunk iterations once per context into a CUDA graph (on a private
+// non-blocking stream; the graph is launched into the caller's stream).
+static int build_cg_graph(sem_ctx *ctx) {
+    if (!ctx->cap_stream) CU(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    const int64_t l0 = ctx->launches;
+    CU(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    int rc = SEM_OK;
+    for (int q = 0; q < kChunk && rc == SEM_OK; ++q) rc = enqueue_iteration(ctx, q, ctx->cap_stream);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &g);
+    ctx->graph_kernels = ctx->launches - l0;
+    ctx->launches = l0;
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    CU(e);
+    e = cudaGraphInstantiate(&ctx->graph_exec, g, 0);
+    cudaGraphDestroy(g);
+    CU(e);
     return SEM_OK;
 }
 
@@ -625,35 +702,38 @@ extern "C" int sem_cg(sem_ctx *ctx, const double *b, double *x, double tol, int 
     }
     // r = mask (b - Q Q^T A_L x0)
     LAUNCH(launch_ax(ctx->dm, x, v.w, s));
-    if ((rc = dssum_impl(ctx, v.w, 1, 0))) return rc;
+    if ((rc = dssum_impl(ctx, v.w, 1, -1, s))) return rc;
     LAUNCH(launch_cg_init(ctx->dm, v, s));
     if (ctx->dm.ndir > 0) LAUNCH(launch_mask(ctx->dm, v.r, s));
-    LAUNCH(launch_rr(ctx->dm, v, 0, false, s));
-    if ((rc = allgather_scalar(ctx, v.rr_all + 0 * P))) return rc;
+    LAUNCH(launch_rr(ctx->dm, v, false, s));
+    if ((rc = allgather_scalar(ctx, v.rr_all + 0 * P, s))) return rc;
 
-    // iterations, enqueued in chunks; the device flag is polled one chunk behind
-    const int chunk = 8;
+    // Iterations in chunks of kChunk (a multiple of 4: the all-gather slot of
+    // position q in a chunk is q & 3 == k & 3).  The device decides when to
+    // stop; the host polls the sticky flag one chunk behind and launches no
+    // more chunks once it is set (later kernels of a chunk are no-ops).  Each
+    // chunk is one CUDA-graph launch unless profiling (per-launch events).
+    const bool graph = !ctx->prof && ctx->use_graph;
+    if (graph && !ctx->graph_exec && (rc = build_cg_graph(ctx))) return rc;
     int k = 0, c = 0;
-    bool finished = false;
-    while (!finished) {
-        for (int q = 0; q < chunk && k <= maxit; ++q, ++k) {
-            LAUNCHP(kProfAxCg, (k == 0 ? 72.0 : 96.0) * ctx->L, k, launch_ax_cg(ctx->dm, v, k, s));
-            if (k == maxit) continue;  // K1(maxit) only evaluates the stopping rule
-            if ((rc = dssum_impl(ctx, v.w, 2, k))) return rc;
-            if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P))) return rc;
-            LAUNCHP(kProfRr, 24.0 * ctx->L, k, launch_rr(ctx->dm, v, k, true, s));
-            if ((rc = allgather_scalar(ctx, v.rr_all + ((k + 1) & 3) * P))) return rc;
+    while (true) {
+        if (graph) {
+            CU(cudaGraphLaunch(ctx->graph_exec, s));
+            ctx->launches += ctx->graph_kernels;
+            k += kChunk;
+        } else {
+            for (int q = 0; q < kChunk; ++q, ++k)
+                if ((rc = enqueue_iteration(ctx, k, s))) return rc;
         }
         CU(cudaMemcpyAsync(&ctx->host_state[c & 1], v.st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
         CU(cudaEventRecord(ctx->ev[c & 1], s));
-        if (k > maxit) {  // everything that can run has been enqueued
-            CU(cudaEventSynchronize(ctx->ev[c & 1]));
-            finished = true;
-            break;
-        }
         if (c > 0) {
             CU(cudaEventSynchronize(ctx->ev[(c - 1) & 1]));
-            if (ctx->host_state[(c - 1) & 1].done) finished = true;
+            if (ctx->host_state[(c - 1) & 1].done) break;
+        }
+        if (k > maxit + 3 * kChunk) {  // the device must have stopped by now
+            CU(cudaEventSynchronize(ctx->ev[c & 1]));
+            break;
         }
         ++c;
     }

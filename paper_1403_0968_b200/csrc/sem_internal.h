@@ -22,6 +22,22 @@ struct CgState {
     double rel_res;             // sqrt(rho_k / rho0)
     double alpha[kRing];        // alpha_k in slot k & 3
     uint32_t ticket[4];         // last-block-done counters: 0 = gs/pap, 1 = rr
+    int32_t kcur;               // current CG iteration k (advanced by the r-update kernel)
+    int32_t pad_;
+    double *xptr;               // the caller's x for this solve (graph-invariant kernels)
+};
+
+// Gather-scatter groups are stored by class (Dirichlet flag, multiplicity m):
+// groups [start[c], start[c+1]) of class c have m[c] copies each; copy t of
+// group start[c] + q is local index idx[idxoff[c] + t * count_c + q].
+// Dirichlet classes come first.
+constexpr int kMaxClasses = 40;
+struct GsClasses {
+    int32_t n;
+    int32_t start[kMaxClasses + 1];
+    int32_t m[kMaxClasses];
+    int32_t idxoff[kMaxClasses];
+    int32_t dir[kMaxClasses];
 };
 
 // Everything a kernel needs to know about the discretisation on this rank.
@@ -33,9 +49,9 @@ struct DevMesh {
     const double *BM;           // [L] lumped mass w_i w_j w_k J
     // gather-scatter plan over element-SURFACE nodes: groups of local copies of
     // one global id, Dirichlet groups first ([0, ndir)), copies in ascending
-    // local order.
-    const int32_t *gs_off;      // [ngroups + 1]
-    const int32_t *gs_idx;      // [nsurf]
+    // local order, stored by class (see GsClasses).
+    GsClasses cls;
+    const int32_t *gs_idx;      // [nsurf], class-transposed
     int32_t ngroups, ndir, nsurf;
     const uint32_t *owner;      // [ceil(L/32)] bit l: this copy counts once in (.,.)_c
     int rank, nranks;
@@ -61,17 +77,20 @@ int ax_blocks(int N, int64_t E);      // grid size of the Ax kernels for E eleme
 cudaError_t launch_geom(const DevMesh &m, const double *xyz, double *G, double *BM,
                         int *bad, cudaStream_t s);
 cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t s);
-cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, int k, cudaStream_t s);
+// The CG kernels take the iteration k from CgState::kcur (device), so one
+// captured CUDA graph of a chunk of iterations is valid for every chunk.
+cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, cudaStream_t s);
 // mode: 0 = plain dssum, 1 = dssum + mask, 2 = dssum + mask + (w,p) partial +
 // last-block reduction into pap_all[k & 3][rank] (also folds the Ax partials)
-cudaError_t launch_gs(const DevMesh &m, double *w, int mode, const CgVecs *v, int k,
-                      int nb_ax, cudaStream_t s);
+cudaError_t launch_gs(const DevMesh &m, double *w, int mode, const CgVecs *v, int nb_ax,
+                      cudaStream_t s);
 cudaError_t launch_mask(const DevMesh &m, double *w, cudaStream_t s);
 cudaError_t launch_mass(const DevMesh &m, const double *f, double *b, cudaStream_t s);
+// r = b - w, resets the CG state (k = 0, x pointer of this solve)
 cudaError_t launch_cg_init(const DevMesh &m, const CgVecs &v, cudaStream_t s);
-// update: r -= alpha_k w then (r,r)_c partial into rr_all[(k+1) & 3][rank];
+// update: r -= alpha_k w then (r,r)_c partial into rr_all[(k+1) & 3][rank], k += 1;
 // !update (init): (r,r)_c of r into rr_all[0][rank]
-cudaError_t launch_rr(const DevMesh &m, const CgVecs &v, int k, bool update, cudaStream_t s);
+cudaError_t launch_rr(const DevMesh &m, const CgVecs &v, bool update, cudaStream_t s);
 cudaError_t launch_cg_finish(const DevMesh &m, const CgVecs &v, cudaStream_t s);
 
 // ax_tma.cu
@@ -80,6 +99,6 @@ int tma_blocks(int N, int64_t E, int nsm, bool cg);
 cudaError_t tma_prepare(int N);
 cudaError_t upload_const_D(int N, const double *D_host);
 cudaError_t launch_ax_tma(const DevMesh &m, const double *u, double *w, cudaStream_t s);
-cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, int k, cudaStream_t s);
+cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, cudaStream_t s);
 
 }  // namespace sem

@@ -10,6 +10,7 @@
 // Layout: local node (i,j,k) of element e at e*n^3 + i + n*j + n^2*k.
 #include <cstdio>
 
+#include "cg_device.cuh"
 #include "sem_internal.h"
 
 namespace sem {
@@ -142,11 +143,11 @@ struct AxCfg {
 
 struct AxCgArgs {
     const double *r;
-    double *x, *p, *w;
+    double *p, *w;
     double *partials;
     const double *rr_all;
     CgState *st;
-    int k, nranks;
+    int nranks;
 };
 
 template <int N, bool CG>
@@ -162,33 +163,15 @@ ax_kernel(int64_t E, const double *__restrict__ Dg, const double *__restrict__ G
     __shared__ double sred[(NT + 31) / 32];
 
     double beta = 0.0, alpha_prev = 0.0;
+    int kit = 0;
+    double *xg = nullptr;
     if constexpr (CG) {
-        CgState *st = cg.st;
-        if (*(volatile int32_t *)&st->done) return;
-        const int k = cg.k;
-        const double rho = sum_ranks(cg.rr_all + (k & 3) * cg.nranks, cg.nranks);
-        double rho0 = (k == 0) ? rho : st->rho0;
-        bool done;
-        if (k == 0 && rho0 == 0.0) done = true;
-        else done = !(k < st->maxit && sqrt(rho) > st->tol * sqrt(rho0));
-        if (done) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) {
-                st->rho0 = rho0;
-                st->iters = k;
-                st->rel_res = (rho0 == 0.0) ? 0.0 : sqrt(rho) / sqrt(rho0);
-                st->converged = (rho0 == 0.0) || !(sqrt(rho) > st->tol * sqrt(rho0));
-                __threadfence();
-                st->done = 1;
-            }
-            return;
-        }
-        if (k == 0) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) st->rho0 = rho0;
-        } else {
-            const double rho_old = sum_ranks(cg.rr_all + ((k - 1) & 3) * cg.nranks, cg.nranks);
-            beta = rho / rho_old;
-            alpha_prev = st->alpha[(k - 1) & 3];
-        }
+        const CgStep c = cg_k1_prologue(cg.st, cg.rr_all, cg.nranks);
+        if (c.done) return;
+        beta = c.beta;
+        alpha_prev = c.alpha_prev;
+        kit = c.k;
+        xg = c.x;
     }
 
     const int tid = threadIdx.x;
@@ -208,11 +191,11 @@ ax_kernel(int64_t E, const double *__restrict__ Dg, const double *__restrict__ G
                 const int64_t l = base + k * n2;
                 const double rl = cg.r[l];
                 double pl;
-                if (cg.k == 0) {
+                if (kit == 0) {
                     pl = rl;
                 } else {
                     const double po = cg.p[l];
-                    cg.x[l] += alpha_prev * po;
+                    xg[l] += alpha_prev * po;
                     pl = rl + beta * po;
                 }
                 cg.p[l] = pl;
@@ -288,22 +271,64 @@ ax_kernel(int64_t E, const double *__restrict__ Dg, const double *__restrict__ G
 
 // --------------------------------------------------------------------------
 // a6/a8: gather-scatter over element-surface groups, one thread per group.
+// Groups are stored by CLASS (Dirichlet flag, multiplicity m); inside a class
+// the copy indices are transposed ([m][count]) so lane-consecutive groups read
+// their t-th copy index coalesced, and all m value loads are in flight at
+// once (m is a compile-time constant on the common classes).
 // mode 0: Q Q^T; 1: + mask; 2: + mask + (w,p)_c partial with last-block
 // reduction of [Ax partials | gs partials] into pap_all[k&3][rank].
 // --------------------------------------------------------------------------
 struct GsArgs {
-    const int32_t *off, *idx;
-    int32_t ngroups, ndir;
+    GsClasses cls;
+    const int32_t *idx;
+    int32_t ngroups;
     double *w;
     const double *p;
     double *partials;     // Ax partials [0, nb_ax), gs partials after
     int nb_ax;
-    double *pap_out;
+    double *pap_all;      // [4][nranks]; this rank's slot k & 3 receives the sum
+    int rank, nranks;
     CgState *st;
 };
 
+__device__ __forceinline__ int gs_find_class(const GsClasses &c, int g) {
+    int q = 0;
+    while (q + 1 < c.n && g >= c.start[q + 1]) ++q;
+    return q;
+}
+
+template <int MODE, int M>
+__device__ __forceinline__ double gs_group(const int32_t *__restrict__ idx, int cnt, int gl,
+                                           bool dir, double *__restrict__ w,
+                                           const double *__restrict__ p) {
+    int li[M];
+    double v[M];
+#pragma unroll
+    for (int t = 0; t < M; ++t) li[t] = __ldg(idx + t * cnt + gl);
+#pragma unroll
+    for (int t = 0; t < M; ++t) v[t] = w[li[t]];
+    double s = v[0];
+#pragma unroll
+    for (int t = 1; t < M; ++t) s += v[t];          // ascending local order
+    if (MODE >= 1 && dir) s = 0.0;
+#pragma unroll
+    for (int t = 0; t < M; ++t) w[li[t]] = s;
+    return (MODE == 2 && !dir) ? s * p[li[0]] : 0.0;
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(kGsThreads) gs_kernel(GsArgs a) {
+__device__ __forceinline__ double gs_group_generic(const int32_t *__restrict__ idx, int m, int cnt,
+                                                   int gl, bool dir, double *__restrict__ w,
+                                                   const double *__restrict__ p) {
+    double s = w[__ldg(idx + gl)];
+    for (int t = 1; t < m; ++t) s += w[__ldg(idx + t * cnt + gl)];
+    if (MODE >= 1 && dir) s = 0.0;
+    for (int t = 0; t < m; ++t) w[__ldg(idx + t * cnt + gl)] = s;
+    return (MODE == 2 && !dir) ? s * p[__ldg(idx + gl)] : 0.0;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kGsThreads) gs_kernel(const __grid_constant__ GsArgs a) {
     __shared__ double sred[kGsThreads / 32];
     __shared__ int sflag;
     if constexpr (MODE == 2) {
@@ -312,12 +337,20 @@ __global__ void __launch_bounds__(kGsThreads) gs_kernel(GsArgs a) {
     const int g = blockIdx.x * kGsThreads + threadIdx.x;
     double part = 0.0;
     if (g < a.ngroups) {
-        const int o0 = a.off[g], o1 = a.off[g + 1];
-        double s = 0.0;
-        for (int t = o0; t < o1; ++t) s += a.w[a.idx[t]];
-        if (MODE >= 1 && g < a.ndir) s = 0.0;
-        for (int t = o0; t < o1; ++t) a.w[a.idx[t]] = s;
-        if (MODE == 2 && g >= a.ndir) part = s * a.p[a.idx[o0]];
+        const int c = gs_find_class(a.cls, g);
+        const int m = a.cls.m[c], cnt = a.cls.start[c + 1] - a.cls.start[c];
+        const int gl = g - a.cls.start[c];
+        const bool dir = a.cls.dir[c] != 0;
+        const int32_t *ix = a.idx + a.cls.idxoff[c];
+        switch (m) {
+        case 1: part = gs_group<MODE, 1>(ix, cnt, gl, dir, a.w, a.p); break;
+        case 2: part = gs_group<MODE, 2>(ix, cnt, gl, dir, a.w, a.p); break;
+        case 3: part = gs_group<MODE, 3>(ix, cnt, gl, dir, a.w, a.p); break;
+        case 4: part = gs_group<MODE, 4>(ix, cnt, gl, dir, a.w, a.p); break;
+        case 6: part = gs_group<MODE, 6>(ix, cnt, gl, dir, a.w, a.p); break;
+        case 8: part = gs_group<MODE, 8>(ix, cnt, gl, dir, a.w, a.p); break;
+        default: part = gs_group_generic<MODE>(ix, m, cnt, gl, dir, a.w, a.p); break;
+        }
     }
     if constexpr (MODE == 2) {
         const double bs = block_sum<kGsThreads>(part, sred);
@@ -325,18 +358,23 @@ __global__ void __launch_bounds__(kGsThreads) gs_kernel(GsArgs a) {
         if (last_block(&a.st->ticket[0], &sflag)) {
             const double tot = block_sum_array<kGsThreads>(a.partials, a.nb_ax + gridDim.x, sred);
             if (threadIdx.x == 0) {
-                *a.pap_out = tot;
+                const int k = *(volatile int32_t *)&a.st->kcur;
+                a.pap_all[(k & 3) * a.nranks + a.rank] = tot;
                 a.st->ticket[0] = 0;
             }
         }
     }
 }
 
-__global__ void mask_kernel(const int32_t *__restrict__ off, const int32_t *__restrict__ idx,
+// zero every copy of the Dirichlet groups (the leading classes)
+__global__ void mask_kernel(const __grid_constant__ GsClasses cls, const int32_t *__restrict__ idx,
                             int32_t ndir, double *__restrict__ w) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g < ndir)
-        for (int t = off[g]; t < off[g + 1]; ++t) w[idx[t]] = 0.0;
+    if (g >= ndir) return;
+    const int c = gs_find_class(cls, g);
+    const int m = cls.m[c], cnt = cls.start[c + 1] - cls.start[c], gl = g - cls.start[c];
+    const int32_t *ix = idx + cls.idxoff[c];
+    for (int t = 0; t < m; ++t) w[__ldg(ix + t * cnt + gl)] = 0.0;
 }
 
 __global__ void mass_kernel(int64_t L, const double *__restrict__ BM, const double *f,
@@ -348,7 +386,7 @@ __global__ void mass_kernel(int64_t L, const double *__restrict__ BM, const doub
 
 __global__ void cg_init_kernel(int64_t L, const double *__restrict__ b,
                                const double *__restrict__ w, double *__restrict__ r,
-                               CgState *st) {
+                               CgState *st, double *x) {
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L;
          l += (int64_t)gridDim.x * blockDim.x)
         r[l] = b[l] - w[l];
@@ -359,28 +397,60 @@ __global__ void cg_init_kernel(int64_t L, const double *__restrict__ b,
         st->rel_res = 0.0;
         for (int q = 0; q < kRing; ++q) st->alpha[q] = 0.0;
         st->ticket[0] = st->ticket[1] = 0;
+        st->kcur = 0;
+        st->xptr = x;
     }
 }
 
-// a9: r -= alpha_k w (update) and (r,r)_c over owner copies.
+// a9: r -= alpha_k w (update) and (r,r)_c over owner copies.  r and w are
+// workspace buffers (256-byte aligned), processed two nodes per 16-byte access.
 template <bool UPDATE>
 __global__ void __launch_bounds__(kRrThreads)
 rr_kernel(int64_t L, double *__restrict__ r, const double *__restrict__ w,
-          const uint32_t *__restrict__ owner, double *partials, const double *rr_in,
-          const double *pap_all, double *rr_out, CgState *st, int k, int nranks) {
+          const uint32_t *__restrict__ owner, double *partials, double *rr_all,
+          const double *pap_all, CgState *st, int rank, int nranks) {
     __shared__ double sred[kRrThreads / 32];
     __shared__ int sflag;
     double alpha = 0.0;
+    int k = 0;
     if constexpr (UPDATE) {
         if (*(volatile int32_t *)&st->done) return;
-        const double rho = sum_ranks(rr_in, nranks);
-        const double pap = sum_ranks(pap_all, nranks);
+        k = *(volatile int32_t *)&st->kcur;
+        const double rho = sum_rank_slot(rr_all, k & 3, nranks);
+        const double pap = sum_rank_slot(pap_all, k & 3, nranks);
         alpha = rho / pap;
         if (blockIdx.x == 0 && threadIdx.x == 0) st->alpha[k & 3] = alpha;
     }
     double part = 0.0;
-    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L;
-         l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t L2 = L >> 1;
+    double2 *r2 = reinterpret_cast<double2 *>(r);
+    const double2 *w2 = reinterpret_cast<const double2 *>(w);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < L2; h += 2 * stride) {
+        double2 ra = r2[h], rb = make_double2(0.0, 0.0);
+        const bool hb = h + stride < L2;
+        if (hb) rb = r2[h + stride];
+        const uint32_t oa = __ldg(owner + (h >> 4)) >> ((2 * h) & 31);
+        const uint32_t ob = hb ? (__ldg(owner + ((h + stride) >> 4)) >> ((2 * (h + stride)) & 31)) : 0u;
+        if constexpr (UPDATE) {
+            const double2 wa = __ldcs(w2 + h);
+            ra.x -= alpha * wa.x;
+            ra.y -= alpha * wa.y;
+            r2[h] = ra;
+            if (hb) {
+                const double2 wb = __ldcs(w2 + h + stride);
+                rb.x -= alpha * wb.x;
+                rb.y -= alpha * wb.y;
+                r2[h + stride] = rb;
+            }
+        }
+        if (oa & 1u) part += ra.x * ra.x;
+        if (oa & 2u) part += ra.y * ra.y;
+        if (ob & 1u) part += rb.x * rb.x;
+        if (ob & 2u) part += rb.y * rb.y;
+    }
+    if ((L & 1) && blockIdx.x == 0 && threadIdx.x == 0) {   // odd tail node
+        const int64_t l = L - 1;
         double rl = r[l];
         if constexpr (UPDATE) {
             rl -= alpha * w[l];
@@ -393,8 +463,13 @@ rr_kernel(int64_t L, double *__restrict__ r, const double *__restrict__ w,
     if (last_block(&st->ticket[1], &sflag)) {
         const double tot = block_sum_array<kRrThreads>(partials, gridDim.x, sred);
         if (threadIdx.x == 0) {
-            *rr_out = tot;
+            // init: slot 0; update at iteration k: slot k+1, then advance k
+            rr_all[(UPDATE ? ((k + 1) & 3) : 0) * nranks + rank] = tot;
             st->ticket[1] = 0;
+            if (UPDATE) {
+                __threadfence();
+                st->kcur = k + 1;
+            }
         }
     }
 }
@@ -466,21 +541,20 @@ cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t
     return cudaGetLastError();
 }
 
-cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, int k, cudaStream_t s) {
-    if (m.use_tma) return launch_ax_cg_tma(m, v, k, s);
-    AxCgArgs a{v.r, v.x, v.p, v.w, v.partials, v.rr_all, v.st, k, m.nranks};
+cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
+    if (m.use_tma) return launch_ax_cg_tma(m, v, s);
+    AxCgArgs a{v.r, v.p, v.w, v.partials, v.rr_all, v.st, m.nranks};
     SEM_DISPATCH_N(m.N, (ax_kernel<NN, true><<<ax_blocks_t<NN>(m.E), AxCfg<NN>::NT, 0, s>>>(
                              m.E, m.D, m.G, nullptr, v.w, a)));
     return cudaGetLastError();
 }
 
-cudaError_t launch_gs(const DevMesh &m, double *w, int mode, const CgVecs *v, int k, int nb_ax,
+cudaError_t launch_gs(const DevMesh &m, double *w, int mode, const CgVecs *v, int nb_ax,
                       cudaStream_t s) {
     GsArgs a{};
-    a.off = m.gs_off;
+    a.cls = m.cls;
     a.idx = m.gs_idx;
     a.ngroups = m.ngroups;
-    a.ndir = m.ndir;
     a.w = w;
     int nb = (m.ngroups + kGsThreads - 1) / kGsThreads;
     if (nb < 1) nb = 1;
@@ -488,7 +562,9 @@ cudaError_t launch_gs(const DevMesh &m, double *w, int mode, const CgVecs *v, in
         a.p = v->p;
         a.partials = v->partials;
         a.nb_ax = nb_ax;
-        a.pap_out = v->pap_all + (k & 3) * m.nranks + m.rank;
+        a.pap_all = v->pap_all;
+        a.rank = m.rank;
+        a.nranks = m.nranks;
         a.st = v->st;
         gs_kernel<2><<<nb, kGsThreads, 0, s>>>(a);
     } else if (mode == 1) {
@@ -501,7 +577,7 @@ cudaError_t launch_gs(const DevMesh &m, double *w, int mode, const CgVecs *v, in
 
 cudaError_t launch_mask(const DevMesh &m, double *w, cudaStream_t s) {
     if (m.ndir == 0) return cudaSuccess;
-    mask_kernel<<<(m.ndir + 255) / 256, 256, 0, s>>>(m.gs_off, m.gs_idx, m.ndir, w);
+    mask_kernel<<<(m.ndir + 255) / 256, 256, 0, s>>>(m.cls, m.gs_idx, m.ndir, w);
     return cudaGetLastError();
 }
 
@@ -511,21 +587,17 @@ cudaError_t launch_mass(const DevMesh &m, const double *f, double *b, cudaStream
 }
 
 cudaError_t launch_cg_init(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
-    cg_init_kernel<<<grid_for(m.L, 256), 256, 0, s>>>(m.L, v.b, v.w, v.r, v.st);
+    cg_init_kernel<<<grid_for(m.L, 256), 256, 0, s>>>(m.L, v.b, v.w, v.r, v.st, v.x);
     return cudaGetLastError();
 }
 
-cudaError_t launch_rr(const DevMesh &m, const CgVecs &v, int k, bool update, cudaStream_t s) {
-    const int P = m.nranks;
-    if (update) {
-        rr_kernel<true><<<kRrBlocks, kRrThreads, 0, s>>>(
-            m.L, v.r, v.w, m.owner, v.partials, v.rr_all + (k & 3) * P, v.pap_all + (k & 3) * P,
-            v.rr_all + ((k + 1) & 3) * P + m.rank, v.st, k, P);
-    } else {
+cudaError_t launch_rr(const DevMesh &m, const CgVecs &v, bool update, cudaStream_t s) {
+    if (update)
+        rr_kernel<true><<<kRrBlocks, kRrThreads, 0, s>>>(m.L, v.r, v.w, m.owner, v.partials, v.rr_all,
+                                                         v.pap_all, v.st, m.rank, m.nranks);
+    else
         rr_kernel<false><<<kRrBlocks, kRrThreads, 0, s>>>(m.L, v.r, v.w, m.owner, v.partials,
-                                                          nullptr, nullptr, v.rr_all + m.rank,
-                                                          v.st, 0, P);
-    }
+                                                          v.rr_all, v.pap_all, v.st, m.rank, m.nranks);
     return cudaGetLastError();
 }
 
