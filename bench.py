@@ -69,13 +69,14 @@ def ncu_traffic():
     if not os.path.isdir(d):
         return None
     files = sorted(f for f in os.listdir(d) if f.startswith("ncu_summary") and f.endswith(".json"))
-    if not files:
-        return None
-    try:
-        s = json.load(open(os.path.join(d, files[-1])))
-        return s.get("dominant", {}).get("dram_bytes_per_launch")
-    except Exception:
-        return None
+    for f in reversed(files):   # newest tag that captured the dominant kernel
+        try:
+            s = json.load(open(os.path.join(d, f)))
+        except Exception:
+            continue
+        if "dominant" in s:
+            return s["dominant"].get("dram_bytes_per_launch")
+    return None
 
 
 class ClockSampler:
@@ -288,7 +289,7 @@ def main():
 
     # dominant kernel roofline (K1 = fused CG Ax kernel), algorithmic bytes
     peak, peak_src = peaks()
-    k1_ms, k1_n, k1_bytes = prof["ax_cg"]
+    k1_ms, k1_n, k1_bytes = prof["k1"]
     achieved = (k1_bytes / k1_n) / (k1_ms / k1_n / 1e3) / 1e9 if k1_n else None
     traffic = ncu_traffic()
     shares = {k: v[0] / prof_ms for k, v in prof.items() if v[1]}

@@ -150,12 +150,14 @@ int sem_nccl_get_unique_id(void *id_out);
  * sem_profile(ctx, 1) resets the accumulators and brackets every later launch
  * with a pair of CUDA events on the context stream (host-side cost only);
  * sem_profile(ctx, 0) stops.  sem_profile_read synchronises the stream and
- * returns, for class `which` (0 = sem_ax kernel, 1 = fused CG Ax kernel K1,
- * 2 = gather-scatter, 3 = CG r-update/dot kernel, 4 = other), the summed
- * device milliseconds, the number of launches that did work (CG launches after
- * the stopping decision are excluded) and their ALGORITHMIC bytes (DESIGN.md:
- * Ax 64 B/node; K1 96 B/node, 72 at k = 0; r-update 24 B/node; gather-scatter
- * 16 B per surface copy + 8 B per non-Dirichlet group for (w,p)). */
+ * returns, for class `which` (0 = sem_ax kernel, 1 = CG kernel K1: x/p update
+ * + Ax + (w,p), 2 = CG kernel K2: DSSUM + mask fused with the r update and
+ * (r,r), 3 = sem_dssum gather-scatter, 4 = other), the summed device
+ * milliseconds, the number of launches that did work (CG launches after the
+ * stopping decision are excluded) and their ALGORITHMIC bytes (DESIGN.md:
+ * Ax 64 B/node; K1 96 B/node, 72 at k = 0; K2 16 B per surface copy + 8 B per
+ * non-Dirichlet surface group + 24 B per element-interior node; gather-scatter
+ * 16 B per surface copy). */
 int sem_profile(sem_ctx *ctx, int enable);
 int sem_profile_read(sem_ctx *ctx, int which, double *ms, int64_t *launches, double *bytes);
 

@@ -10,8 +10,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libsem.so")
-SOURCES = ["sem_kernels.cu", "ax_tma.cu", "sem_host.cpp", "sem_comm.cu"]
-HEADERS = ["sem_internal.h", "sem_comm.h"]
+SOURCES = ["sem_kernels.cu", "ax_tma.cu", "cg_update.cu", "sem_host.cpp", "sem_comm.cu"]
+HEADERS = ["sem_internal.h", "sem_comm.h", "cg_device.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -133,17 +133,29 @@ __device__ __forceinline__ VecRange vec_range(int64_t first, int64_t nd, int64_t
     return r;
 }
 
+// expect_tx without an arrival (the arrival comes later, after the plain-load
+// tails are in shared memory) and a plain arrival (release semantics).
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 struct TmaArgs {
     int64_t E;
     const double *G;
-    // plain: u -> w.  CG: r, p (in/out), x (in/out) -> w
+    // plain: u -> w.  CG: r, p (in/out), x (in/out, the solve's x work vector) -> w
     const double *u;
     const double *r;
-    double *p, *w;
+    double *p, *x, *w;
     double *partials;
     const double *rr_all;
+    double *pap_all;
     CgState *st;
-    int nranks;
+    int rank, nranks;
 };
 
 template <int N, bool CG>
@@ -156,19 +168,7 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
     extern __shared__ __align__(128) double smem[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + size_t(NG) * 2 * STAGE);  // [NG][2]
     __shared__ double sred[(Lo::NT + 31) / 32];
-
-    // ---- CG prologue: stopping rule, beta, alpha_prev (uniform) ----
-    double beta = 0.0, alpha_prev = 0.0;
-    int kit = 0;
-    double *xg = nullptr;
-    if constexpr (CG) {
-        const CgStep c = cg_k1_prologue(a.st, a.rr_all, a.nranks);
-        if (c.done) return;
-        beta = c.beta;
-        alpha_prev = c.alpha_prev;
-        kit = c.k;
-        xg = c.x;
-    }
+    __shared__ int sflag;
 
     const int tid = threadIdx.x;
     const int g = tid / GT;                 // group
@@ -192,39 +192,86 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    if constexpr (CG) pdl_trigger();   // let the gather-scatter grid launch early
 
     const uint64_t pol_g = policy_evict_first();
     const uint64_t pol_v = CG ? policy_evict_last() : policy_evict_first();
 
-    // Leader: issue the copies of unit `unit` into stage s.  Plain-load tails
-    // are stored BEFORE the mbarrier arrive (release), the bulk copies after
-    // expect_tx; the group observes all of it through the mbarrier phase.
-    auto issue_unit = [&](int64_t unit, int s) {
-        double *sb = stage0 + size_t(s) * STAGE;
+    // Leader, two steps per unit.  issue_G: expect the unit's bytes, start the
+    // geometric-factor copy (static data: may run before the previous kernel
+    // has finished).  issue_V: plain-load tails of the vectors into shared
+    // memory, the arrival (release), then the vector bulk copies.
+    auto unit_bytes = [&](int64_t unit, VecRange &vr, int64_t &first, int64_t &nd, uint32_t &vb,
+                          uint32_t &gb) {
         const int64_t e0 = unit * EPG;
         const int64_t ne = (a.E - e0 < EPG) ? (a.E - e0) : EPG;
-        const int64_t first = e0 * n3, nd = ne * n3;
-        const VecRange vr = vec_range(first, nd, L);
+        first = e0 * n3;
+        nd = ne * n3;
+        vr = vec_range(first, nd, L);
+        vb = (uint32_t)((vr.a1 - vr.a0) * 8);
+        gb = (uint32_t)(ne * 6 * n3 * 8);
+    };
+    auto issue_G = [&](int64_t unit, int s) {
+        VecRange vr;
+        int64_t first, nd;
+        uint32_t vb, gb;
+        unit_bytes(unit, vr, first, nd, vb, gb);
+        double *sb = stage0 + size_t(s) * STAGE;
+        mbar_expect_tx_only(gbar + s, NV * vb + gb);
+        bulk_g2s(sb + NV * VL, a.G + unit * EPG * 6 * n3, gb, gbar + s, pol_g);
+    };
+    auto issue_V = [&](int64_t unit, int s) {
+        VecRange vr;
+        int64_t first, nd;
+        uint32_t vb, gb;
+        unit_bytes(unit, vr, first, nd, vb, gb);
+        double *sb = stage0 + size_t(s) * STAGE;
         const double *vsrc[3];
         if constexpr (CG) {
             vsrc[0] = a.r;
             vsrc[1] = a.p;
-            vsrc[2] = xg;
+            vsrc[2] = a.x;
         } else {
             vsrc[0] = a.u;
         }
         for (int v = 0; v < NV; ++v)
             for (int64_t q = vr.a1; q < first + nd; ++q) sb[v * VL + (q - vr.a0)] = __ldg(vsrc[v] + q);
-        const uint32_t vb = (uint32_t)((vr.a1 - vr.a0) * 8);
-        const uint32_t gb = (uint32_t)(ne * 6 * n3 * 8);
-        mbar_expect_tx(gbar + s, NV * vb + gb);
+        mbar_arrive(gbar + s);
         for (int v = 0; v < NV; ++v) bulk_g2s(sb + v * VL, vsrc[v] + vr.a0, vb, gbar + s, pol_v);
-        bulk_g2s(sb + NV * VL, a.G + e0 * 6 * n3, gb, gbar + s, pol_g);
     };
 
     if (leader) {
-        if (u0 < nunits) issue_unit(u0, 0);
-        if (u0 + TG < nunits) issue_unit(u0 + TG, 1);
+        if (u0 < nunits) issue_G(u0, 0);
+        if (u0 + TG < nunits) issue_G(u0 + TG, 1);
+    }
+
+    // ---- CG prologue: wait for the previous kernel, stopping rule, beta ----
+    double beta = 0.0, alpha_prev = 0.0;
+    int kit = 0;
+    if constexpr (CG) {
+        pdl_wait();
+        const CgStep c = cg_k1_prologue(a.st);
+        if (c.done) {
+            // complete the protocol of the copies already in flight, then leave
+            if (leader) {
+                if (u0 < nunits) {
+                    issue_V(u0, 0);
+                    mbar_wait(gbar + 0, 0);
+                }
+                if (u0 + TG < nunits) {
+                    issue_V(u0 + TG, 1);
+                    mbar_wait(gbar + 1, 0);
+                }
+            }
+            return;
+        }
+        beta = c.beta;
+        alpha_prev = c.alpha_prev;
+        kit = c.k;
+    }
+    if (leader) {
+        if (u0 < nunits) issue_V(u0, 0);
+        if (u0 + TG < nunits) issue_V(u0 + TG, 1);
     }
 
     // thread-varying D entries in registers
@@ -266,7 +313,7 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
                         pl = rl;
                     } else {
                         const double po = sp[q];
-                        xg[gbase + k * n2] = sx[q] + alpha_prev * po;
+                        a.x[gbase + k * n2] = sx[q] + alpha_prev * po;
                         pl = rl + beta * po;
                     }
                     sp[q] = pl;
@@ -327,28 +374,31 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
             const double wv = wr + ws + wt;
             if (on) {
                 a.w[gbase + k * n2] = wv;
-                if constexpr (CG) {
-                    if (k > 0 && k < N && i > 0 && i < N && j > 0 && j < N) pap = fma(wv, col[k], pap);
-                }
+                if constexpr (CG) pap = fma(wv, col[k], pap);
             }
         }
         fence_proxy_async();     // generic smem writes before the next async refill
         group_bar(1 + g, GT);    // stage s fully consumed
-        if (leader && unit + 2 * TG < nunits) issue_unit(unit + 2 * TG, s);
+        if (leader && unit + 2 * TG < nunits) {
+            issue_G(unit + 2 * TG, s);
+            issue_V(unit + 2 * TG, s);
+        }
     }
 
     if constexpr (CG) {
-        // deterministic block reduction of the interior (w,p) partial
-        double v = pap;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        __syncthreads();
-        if ((tid & 31) == 0) sred[tid >> 5] = v;
-        __syncthreads();
-        if (tid == 0) {
-            double s = 0.0;
-            for (int q = 0; q < (Lo::NT + 31) / 32; ++q) s += sred[q];
-            a.partials[blockIdx.x] = s;
+        // (p, mask Q Q^T A_L p)_c = sum_e p_e^T A_e p_e because p is continuous
+        // and zero on the Dirichlet boundary: every local node counts, no
+        // weights, no assembly.  Deterministic block sum, then the last CTA
+        // sums the per-CTA partials in CTA order into this rank's slot k & 3.
+        const double bs = block_sum<Lo::NT>(pap, sred);
+        if (tid == 0) a.partials[blockIdx.x] = bs;
+        if (last_block(&a.st->ticket[0], &sflag)) {
+            const double tot = block_sum_array<Lo::NT>(a.partials, gridDim.x, sred);
+            if (tid == 0) {
+                if (a.nranks == 1) cg_finalize_pap(a.st, tot);
+                else a.pap_all[(kit & 3) * a.nranks + a.rank] = tot;
+                a.st->ticket[0] = 0;
+            }
         }
     }
 }
@@ -358,16 +408,16 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
 // ---------------------------------------------------------------------------
 #define SEM_TMA_DISPATCH(N_, ...)                                            \
     switch (N_) {                                                            \
-    case 1: { constexpr int NN = 1; __VA_ARGS__; } break;                           \
-    case 2: { constexpr int NN = 2; __VA_ARGS__; } break;                           \
-    case 3: { constexpr int NN = 3; __VA_ARGS__; } break;                           \
-    case 4: { constexpr int NN = 4; __VA_ARGS__; } break;                           \
-    case 5: { constexpr int NN = 5; __VA_ARGS__; } break;                           \
-    case 6: { constexpr int NN = 6; __VA_ARGS__; } break;                           \
-    case 7: { constexpr int NN = 7; __VA_ARGS__; } break;                           \
-    case 8: { constexpr int NN = 8; __VA_ARGS__; } break;                           \
-    case 9: { constexpr int NN = 9; __VA_ARGS__; } break;                           \
-    case 10: { constexpr int NN = 10; __VA_ARGS__; } break;                         \
+    case 1: { constexpr int NN = 1; __VA_ARGS__; } break;                    \
+    case 2: { constexpr int NN = 2; __VA_ARGS__; } break;                    \
+    case 3: { constexpr int NN = 3; __VA_ARGS__; } break;                    \
+    case 4: { constexpr int NN = 4; __VA_ARGS__; } break;                    \
+    case 5: { constexpr int NN = 5; __VA_ARGS__; } break;                    \
+    case 6: { constexpr int NN = 6; __VA_ARGS__; } break;                    \
+    case 7: { constexpr int NN = 7; __VA_ARGS__; } break;                    \
+    case 8: { constexpr int NN = 8; __VA_ARGS__; } break;                    \
+    case 9: { constexpr int NN = 9; __VA_ARGS__; } break;                    \
+    case 10: { constexpr int NN = 10; __VA_ARGS__; } break;                  \
     default: break;                                                          \
     }
 
@@ -423,15 +473,18 @@ cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, cudaStream_t s) 
     a.G = m.G;
     a.r = v.r;
     a.p = v.p;
+    a.x = v.xw;
     a.w = v.w;
     a.partials = v.partials;
     a.rr_all = v.rr_all;
+    a.pap_all = v.pap_all;
     a.st = v.st;
+    a.rank = m.rank;
     a.nranks = m.nranks;
-    SEM_TMA_DISPATCH(m.N, (ax_tma_kernel<NN, true><<<tma_grid<NN, true>(m.E, m.nsm),
-                                                     TmaLayout<NN, true>::NT,
-                                                     TmaLayout<NN, true>::SMEM, s>>>(a)));
-    return cudaGetLastError();
+    cudaError_t e = cudaSuccess;
+    SEM_TMA_DISPATCH(m.N, e = launch_pdl(ax_tma_kernel<NN, true>, tma_grid<NN, true>(m.E, m.nsm),
+                                         TmaLayout<NN, true>::NT, TmaLayout<NN, true>::SMEM, s, a));
+    return e;
 }
 
 }  // namespace sem

@@ -1,0 +1,239 @@
+// cg_update.cu -- K2 of the CG iteration: the
+// direct-stiffness summation of w = A_L p fused with the residual update and
+// the new residual norm (PAPER.md:667 global-local numbering; :672-673 PCG):
+//
+//   for every element-surface global node g (one thread):
+//       s_g = sum of its local copies of w, ascending local order  (= Q Q^T w)
+//       Dirichlet: nothing (r stays 0, contributes 0)              (mask)
+//       else      r_g <- r_g - alpha s_g, written to every copy; rho += r_g^2
+//   for every element-interior node (m = 1, never Dirichlet):
+//       r <- r - alpha w; rho += r^2
+//
+// so the assembled w is never written back, (r,r)_c needs no weights (each
+// global node is visited once) and one launch + one reduction replaces the
+// gather-scatter pass and the separate r-update pass.  alpha = rho_k / pAp_k
+// with pAp from K1.  INIT = true forms r0 = mask (b - Q Q^T A_L x0) and rho_0.
+#include "cg_device.cuh"
+#include "sem_internal.h"
+
+namespace sem {
+
+struct K2Args {
+    GsClasses cls;
+    const int32_t *idx;       // class-transposed copies of every surface group
+    int32_t ngroups;
+    int64_t E;
+    const double *w;
+    const double *b;          // INIT only
+    double *r;
+    double *partials;
+    double *rr_all;
+    const double *pap_all;
+    CgState *st;
+    int rank, nranks;
+};
+
+constexpr int kK2Threads = 256;
+constexpr int kK2BlocksPerSM = 4;
+
+// One batch of U groups of a class with compile-time multiplicity M (M = 0:
+// runtime m, up to 8).  All index loads, then all value loads, are issued
+// before any use, so a thread keeps U*M requests in flight.
+template <int M, int U, bool INIT>
+__device__ __forceinline__ double k2_groups(const K2Args &a, const int32_t *__restrict__ ix, int m,
+                                            int cnt, int q0, int qstride, double alpha) {
+    constexpr int MM = M ? M : 8;
+    const int mm = M ? M : m;
+    int li[U][MM];
+    bool on[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int q = q0 + u * qstride;
+        on[u] = q < cnt;
+#pragma unroll
+        for (int t = 0; t < MM; ++t) li[u][t] = (on[u] && t < mm) ? __ldg(ix + t * cnt + q) : 0;
+    }
+    double v[U][MM], r0[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int t = 0; t < MM; ++t) v[u][t] = (on[u] && t < mm) ? a.w[li[u][t]] : 0.0;
+        r0[u] = on[u] ? (INIT ? a.b[li[u][0]] : a.r[li[u][0]]) : 0.0;
+    }
+    double part = 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (!on[u]) continue;
+        double s = v[u][0];
+#pragma unroll
+        for (int t = 1; t < MM; ++t)
+            if (t < mm) s += v[u][t];                        // ascending local order
+        const double rn = INIT ? r0[u] - s : r0[u] - alpha * s;
+#pragma unroll
+        for (int t = 0; t < MM; ++t)
+            if (t < mm) a.r[li[u][t]] = rn;
+        part += rn * rn;
+    }
+    return part;
+}
+
+template <int N, bool INIT>
+__global__ void __launch_bounds__(kK2Threads) k2_kernel(const __grid_constant__ K2Args a) {
+    constexpr int n = N + 1, n2 = n * n, n3 = n2 * n, ni = N - 1;   // interior extent
+    constexpr int U = 4;
+    __shared__ double sred[kK2Threads / 32];
+    __shared__ int sflag;
+    if constexpr (!INIT) pdl_trigger();
+    const int tid = blockIdx.x * kK2Threads + threadIdx.x;
+    const int nth = gridDim.x * kK2Threads;
+
+    double alpha = 0.0;
+    int k = 0;
+    if constexpr (!INIT) {
+        pdl_wait();
+        // one round trip of independent loads (alpha_k was derived by K1)
+        const int done = ld_state(&a.st->done);
+        k = ld_state(&a.st->kcur);
+        alpha = __ldcg(&a.st->alpha_k);
+        if (done) return;
+    }
+
+    double part = 0.0;
+    // ---- element-surface global nodes, class by class ----
+    for (int c = 0; c < a.cls.n; ++c) {
+        const int cnt = a.cls.start[c + 1] - a.cls.start[c];
+        const int m = a.cls.m[c];
+        const int32_t *ix = a.idx + a.cls.idxoff[c];
+        if (a.cls.dir[c]) {
+            // Dirichlet: r stays 0 (mask); at INIT zero every copy
+            if constexpr (INIT)
+                for (int q = tid; q < cnt; q += nth)
+                    for (int t = 0; t < m; ++t) a.r[__ldg(ix + t * cnt + q)] = 0.0;
+            continue;
+        }
+        // U groups per thread per batch, fewer for the larger multiplicities
+        switch (m) {
+        case 1:
+            for (int q0 = tid; q0 < cnt; q0 += 4 * nth)
+                part += k2_groups<1, 4, INIT>(a, ix, m, cnt, q0, nth, alpha);
+            break;
+        case 2:
+            for (int q0 = tid; q0 < cnt; q0 += 4 * nth)
+                part += k2_groups<2, 4, INIT>(a, ix, m, cnt, q0, nth, alpha);
+            break;
+        case 4:
+            for (int q0 = tid; q0 < cnt; q0 += 2 * nth)
+                part += k2_groups<4, 2, INIT>(a, ix, m, cnt, q0, nth, alpha);
+            break;
+        case 8:
+            for (int q0 = tid; q0 < cnt; q0 += nth)
+                part += k2_groups<8, 1, INIT>(a, ix, m, cnt, q0, nth, alpha);
+            break;
+        default:
+            for (int q = tid; q < cnt; q += nth) {
+                double s = a.w[__ldg(ix + q)];
+                for (int t = 1; t < m; ++t) s += a.w[__ldg(ix + t * cnt + q)];
+                const double r0 = INIT ? a.b[__ldg(ix + q)] : a.r[__ldg(ix + q)];
+                const double rn = INIT ? r0 - s : r0 - alpha * s;
+                for (int t = 0; t < m; ++t) a.r[__ldg(ix + t * cnt + q)] = rn;
+                part += rn * rn;
+            }
+            break;
+        }
+    }
+
+    // ---- element-interior nodes (m = 1, never Dirichlet), i fastest ----
+    if constexpr (ni > 0) {
+        constexpr int NI3 = ni * ni * ni;
+        const int nint = (int)(a.E * NI3);
+        for (int t0 = tid; t0 < nint; t0 += U * nth) {
+            int l[U];
+            double rv[U], wv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int t = t0 + u * nth;
+                const int tt = t < nint ? t : 0;
+                const int e = tt / NI3;
+                const int q = tt - e * NI3;
+                const int ii = q % ni, jj = (q / ni) % ni, kk = q / (ni * ni);
+                l[u] = (t < nint) ? e * n3 + (kk + 1) * n2 + (jj + 1) * n + (ii + 1) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (l[u] >= 0) {
+                    rv[u] = INIT ? a.b[l[u]] : a.r[l[u]];
+                    wv[u] = __ldcs(a.w + l[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (l[u] >= 0) {
+                    const double rn = INIT ? rv[u] - wv[u] : rv[u] - alpha * wv[u];
+                    a.r[l[u]] = rn;
+                    part += rn * rn;
+                }
+            }
+        }
+    }
+
+    const double bs = block_sum<kK2Threads>(part, sred);
+    if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
+    if (last_block(&a.st->ticket[1], &sflag)) {
+        const double tot = block_sum_array<kK2Threads>(a.partials, gridDim.x, sred);
+        if (threadIdx.x == 0) {
+            a.st->ticket[1] = 0;
+            const int kn = INIT ? 0 : k + 1;
+            if (a.nranks == 1) cg_finalize_rho(a.st, kn, tot);
+            else a.rr_all[(kn & 3) * a.nranks + a.rank] = tot;
+        }
+    }
+}
+
+#define SEM_K2_DISPATCH(N_, ...)                                             \
+    switch (N_) {                                                            \
+    case 1: { constexpr int NN = 1; __VA_ARGS__; } break;                    \
+    case 2: { constexpr int NN = 2; __VA_ARGS__; } break;                    \
+    case 3: { constexpr int NN = 3; __VA_ARGS__; } break;                    \
+    case 4: { constexpr int NN = 4; __VA_ARGS__; } break;                    \
+    case 5: { constexpr int NN = 5; __VA_ARGS__; } break;                    \
+    case 6: { constexpr int NN = 6; __VA_ARGS__; } break;                    \
+    case 7: { constexpr int NN = 7; __VA_ARGS__; } break;                    \
+    case 8: { constexpr int NN = 8; __VA_ARGS__; } break;                    \
+    case 9: { constexpr int NN = 9; __VA_ARGS__; } break;                    \
+    case 10: { constexpr int NN = 10; __VA_ARGS__; } break;                  \
+    case 11: { constexpr int NN = 11; __VA_ARGS__; } break;                  \
+    case 12: { constexpr int NN = 12; __VA_ARGS__; } break;                  \
+    case 13: { constexpr int NN = 13; __VA_ARGS__; } break;                  \
+    case 14: { constexpr int NN = 14; __VA_ARGS__; } break;                  \
+    case 15: { constexpr int NN = 15; __VA_ARGS__; } break;                  \
+    default: break;                                                          \
+    }
+
+int k2_blocks(int nsm) { return nsm * kK2BlocksPerSM; }
+
+cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t s) {
+    K2Args a{};
+    a.cls = m.cls;
+    a.idx = m.gs_idx;
+    a.ngroups = m.ngroups;
+    a.E = m.E;
+    a.w = v.w;
+    a.b = v.b;
+    a.r = v.r;
+    a.partials = v.partials;
+    a.rr_all = v.rr_all;
+    a.pap_all = v.pap_all;
+    a.st = v.st;
+    a.rank = m.rank;
+    a.nranks = m.nranks;
+    const int nb = k2_blocks(m.nsm);
+    cudaError_t e = cudaSuccess;
+    if (init) {
+        SEM_K2_DISPATCH(m.N, (k2_kernel<NN, true><<<nb, kK2Threads, 0, s>>>(a), e = cudaGetLastError()));
+    } else {
+        SEM_K2_DISPATCH(m.N, e = launch_pdl(k2_kernel<NN, false>, nb, kK2Threads, 0, s, a));
+    }
+    return e;
+}
+
+}  // namespace sem

@@ -13,7 +13,7 @@ int comm_setup(Comm *&c, const sem_mesh *, const std::vector<int64_t> &, const s
     err = "nranks > 1 not built yet";
     return SEM_EINVAL;
 }
-int comm_dssum(Comm *, const DevMesh &, double *, int, CgVecs *, int, cudaStream_t, int64_t &,
+int comm_dssum(Comm *, const DevMesh &, double *, int, CgVecs *, cudaStream_t, int64_t &,
                std::string &err) {
     err = "no communicator";
     return SEM_ESTATE;

@@ -16,7 +16,7 @@ int comm_setup(Comm *&c, const sem_mesh *mesh, const std::vector<int64_t> &surf_
                const std::vector<int32_t> &idx, int64_t &nglobal, cudaStream_t s,
                std::string &err);
 // Q Q^T across ranks (mode as launch_gs).  nlaunch receives the kernel count.
-int comm_dssum(Comm *c, const DevMesh &m, double *w, int mode, CgVecs *v, int nb_ax,
+int comm_dssum(Comm *c, const DevMesh &m, double *w, int mode, CgVecs *v,
                cudaStream_t s, int64_t &nlaunch, std::string &err);
 // In-place all-gather of one double per rank at slot_base[0..nranks).
 int comm_allgather_scalar(Comm *c, double *slot_base, cudaStream_t s, std::string &err);

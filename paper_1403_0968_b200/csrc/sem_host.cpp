@@ -23,7 +23,7 @@
 using namespace sem;
 
 // kernel classes for sem_profile_read (documented in include/sem.h)
-enum { kProfAx = 0, kProfAxCg = 1, kProfGs = 2, kProfRr = 3, kProfOther = 4, kProfClasses = 5 };
+enum { kProfAx = 0, kProfAxCg = 1, kProfK2 = 2, kProfGs = 3, kProfOther = 4, kProfClasses = 5 };
 
 struct sem_ctx {
     int N = 0, n = 0, n3 = 0;
@@ -211,7 +211,7 @@ static void diff_matrix(int N, const double *x, double *D) {
 // ---------------------------------------------------------------------------
 namespace {
 struct Layout {
-    size_t G, BM, r, p, w, D, gs_idx, owner, partials, rr_all, pap_all, st, total;
+    size_t G, BM, r, p, w, xw, D, gs_idx, partials, rr_all, pap_all, st, total;
     int64_t nsurf_cap, partial_cap;
 };
 
@@ -226,7 +226,8 @@ Layout make_layout(int N, int64_t E, int nranks) {
     // TMA grid (<= one CTA per SM, <= E)
     const int nb_ax = std::max<int>(ax_blocks(N, E), (int)std::min<int64_t>(E, 1024));
     const int64_t nb_gs = (Lo.nsurf_cap + kGsThreads - 1) / kGsThreads + 1;
-    Lo.partial_cap = std::max<int64_t>(nb_ax + nb_gs, kRrBlocks) + 16;
+    // per-block partials: the Ax kernels, or K2 (group blocks + interior blocks)
+    Lo.partial_cap = std::max<int64_t>(nb_ax, nb_gs + 148 * 8) + 16;
     size_t o = 0;
     auto take = [&](size_t bytes) {
         size_t at = o;
@@ -238,9 +239,9 @@ Layout make_layout(int N, int64_t E, int nranks) {
     Lo.r = take(sizeof(double) * L);
     Lo.p = take(sizeof(double) * L);
     Lo.w = take(sizeof(double) * L);
+    Lo.xw = take(sizeof(double) * L);
     Lo.D = take(sizeof(double) * (n * n + n));
     Lo.gs_idx = take(sizeof(int32_t) * Lo.nsurf_cap);
-    Lo.owner = take(sizeof(uint32_t) * ((L + 31) / 32));
     Lo.partials = take(sizeof(double) * Lo.partial_cap);
     Lo.rr_all = take(sizeof(double) * kRing * nranks);
     Lo.pap_all = take(sizeof(double) * kRing * nranks);
@@ -279,7 +280,6 @@ struct HostPlan {
     std::vector<int32_t> cidx;          // the same copies, class-transposed (device layout)
     GsClasses cls{};
     int32_t ngroups = 0, ndir = 0;
-    std::vector<uint32_t> owner;
     int64_t ndistinct = 0;
     // for multi-rank: distinct surface global ids (ascending) and their group
     std::vector<int64_t> surf_ids;
@@ -323,7 +323,6 @@ int build_plan(const sem_mesh *m, int N, HostPlan &hp, std::string &err) {
     std::vector<int32_t> order = sort_by_glo(glo, L, gmin, gmax);
     struct G { int32_t a, b; uint8_t d; int32_t first; };
     std::vector<G> groups;
-    hp.owner.assign((L + 31) / 32, 0u);
     int64_t a = 0;
     hp.ndistinct = 0;
     while (a < L) {
@@ -351,10 +350,6 @@ int build_plan(const sem_mesh *m, int N, HostPlan &hp, std::string &err) {
             }
         } else {
             groups.push_back({(int32_t)a, (int32_t)b, d0, order[a]});
-        }
-        if (!d0) {
-            const int32_t o = order[a];  // lowest local index owns the node
-            hp.owner[o >> 5] |= 1u << (o & 31);
         }
         a = b;
     }
@@ -482,13 +477,13 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
     dm.ngroups = hp.ngroups;
     dm.ndir = hp.ndir;
     dm.nsurf = (int32_t)hp.idx.size();
-    dm.owner = reinterpret_cast<uint32_t *>(ws + Lo.owner);
     dm.rank = ctx->rank;
     dm.nranks = ctx->nranks;
     CgVecs &cv = ctx->cv;
     cv.r = reinterpret_cast<double *>(ws + Lo.r);
     cv.p = reinterpret_cast<double *>(ws + Lo.p);
     cv.w = reinterpret_cast<double *>(ws + Lo.w);
+    cv.xw = reinterpret_cast<double *>(ws + Lo.xw);
     cv.partials = reinterpret_cast<double *>(ws + Lo.partials);
     cv.rr_all = reinterpret_cast<double *>(ws + Lo.rr_all);
     cv.pap_all = reinterpret_cast<double *>(ws + Lo.pap_all);
@@ -521,8 +516,6 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         if (!hp.cidx.empty())
             CU(cudaMemcpyAsync((void *)dm.gs_idx, hp.cidx.data(), sizeof(int32_t) * hp.cidx.size(),
                                cudaMemcpyHostToDevice, s));
-        CU(cudaMemcpyAsync((void *)dm.owner, hp.owner.data(), sizeof(uint32_t) * hp.owner.size(),
-                           cudaMemcpyHostToDevice, s));
         CU(cudaMemsetAsync(cv.st, 0, sizeof(CgState), s));
         CU(cudaMemsetAsync(cv.rr_all, 0, sizeof(double) * kRing * ctx->nranks, s));
         CU(cudaMemsetAsync(cv.pap_all, 0, sizeof(double) * kRing * ctx->nranks, s));
@@ -596,13 +589,13 @@ extern "C" int sem_ax(sem_ctx *ctx, const double *u, double *w) {
 
 static int dssum_impl(sem_ctx *ctx, double *w, int mode, int k, cudaStream_t s) {
     if (ctx->nranks == 1) {
-        const double by = 16.0 * ctx->dm.nsurf + (mode == 2 ? 8.0 * (ctx->dm.ngroups - ctx->dm.ndir) : 0.0);
-        LAUNCHP(kProfGs, by, mode == 2 ? k : -1, launch_gs(ctx->dm, w, mode, &ctx->cv, ctx->nb_ax, s));
+        const double by = 16.0 * ctx->dm.nsurf;
+        LAUNCHP(kProfGs, by, mode == 2 ? k : -1, launch_gs(ctx->dm, w, mode, &ctx->cv, s));
         return SEM_OK;
     }
     std::string cerr;
     int64_t nl = 0;
-    int rc = comm_dssum(ctx->comm, ctx->dm, w, mode, &ctx->cv, ctx->nb_ax, s, nl, cerr);
+    int rc = comm_dssum(ctx->comm, ctx->dm, w, mode, &ctx->cv, s, nl, cerr);
     ctx->launches += nl;
     if (rc) {
         if (rc == SEM_ECUDA) ctx->broken = true;
@@ -642,19 +635,33 @@ static int allgather_scalar(sem_ctx *ctx, double *slot_base, cudaStream_t s) {
     return SEM_OK;
 }
 
-// One CG iteration: K1 (x/p update + Ax + interior (w,p)), gather-scatter
-// with mask and surface (w,p) + alpha's reduction, [all-gather], r-update with
-// (r,r) + beta's reduction, [all-gather].  k: host count (all-gather slot k & 3
-// and profiling only; the kernels read k from the device state).
+// Algorithmic bytes of one K2 launch: w copies read + r copies written at
+// surface nodes, r read once per non-Dirichlet group, and r read/write + w
+// read at element-interior nodes.
+static double k2_bytes(const sem_ctx *ctx) {
+    const int64_t ni = ctx->N - 1;
+    const double nint = double(ctx->E) * ni * ni * ni;
+    return 16.0 * ctx->dm.nsurf + 8.0 * (ctx->dm.ngroups - ctx->dm.ndir) + 24.0 * nint;
+}
+
+// One CG iteration: K1 (x/p update + Ax + (w,p) -> pap slot), [all-gather of
+// pap], K2 (Q Q^T w + mask fused with r -= alpha w and (r,r) -> rr slot),
+// [all-gather of rr].  k: host count (all-gather slot k & 3 and profiling
+// only; the kernels read k from the device state).
 static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
     CgVecs &v = ctx->cv;
     const int P = ctx->nranks;
     int rc;
     LAUNCHP(kProfAxCg, (k == 0 ? 72.0 : 96.0) * ctx->L, k, launch_ax_cg(ctx->dm, v, s));
-    if ((rc = dssum_impl(ctx, v.w, 2, k, s))) return rc;
-    if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P, s))) return rc;
-    LAUNCHP(kProfRr, 24.0 * ctx->L, k, launch_rr(ctx->dm, v, true, s));
-    if ((rc = allgather_scalar(ctx, v.rr_all + ((k + 1) & 3) * P, s))) return rc;
+    if (P > 1) {
+        if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P, s))) return rc;
+        LAUNCH(launch_cg_fin_pap(ctx->dm, v, s));
+    }
+    LAUNCHP(kProfK2, k2_bytes(ctx), k, launch_k2(ctx->dm, v, false, s));
+    if (P > 1) {
+        if ((rc = allgather_scalar(ctx, v.rr_all + ((k + 1) & 3) * P, s))) return rc;
+        LAUNCH(launch_cg_fin_rho(ctx->dm, v, false, s));
+    }
     return SEM_OK;
 }
 
@@ -702,11 +709,12 @@ extern "C" int sem_cg(sem_ctx *ctx, const double *b, double *x, double tol, int 
     }
     // r = mask (b - Q Q^T A_L x0)
     LAUNCH(launch_ax(ctx->dm, x, v.w, s));
-    if ((rc = dssum_impl(ctx, v.w, 1, -1, s))) return rc;
     LAUNCH(launch_cg_init(ctx->dm, v, s));
-    if (ctx->dm.ndir > 0) LAUNCH(launch_mask(ctx->dm, v.r, s));
-    LAUNCH(launch_rr(ctx->dm, v, false, s));
-    if ((rc = allgather_scalar(ctx, v.rr_all + 0 * P, s))) return rc;
+    LAUNCH(launch_k2(ctx->dm, v, true, s));
+    if (P > 1) {
+        if ((rc = allgather_scalar(ctx, v.rr_all + 0 * P, s))) return rc;
+        LAUNCH(launch_cg_fin_rho(ctx->dm, v, true, s));
+    }
 
     // Iterations in chunks of kChunk (a multiple of 4: the all-gather slot of
     // position q in a chunk is q & 3 == k & 3).  The device decides when to

@@ -20,11 +20,13 @@ struct CgState {
     int32_t iters;              // iteration count at which it fired
     int32_t converged;          // 1 if sqrt(rho) <= tol sqrt(rho0) (or rho0 == 0)
     double rel_res;             // sqrt(rho_k / rho0)
-    double alpha[kRing];        // alpha_k in slot k & 3
-    uint32_t ticket[4];         // last-block-done counters: 0 = gs/pap, 1 = rr
-    int32_t kcur;               // current CG iteration k (advanced by the r-update kernel)
+    double rho_cur;             // rho_k of the current iteration k
+    double beta;                // beta_k (0 at k = 0), for K1
+    double alpha_km1;           // alpha_{k-1} (0 at k = 0), for K1's deferred x update
+    double alpha_k;             // alpha_k, set after K1's (p, A p), for K2
+    uint32_t ticket[4];         // last-block-done counters: 0 = K1 (pAp), 1 = K2 (rr)
+    int32_t kcur;               // current CG iteration k (advanced at the end of K2)
     int32_t pad_;
-    double *xptr;               // the caller's x for this solve (graph-invariant kernels)
 };
 
 // Gather-scatter groups are stored by class (Dirichlet flag, multiplicity m):
@@ -53,7 +55,6 @@ struct DevMesh {
     GsClasses cls;
     const int32_t *gs_idx;      // [nsurf], class-transposed
     int32_t ngroups, ndir, nsurf;
-    const uint32_t *owner;      // [ceil(L/32)] bit l: this copy counts once in (.,.)_c
     int rank, nranks;
     int nsm;                    // SM count of the device (persistent grids)
     bool use_tma;               // TMA-pipelined Ax kernels (N <= kTmaMaxN)
@@ -61,15 +62,15 @@ struct DevMesh {
 
 struct CgVecs {
     const double *b;
-    double *x, *r, *p, *w;
+    double *x;                  // the caller's x of this solve (x0 in, solution out)
+    double *xw;                 // workspace copy of x updated by K1 (graph-invariant pointer)
+    double *r, *p, *w;
     double *partials;           // [kPartialCap] per-block partial sums
     double *rr_all;             // [kRing][nranks] rank partials of (r,r)_c
     double *pap_all;            // [kRing][nranks] rank partials of (w,p)_c
     CgState *st;
 };
 
-constexpr int kRrBlocks = 148 * 4;     // grid of the r-update / (r,r) kernel
-constexpr int kRrThreads = 256;
 constexpr int kGsThreads = 256;
 
 // ---- launchers (sem_kernels.cu); all return cudaGetLastError() ----
@@ -80,18 +81,22 @@ cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t
 // The CG kernels take the iteration k from CgState::kcur (device), so one
 // captured CUDA graph of a chunk of iterations is valid for every chunk.
 cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, cudaStream_t s);
-// mode: 0 = plain dssum, 1 = dssum + mask, 2 = dssum + mask + (w,p) partial +
-// last-block reduction into pap_all[k & 3][rank] (also folds the Ax partials)
-cudaError_t launch_gs(const DevMesh &m, double *w, int mode, const CgVecs *v, int nb_ax,
-                      cudaStream_t s);
+// mode: 0 = plain dssum, 1 = dssum + mask, 2 = CG iteration (dssum + mask,
+// programmatic dependent of K1, no-op after the stop; v needed)
+cudaError_t launch_gs(const DevMesh &m, double *w, int mode, const CgVecs *v, cudaStream_t s);
 cudaError_t launch_mask(const DevMesh &m, double *w, cudaStream_t s);
 cudaError_t launch_mass(const DevMesh &m, const double *f, double *b, cudaStream_t s);
-// r = b - w, resets the CG state (k = 0, x pointer of this solve)
+// xw = x0, resets the CG state (k = 0)
 cudaError_t launch_cg_init(const DevMesh &m, const CgVecs &v, cudaStream_t s);
-// update: r -= alpha_k w then (r,r)_c partial into rr_all[(k+1) & 3][rank], k += 1;
-// !update (init): (r,r)_c of r into rr_all[0][rank]
-cudaError_t launch_rr(const DevMesh &m, const CgVecs &v, bool update, cudaStream_t s);
+// cg_update.cu, K2: Q Q^T w fused with the r update and (r,r)_c into
+// rr_all[(k+1) & 3][rank], k += 1; init: r0 = mask (b - Q Q^T w), rho_0 into slot 0
+int k2_blocks(int nsm);
+cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t s);
 cudaError_t launch_cg_finish(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+// multi-rank: fold the all-gathered rank partials (ascending rank order) into
+// alpha_k, or into rho / beta / the stopping decision
+cudaError_t launch_cg_fin_pap(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+cudaError_t launch_cg_fin_rho(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t s);
 
 // ax_tma.cu
 bool tma_supported(int N);

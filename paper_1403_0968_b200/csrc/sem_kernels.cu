@@ -5,7 +5,6 @@
 //   geom_kernel      a1: isoparametric geometric factors G^ = w J (dr/dx)(dr/dx)^T
 //   ax_kernel<N,..>  a3-a5: w = D^T G^ D u per element (sum factorisation)
 //   gs_kernel        a6/a8: Q Q^T over element-surface groups (+ mask, + (w,p)_c)
-//   rr_kernel        a9: r -= alpha w and (r,r)_c, deterministic last-block reduce
 //
 // Layout: local node (i,j,k) of element e at e*n^3 + i + n*j + n^2*k.
 #include <cstdio>
@@ -18,47 +17,7 @@ namespace sem {
 // --------------------------------------------------------------------------
 // helpers
 // --------------------------------------------------------------------------
-template <int NT>
-__device__ __forceinline__ double block_sum(double v, double *red) {
-    // deterministic: fixed shuffle tree per warp, then warp 0 sums the warp
-    // results in warp order.
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    constexpr int NW = (NT + 31) / 32;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    __syncthreads();
-    if (lane == 0) red[wid] = v;
-    __syncthreads();
-    double s = 0.0;
-    if (threadIdx.x == 0) {
-        for (int q = 0; q < NW; ++q) s += red[q];
-    }
-    return s;  // valid in thread 0 only
-}
-
-// Fixed-order sum of cnt partials by one whole block (deterministic for a
-// fixed blockDim).  Result valid in thread 0.
-template <int NT>
-__device__ double block_sum_array(const double *a, int cnt, double *red) {
-    double s = 0.0;
-    for (int t = threadIdx.x; t < cnt; t += NT) s += __ldcg(a + t);
-    return block_sum<NT>(s, red);
-}
-
-// Last-block-done protocol: every block has written its partial; returns true
-// in the block that arrived last (all partials are then visible to it).
-__device__ __forceinline__ bool last_block(uint32_t *ticket, int *sflag) {
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t t = atomicAdd(ticket, 1u);
-        *sflag = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    bool last = *sflag;
-    if (last) __threadfence();
-    return last;
-}
+// (block_sum, block_sum_array, last_block: cg_device.cuh)
 
 __device__ __forceinline__ double sum_ranks(const double *a, int nranks) {
     double s = 0.0;
@@ -130,7 +89,8 @@ __global__ void geom_kernel(int n, int64_t E, const double *__restrict__ D,
 //   contractions from f_r, f_s staged per slice in shared memory.
 // CG = true fuses the CG prologue/epilogue (K1 of DESIGN.md):
 //   x += alpha_{k-1} p_{k-1};  p = r + beta_k p_{k-1};  w = A_L p;
-//   per-block partial of (w,p) over element-interior nodes.
+//   (w,p) over all local nodes (= p^T mask QQ^T A_L p), reduced into
+//   pap_all[k & 3][rank] by the last block.
 // --------------------------------------------------------------------------
 template <int N>
 struct AxCfg {
@@ -143,8 +103,10 @@ struct AxCfg {
 
 struct AxCgArgs {
     const double *r;
-    double *p, *w;
+    double *p, *x;
     double *partials;
+    double *pap_all;
+    int rank;
     const double *rr_all;
     CgState *st;
     int nranks;
@@ -160,18 +122,20 @@ ax_kernel(int64_t E, const double *__restrict__ Dg, const double *__restrict__ G
     __shared__ double su[EPB][n3];
     __shared__ double sfr[EPB][n2];
     __shared__ double sfs[EPB][n2];
+    __shared__ int sflag;
     __shared__ double sred[(NT + 31) / 32];
 
     double beta = 0.0, alpha_prev = 0.0;
     int kit = 0;
-    double *xg = nullptr;
+    double *xg = cg.x;
     if constexpr (CG) {
-        const CgStep c = cg_k1_prologue(cg.st, cg.rr_all, cg.nranks);
+        pdl_trigger();
+        pdl_wait();
+        const CgStep c = cg_k1_prologue(cg.st);
         if (c.done) return;
         beta = c.beta;
         alpha_prev = c.alpha_prev;
         kit = c.k;
-        xg = c.x;
     }
 
     const int tid = threadIdx.x;
@@ -259,13 +223,23 @@ ax_kernel(int64_t E, const double *__restrict__ Dg, const double *__restrict__ G
         for (int k = 0; k < n; ++k) wout[base + k * n2] = rw[k];
     }
     if constexpr (CG) {
+        // (p, mask Q Q^T A_L p)_c = sum_e p_e^T A_e p_e (p continuous, zero on
+        // the Dirichlet boundary); last block folds the partials in order.
         double part = 0.0;
-        if (active && i > 0 && i < N && j > 0 && j < N) {
+        if (active) {
 #pragma unroll
-            for (int k = 1; k < N; ++k) part += rw[k] * ru[k];
+            for (int k = 0; k < n; ++k) part += rw[k] * ru[k];
         }
         const double s = block_sum<NT>(part, sred);
         if (tid == 0) cg.partials[blockIdx.x] = s;
+        if (last_block(&cg.st->ticket[0], &sflag)) {
+            const double tot = block_sum_array<NT>(cg.partials, gridDim.x, sred);
+            if (tid == 0) {
+                if (cg.nranks == 1) cg_finalize_pap(cg.st, tot);
+                else cg.pap_all[(kit & 3) * cg.nranks + cg.rank] = tot;
+                cg.st->ticket[0] = 0;
+            }
+        }
     }
 }
 
@@ -275,20 +249,16 @@ ax_kernel(int64_t E, const double *__restrict__ Dg, const double *__restrict__ G
 // the copy indices are transposed ([m][count]) so lane-consecutive groups read
 // their t-th copy index coalesced, and all m value loads are in flight at
 // once (m is a compile-time constant on the common classes).
-// mode 0: Q Q^T; 1: + mask; 2: + mask + (w,p)_c partial with last-block
-// reduction of [Ax partials | gs partials] into pap_all[k&3][rank].
+// mode 0: Q Q^T; 1: + mask; 2: CG iteration (+ mask; waits for K1 when
+// launched as a programmatic dependent and is a no-op after the stop).
+// The (w,p) dot product is NOT needed here: K1 already has it (see K1).
 // --------------------------------------------------------------------------
 struct GsArgs {
     GsClasses cls;
     const int32_t *idx;
     int32_t ngroups;
     double *w;
-    const double *p;
-    double *partials;     // Ax partials [0, nb_ax), gs partials after
-    int nb_ax;
-    double *pap_all;      // [4][nranks]; this rank's slot k & 3 receives the sum
-    int rank, nranks;
-    CgState *st;
+    const CgState *st;
 };
 
 __device__ __forceinline__ int gs_find_class(const GsClasses &c, int g) {
@@ -297,14 +267,25 @@ __device__ __forceinline__ int gs_find_class(const GsClasses &c, int g) {
     return q;
 }
 
+// CG mode: the plan indices are static, so they are loaded before waiting
+// for the producer of w; then the stop flag decides.
+template <int MODE>
+__device__ __forceinline__ bool gs_ready(const CgState *st) {
+    if constexpr (MODE == 2) {
+        pdl_wait();
+        return !ld_state(&st->done);
+    }
+    return true;
+}
+
 template <int MODE, int M>
-__device__ __forceinline__ double gs_group(const int32_t *__restrict__ idx, int cnt, int gl,
-                                           bool dir, double *__restrict__ w,
-                                           const double *__restrict__ p) {
+__device__ __forceinline__ void gs_group(const int32_t *__restrict__ idx, int cnt, int gl, bool dir,
+                                         double *__restrict__ w, const CgState *st) {
     int li[M];
     double v[M];
 #pragma unroll
     for (int t = 0; t < M; ++t) li[t] = __ldg(idx + t * cnt + gl);
+    if (!gs_ready<MODE>(st)) return;
 #pragma unroll
     for (int t = 0; t < M; ++t) v[t] = w[li[t]];
     double s = v[0];
@@ -313,56 +294,37 @@ __device__ __forceinline__ double gs_group(const int32_t *__restrict__ idx, int 
     if (MODE >= 1 && dir) s = 0.0;
 #pragma unroll
     for (int t = 0; t < M; ++t) w[li[t]] = s;
-    return (MODE == 2 && !dir) ? s * p[li[0]] : 0.0;
 }
 
 template <int MODE>
-__device__ __forceinline__ double gs_group_generic(const int32_t *__restrict__ idx, int m, int cnt,
-                                                   int gl, bool dir, double *__restrict__ w,
-                                                   const double *__restrict__ p) {
+__device__ __forceinline__ void gs_group_generic(const int32_t *__restrict__ idx, int m, int cnt,
+                                                 int gl, bool dir, double *__restrict__ w,
+                                                 const CgState *st) {
+    if (!gs_ready<MODE>(st)) return;
     double s = w[__ldg(idx + gl)];
     for (int t = 1; t < m; ++t) s += w[__ldg(idx + t * cnt + gl)];
     if (MODE >= 1 && dir) s = 0.0;
     for (int t = 0; t < m; ++t) w[__ldg(idx + t * cnt + gl)] = s;
-    return (MODE == 2 && !dir) ? s * p[__ldg(idx + gl)] : 0.0;
 }
 
 template <int MODE>
 __global__ void __launch_bounds__(kGsThreads) gs_kernel(const __grid_constant__ GsArgs a) {
-    __shared__ double sred[kGsThreads / 32];
-    __shared__ int sflag;
-    if constexpr (MODE == 2) {
-        if (*(volatile int32_t *)&a.st->done) return;
-    }
+    if constexpr (MODE == 2) pdl_trigger();
     const int g = blockIdx.x * kGsThreads + threadIdx.x;
-    double part = 0.0;
-    if (g < a.ngroups) {
-        const int c = gs_find_class(a.cls, g);
-        const int m = a.cls.m[c], cnt = a.cls.start[c + 1] - a.cls.start[c];
-        const int gl = g - a.cls.start[c];
-        const bool dir = a.cls.dir[c] != 0;
-        const int32_t *ix = a.idx + a.cls.idxoff[c];
-        switch (m) {
-        case 1: part = gs_group<MODE, 1>(ix, cnt, gl, dir, a.w, a.p); break;
-        case 2: part = gs_group<MODE, 2>(ix, cnt, gl, dir, a.w, a.p); break;
-        case 3: part = gs_group<MODE, 3>(ix, cnt, gl, dir, a.w, a.p); break;
-        case 4: part = gs_group<MODE, 4>(ix, cnt, gl, dir, a.w, a.p); break;
-        case 6: part = gs_group<MODE, 6>(ix, cnt, gl, dir, a.w, a.p); break;
-        case 8: part = gs_group<MODE, 8>(ix, cnt, gl, dir, a.w, a.p); break;
-        default: part = gs_group_generic<MODE>(ix, m, cnt, gl, dir, a.w, a.p); break;
-        }
-    }
-    if constexpr (MODE == 2) {
-        const double bs = block_sum<kGsThreads>(part, sred);
-        if (threadIdx.x == 0) a.partials[a.nb_ax + blockIdx.x] = bs;
-        if (last_block(&a.st->ticket[0], &sflag)) {
-            const double tot = block_sum_array<kGsThreads>(a.partials, a.nb_ax + gridDim.x, sred);
-            if (threadIdx.x == 0) {
-                const int k = *(volatile int32_t *)&a.st->kcur;
-                a.pap_all[(k & 3) * a.nranks + a.rank] = tot;
-                a.st->ticket[0] = 0;
-            }
-        }
+    if (g >= a.ngroups) return;
+    const int c = gs_find_class(a.cls, g);
+    const int m = a.cls.m[c], cnt = a.cls.start[c + 1] - a.cls.start[c];
+    const int gl = g - a.cls.start[c];
+    const bool dir = a.cls.dir[c] != 0;
+    const int32_t *ix = a.idx + a.cls.idxoff[c];
+    switch (m) {
+    case 1: gs_group<MODE, 1>(ix, cnt, gl, dir, a.w, a.st); break;
+    case 2: gs_group<MODE, 2>(ix, cnt, gl, dir, a.w, a.st); break;
+    case 3: gs_group<MODE, 3>(ix, cnt, gl, dir, a.w, a.st); break;
+    case 4: gs_group<MODE, 4>(ix, cnt, gl, dir, a.w, a.st); break;
+    case 6: gs_group<MODE, 6>(ix, cnt, gl, dir, a.w, a.st); break;
+    case 8: gs_group<MODE, 8>(ix, cnt, gl, dir, a.w, a.st); break;
+    default: gs_group_generic<MODE>(ix, m, cnt, gl, dir, a.w, a.st); break;
     }
 }
 
@@ -384,104 +346,45 @@ __global__ void mass_kernel(int64_t L, const double *__restrict__ BM, const doub
         b[l] = BM[l] * f[l];
 }
 
-__global__ void cg_init_kernel(int64_t L, const double *__restrict__ b,
-                               const double *__restrict__ w, double *__restrict__ r,
-                               CgState *st, double *x) {
+// CG start: xw = x0 (K1 updates the workspace copy), reset the device state.
+__global__ void cg_init_kernel(int64_t L, CgState *st, const double *__restrict__ x,
+                               double *__restrict__ xw) {
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L;
          l += (int64_t)gridDim.x * blockDim.x)
-        r[l] = b[l] - w[l];
+        xw[l] = x[l];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         st->done = 0;
         st->iters = 0;
         st->converged = 0;
         st->rel_res = 0.0;
-        for (int q = 0; q < kRing; ++q) st->alpha[q] = 0.0;
+        st->rho_cur = st->beta = st->alpha_km1 = st->alpha_k = 0.0;
         st->ticket[0] = st->ticket[1] = 0;
         st->kcur = 0;
-        st->xptr = x;
     }
 }
 
-// a9: r -= alpha_k w (update) and (r,r)_c over owner copies.  r and w are
-// workspace buffers (256-byte aligned), processed two nodes per 16-byte access.
-template <bool UPDATE>
-__global__ void __launch_bounds__(kRrThreads)
-rr_kernel(int64_t L, double *__restrict__ r, const double *__restrict__ w,
-          const uint32_t *__restrict__ owner, double *partials, double *rr_all,
-          const double *pap_all, CgState *st, int rank, int nranks) {
-    __shared__ double sred[kRrThreads / 32];
-    __shared__ int sflag;
-    double alpha = 0.0;
-    int k = 0;
-    if constexpr (UPDATE) {
-        if (*(volatile int32_t *)&st->done) return;
-        k = *(volatile int32_t *)&st->kcur;
-        const double rho = sum_rank_slot(rr_all, k & 3, nranks);
-        const double pap = sum_rank_slot(pap_all, k & 3, nranks);
-        alpha = rho / pap;
-        if (blockIdx.x == 0 && threadIdx.x == 0) st->alpha[k & 3] = alpha;
-    }
-    double part = 0.0;
-    const int64_t L2 = L >> 1;
-    double2 *r2 = reinterpret_cast<double2 *>(r);
-    const double2 *w2 = reinterpret_cast<const double2 *>(w);
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < L2; h += 2 * stride) {
-        double2 ra = r2[h], rb = make_double2(0.0, 0.0);
-        const bool hb = h + stride < L2;
-        if (hb) rb = r2[h + stride];
-        const uint32_t oa = __ldg(owner + (h >> 4)) >> ((2 * h) & 31);
-        const uint32_t ob = hb ? (__ldg(owner + ((h + stride) >> 4)) >> ((2 * (h + stride)) & 31)) : 0u;
-        if constexpr (UPDATE) {
-            const double2 wa = __ldcs(w2 + h);
-            ra.x -= alpha * wa.x;
-            ra.y -= alpha * wa.y;
-            r2[h] = ra;
-            if (hb) {
-                const double2 wb = __ldcs(w2 + h + stride);
-                rb.x -= alpha * wb.x;
-                rb.y -= alpha * wb.y;
-                r2[h + stride] = rb;
-            }
-        }
-        if (oa & 1u) part += ra.x * ra.x;
-        if (oa & 2u) part += ra.y * ra.y;
-        if (ob & 1u) part += rb.x * rb.x;
-        if (ob & 2u) part += rb.y * rb.y;
-    }
-    if ((L & 1) && blockIdx.x == 0 && threadIdx.x == 0) {   // odd tail node
-        const int64_t l = L - 1;
-        double rl = r[l];
-        if constexpr (UPDATE) {
-            rl -= alpha * w[l];
-            r[l] = rl;
-        }
-        if ((__ldg(owner + (l >> 5)) >> (l & 31)) & 1u) part += rl * rl;
-    }
-    const double bs = block_sum<kRrThreads>(part, sred);
-    if (threadIdx.x == 0) partials[blockIdx.x] = bs;
-    if (last_block(&st->ticket[1], &sflag)) {
-        const double tot = block_sum_array<kRrThreads>(partials, gridDim.x, sred);
-        if (threadIdx.x == 0) {
-            // init: slot 0; update at iteration k: slot k+1, then advance k
-            rr_all[(UPDATE ? ((k + 1) & 3) : 0) * nranks + rank] = tot;
-            st->ticket[1] = 0;
-            if (UPDATE) {
-                __threadfence();
-                st->kcur = k + 1;
-            }
-        }
-    }
+// Multi-rank finalisers (one thread), after the all-gather of the rank partials:
+// sum them in ascending rank order and derive the next scalars.
+__global__ void cg_fin_pap_kernel(CgState *st, const double *pap_all, int nranks) {
+    if (ld_state(&st->done)) return;
+    const int k = ld_state(&st->kcur);
+    cg_finalize_pap(st, sum_rank_slot(pap_all, k & 3, nranks));
 }
 
-__global__ void cg_finish_kernel(int64_t L, double *__restrict__ x,
+__global__ void cg_fin_rho_kernel(CgState *st, const double *rr_all, int nranks, int init) {
+    if (ld_state(&st->done)) return;
+    const int kn = init ? 0 : ld_state(&st->kcur) + 1;
+    cg_finalize_rho(st, kn, sum_rank_slot(rr_all, kn & 3, nranks));
+}
+
+// x = xw + alpha_{it-1} p_{it-1}: the update K1 would have applied next.
+__global__ void cg_finish_kernel(int64_t L, double *__restrict__ x, const double *__restrict__ xw,
                                  const double *__restrict__ p, const CgState *st) {
     const int it = st->iters;
-    if (it < 1) return;
-    const double a = st->alpha[(it - 1) & 3];
+    const double a = (it >= 1) ? st->alpha_km1 : 0.0;
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L;
          l += (int64_t)gridDim.x * blockDim.x)
-        x[l] += a * p[l];
+        x[l] = (it >= 1) ? xw[l] + a * p[l] : xw[l];
 }
 
 // --------------------------------------------------------------------------
@@ -543,14 +446,14 @@ cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t
 
 cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
     if (m.use_tma) return launch_ax_cg_tma(m, v, s);
-    AxCgArgs a{v.r, v.p, v.w, v.partials, v.rr_all, v.st, m.nranks};
-    SEM_DISPATCH_N(m.N, (ax_kernel<NN, true><<<ax_blocks_t<NN>(m.E), AxCfg<NN>::NT, 0, s>>>(
-                             m.E, m.D, m.G, nullptr, v.w, a)));
-    return cudaGetLastError();
+    AxCgArgs a{v.r, v.p, v.xw, v.partials, v.pap_all, m.rank, v.rr_all, v.st, m.nranks};
+    cudaError_t e = cudaSuccess;
+    SEM_DISPATCH_N(m.N, (e = launch_pdl(ax_kernel<NN, true>, ax_blocks_t<NN>(m.E), AxCfg<NN>::NT,
+                                        0, s, m.E, m.D, m.G, (const double *)nullptr, v.w, a)));
+    return e;
 }
 
-cudaError_t launch_gs(const DevMesh &m, double *w, int mode, const CgVecs *v, int nb_ax,
-                      cudaStream_t s) {
+cudaError_t launch_gs(const DevMesh &m, double *w, int mode, const CgVecs *v, cudaStream_t s) {
     GsArgs a{};
     a.cls = m.cls;
     a.idx = m.gs_idx;
@@ -559,14 +462,8 @@ cudaError_t launch_gs(const DevMesh &m, double *w, int mode, const CgVecs *v, in
     int nb = (m.ngroups + kGsThreads - 1) / kGsThreads;
     if (nb < 1) nb = 1;
     if (mode == 2) {
-        a.p = v->p;
-        a.partials = v->partials;
-        a.nb_ax = nb_ax;
-        a.pap_all = v->pap_all;
-        a.rank = m.rank;
-        a.nranks = m.nranks;
         a.st = v->st;
-        gs_kernel<2><<<nb, kGsThreads, 0, s>>>(a);
+        return launch_pdl(gs_kernel<2>, nb, kGsThreads, 0, s, a);
     } else if (mode == 1) {
         gs_kernel<1><<<nb, kGsThreads, 0, s>>>(a);
     } else {
@@ -587,22 +484,22 @@ cudaError_t launch_mass(const DevMesh &m, const double *f, double *b, cudaStream
 }
 
 cudaError_t launch_cg_init(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
-    cg_init_kernel<<<grid_for(m.L, 256), 256, 0, s>>>(m.L, v.b, v.w, v.r, v.st, v.x);
+    cg_init_kernel<<<grid_for(m.L, 256), 256, 0, s>>>(m.L, v.st, v.x, v.xw);
     return cudaGetLastError();
 }
 
-cudaError_t launch_rr(const DevMesh &m, const CgVecs &v, bool update, cudaStream_t s) {
-    if (update)
-        rr_kernel<true><<<kRrBlocks, kRrThreads, 0, s>>>(m.L, v.r, v.w, m.owner, v.partials, v.rr_all,
-                                                         v.pap_all, v.st, m.rank, m.nranks);
-    else
-        rr_kernel<false><<<kRrBlocks, kRrThreads, 0, s>>>(m.L, v.r, v.w, m.owner, v.partials,
-                                                          v.rr_all, v.pap_all, v.st, m.rank, m.nranks);
+cudaError_t launch_cg_fin_pap(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
+    cg_fin_pap_kernel<<<1, 1, 0, s>>>(v.st, v.pap_all, m.nranks);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cg_fin_rho(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t s) {
+    cg_fin_rho_kernel<<<1, 1, 0, s>>>(v.st, v.rr_all, m.nranks, init ? 1 : 0);
     return cudaGetLastError();
 }
 
 cudaError_t launch_cg_finish(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
-    cg_finish_kernel<<<grid_for(m.L, 256), 256, 0, s>>>(m.L, v.x, v.p, v.st);
+    cg_finish_kernel<<<grid_for(m.L, 256), 256, 0, s>>>(m.L, v.x, v.xw, v.p, v.st);
     return cudaGetLastError();
 }
 

@@ -219,7 +219,7 @@ class Context:
         self.mask(b)
         return b
 
-    PROF_CLASSES = ("ax", "ax_cg", "gs", "rr", "other")
+    PROF_CLASSES = ("ax", "k1", "k2", "dssum", "other")
 
     def profile(self, enable: bool = True):
         _check(lib().sem_profile(self._ctx, 1 if enable else 0), self._ctx)

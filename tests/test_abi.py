@@ -84,8 +84,8 @@ def test_workspace_bytes_and_validation(L):
     nb = ctypes.c_size_t(0)
     assert L.sem_workspace_bytes(ctypes.byref(s), N, ctypes.byref(nb)) == 0
     Lloc = m.nlocal
-    # G (6L) + B (L) + r, p, w (3L) doubles dominate
-    assert 80 * Lloc <= nb.value <= 100 * Lloc
+    # G (6L) + B (L) + r, p, w, xw (4L) doubles dominate
+    assert 88 * Lloc <= nb.value <= 110 * Lloc
     assert L.sem_workspace_bytes(ctypes.byref(s), 0, ctypes.byref(nb)) == sem.SEM_EINVAL
     assert L.sem_workspace_bytes(ctypes.byref(s), 16, ctypes.byref(nb)) == sem.SEM_EINVAL
     s.nelem = 0
