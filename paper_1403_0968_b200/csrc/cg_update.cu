@@ -31,10 +31,18 @@ struct K2Args {
     const double *pap_all;
     CgState *st;
     int rank, nranks;
+    int32_t cchunk[kMaxClasses + 1];   // first chunk of each class; cchunk[n] = interior
+    int32_t nchunks;
+    int32_t dbg;                       // timing experiments only (SEM_K2_DEBUG), 0 in production
 };
 
 constexpr int kK2Threads = 256;
 constexpr int kK2BlocksPerSM = 4;
+
+// groups per thread in one chunk, by multiplicity
+__host__ __device__ constexpr int k2_upb(int m) {
+    return (m == 1 || m == 2) ? 4 : (m == 4 ? 2 : 1);
+}
 
 // One batch of U groups of a class with compile-time multiplicity M (M = 0:
 // runtime m, up to 8).  All index loads, then all value loads, are issued
@@ -80,13 +88,9 @@ __device__ __forceinline__ double k2_groups(const K2Args &a, const int32_t *__re
 template <int N, bool INIT>
 __global__ void __launch_bounds__(kK2Threads) k2_kernel(const __grid_constant__ K2Args a) {
     constexpr int n = N + 1, n2 = n * n, n3 = n2 * n, ni = N - 1;   // interior extent
-    constexpr int U = 4;
     __shared__ double sred[kK2Threads / 32];
     __shared__ int sflag;
     if constexpr (!INIT) pdl_trigger();
-    const int tid = blockIdx.x * kK2Threads + threadIdx.x;
-    const int nth = gridDim.x * kK2Threads;
-
     double alpha = 0.0;
     int k = 0;
     if constexpr (!INIT) {
@@ -99,59 +103,59 @@ __global__ void __launch_bounds__(kK2Threads) k2_kernel(const __grid_constant__ 
     }
 
     double part = 0.0;
-    // ---- element-surface global nodes, class by class ----
-    for (int c = 0; c < a.cls.n; ++c) {
-        const int cnt = a.cls.start[c + 1] - a.cls.start[c];
-        const int m = a.cls.m[c];
-        const int32_t *ix = a.idx + a.cls.idxoff[c];
-        if (a.cls.dir[c]) {
-            // Dirichlet: r stays 0 (mask); at INIT zero every copy
-            if constexpr (INIT)
-                for (int q = tid; q < cnt; q += nth)
-                    for (int t = 0; t < m; ++t) a.r[__ldg(ix + t * cnt + q)] = 0.0;
-            continue;
-        }
-        // U groups per thread per batch, fewer for the larger multiplicities
-        switch (m) {
-        case 1:
-            for (int q0 = tid; q0 < cnt; q0 += 4 * nth)
-                part += k2_groups<1, 4, INIT>(a, ix, m, cnt, q0, nth, alpha);
-            break;
-        case 2:
-            for (int q0 = tid; q0 < cnt; q0 += 4 * nth)
-                part += k2_groups<2, 4, INIT>(a, ix, m, cnt, q0, nth, alpha);
-            break;
-        case 4:
-            for (int q0 = tid; q0 < cnt; q0 += 2 * nth)
-                part += k2_groups<4, 2, INIT>(a, ix, m, cnt, q0, nth, alpha);
-            break;
-        case 8:
-            for (int q0 = tid; q0 < cnt; q0 += nth)
-                part += k2_groups<8, 1, INIT>(a, ix, m, cnt, q0, nth, alpha);
-            break;
-        default:
-            for (int q = tid; q < cnt; q += nth) {
-                double s = a.w[__ldg(ix + q)];
-                for (int t = 1; t < m; ++t) s += a.w[__ldg(ix + t * cnt + q)];
-                const double r0 = INIT ? a.b[__ldg(ix + q)] : a.r[__ldg(ix + q)];
-                const double rn = INIT ? r0 - s : r0 - alpha * s;
-                for (int t = 0; t < m; ++t) a.r[__ldg(ix + t * cnt + q)] = rn;
-                part += rn * rn;
+    // Work is cut into chunks of one thread-batch per block: chunks
+    // [cchunk[c], cchunk[c+1]) cover class c (kK2Threads * U_m groups each),
+    // chunks from cchunk[n] on cover the element-interior nodes (kK2Threads * 4
+    // nodes each).  A block walks chunks blockIdx.x, +gridDim.x, ...; every
+    // chunk is one dependent round trip (indices, then values).
+    const int ncls = a.cls.n;
+    for (int ch = blockIdx.x; ch < a.nchunks; ch += gridDim.x) {
+        if ((a.dbg & 1) && ch < a.cchunk[ncls]) continue;
+        if ((a.dbg & 2) && ch >= a.cchunk[ncls]) continue;
+        if (ch < a.cchunk[ncls]) {
+            int c = 0;
+            while (ch >= a.cchunk[c + 1]) ++c;
+            const int cnt = a.cls.start[c + 1] - a.cls.start[c];
+            const int m = a.cls.m[c];
+            const int32_t *ix = a.idx + a.cls.idxoff[c];
+            const int base = (ch - a.cchunk[c]) * kK2Threads * k2_upb(m) + threadIdx.x;
+            if (a.cls.dir[c]) {
+                // Dirichlet (INIT only): r0 = 0 at every copy (mask)
+                for (int u = 0; u < k2_upb(m); ++u) {
+                    const int q = base + u * kK2Threads;
+                    if (q < cnt)
+                        for (int t = 0; t < m; ++t) a.r[__ldg(ix + t * cnt + q)] = 0.0;
+                }
+                continue;
             }
-            break;
-        }
-    }
-
-    // ---- element-interior nodes (m = 1, never Dirichlet), i fastest ----
-    if constexpr (ni > 0) {
-        constexpr int NI3 = ni * ni * ni;
-        const int nint = (int)(a.E * NI3);
-        for (int t0 = tid; t0 < nint; t0 += U * nth) {
+            switch (m) {
+            case 1: part += k2_groups<1, 4, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
+            case 2: part += k2_groups<2, 4, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
+            case 4: part += k2_groups<4, 2, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
+            case 8: part += k2_groups<8, 1, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
+            default: {
+                const int q = base;
+                if (q < cnt) {
+                    double s = a.w[__ldg(ix + q)];
+                    for (int t = 1; t < m; ++t) s += a.w[__ldg(ix + t * cnt + q)];
+                    const double r0 = INIT ? a.b[__ldg(ix + q)] : a.r[__ldg(ix + q)];
+                    const double rn = INIT ? r0 - s : r0 - alpha * s;
+                    for (int t = 0; t < m; ++t) a.r[__ldg(ix + t * cnt + q)] = rn;
+                    part += rn * rn;
+                }
+            } break;
+            }
+        } else if constexpr (ni > 0) {
+            // element-interior nodes (m = 1, never Dirichlet), i fastest
+            constexpr int U = 4;
+            constexpr int NI3 = ni * ni * ni;
+            const int nint = (int)(a.E * NI3);
+            const int t0 = (ch - a.cchunk[ncls]) * kK2Threads * U + threadIdx.x;
             int l[U];
             double rv[U], wv[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int t = t0 + u * nth;
+                const int t = t0 + u * kK2Threads;
                 const int tt = t < nint ? t : 0;
                 const int e = tt / NI3;
                 const int q = tt - e * NI3;
@@ -176,6 +180,13 @@ __global__ void __launch_bounds__(kK2Threads) k2_kernel(const __grid_constant__ 
         }
     }
 
+    if (a.dbg & 4) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            const int kn = INIT ? 0 : k + 1;
+            if (a.nranks == 1) cg_finalize_rho(a.st, kn, part + 1.0);
+        }
+        return;
+    }
     const double bs = block_sum<kK2Threads>(part, sred);
     if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
     if (last_block(&a.st->ticket[1], &sflag)) {
@@ -226,7 +237,25 @@ cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t
     a.st = v.st;
     a.rank = m.rank;
     a.nranks = m.nranks;
-    const int nb = k2_blocks(m.nsm);
+    // chunk table (Dirichlet classes only at INIT)
+    int nch = 0;
+    for (int c = 0; c < m.cls.n; ++c) {
+        a.cchunk[c] = nch;
+        const int cnt = m.cls.start[c + 1] - m.cls.start[c];
+        const int per = kK2Threads * k2_upb(m.cls.m[c]);
+        if (!m.cls.dir[c] || init) nch += (cnt + per - 1) / per;
+    }
+    a.cchunk[m.cls.n] = nch;
+    const int64_t nint = m.E * int64_t(m.N - 1) * (m.N - 1) * (m.N - 1);
+    nch += (int)((nint + 4 * kK2Threads - 1) / (4 * kK2Threads));
+    a.nchunks = nch;
+    static const int dbg = [] {
+        const char *e = getenv("SEM_K2_DEBUG");
+        return e ? atoi(e) : 0;
+    }();
+    a.dbg = init ? 0 : dbg;
+    int nb = k2_blocks(m.nsm);
+    if (nb > nch) nb = nch > 0 ? nch : 1;
     cudaError_t e = cudaSuccess;
     if (init) {
         SEM_K2_DISPATCH(m.N, (k2_kernel<NN, true><<<nb, kK2Threads, 0, s>>>(a), e = cudaGetLastError()));
