@@ -151,11 +151,9 @@ struct TmaArgs {
     const double *u;
     const double *r;
     double *p, *x, *w;
-    double *partials;
-    const double *rr_all;
-    double *pap_all;
+    CgRed red;            // where the scalar reductions live
+    double *part1;        // this kernel's (p, A p) partials, [2][s1]
     CgState *st;
-    int rank, nranks;
 };
 
 template <int N, bool CG>
@@ -167,8 +165,7 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
     constexpr int DO = d_off(N);
     extern __shared__ __align__(128) double smem[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + size_t(NG) * 2 * STAGE);  // [NG][2]
-    __shared__ double sred[(Lo::NT + 31) / 32];
-    __shared__ int sflag;
+    __shared__ double sred[3 * ((Lo::NT + 31) / 32)];
 
     const int tid = threadIdx.x;
     const int g = tid / GT;                 // group
@@ -245,33 +242,28 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
         if (u0 + TG < nunits) issue_G(u0 + TG, 1);
     }
 
-    // ---- CG prologue: wait for the previous kernel, stopping rule, beta ----
+    // ---- the vectors (produced by the previous kernels) follow; the scalars
+    // of this iteration are reduced while all those copies are in flight ----
+    if constexpr (CG) pdl_wait();
+    if (leader) {
+        if (u0 < nunits) issue_V(u0, 0);
+        if (u0 + TG < nunits) issue_V(u0 + TG, 1);
+    }
     double beta = 0.0, alpha_prev = 0.0;
     int kit = 0;
     if constexpr (CG) {
-        pdl_wait();
-        const CgStep c = cg_k1_prologue(a.st);
+        const CgStep c = cg_k1_prologue<Lo::NT>(a.st, a.red, sred);
         if (c.done) {
-            // complete the protocol of the copies already in flight, then leave
+            // drain the copies already in flight, then leave
             if (leader) {
-                if (u0 < nunits) {
-                    issue_V(u0, 0);
-                    mbar_wait(gbar + 0, 0);
-                }
-                if (u0 + TG < nunits) {
-                    issue_V(u0 + TG, 1);
-                    mbar_wait(gbar + 1, 0);
-                }
+                if (u0 < nunits) mbar_wait(gbar + 0, 0);
+                if (u0 + TG < nunits) mbar_wait(gbar + 1, 0);
             }
             return;
         }
         beta = c.beta;
         alpha_prev = c.alpha_prev;
         kit = c.k;
-    }
-    if (leader) {
-        if (u0 < nunits) issue_V(u0, 0);
-        if (u0 + TG < nunits) issue_V(u0 + TG, 1);
     }
 
     // thread-varying D entries in registers
@@ -388,18 +380,10 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
     if constexpr (CG) {
         // (p, mask Q Q^T A_L p)_c = sum_e p_e^T A_e p_e because p is continuous
         // and zero on the Dirichlet boundary: every local node counts, no
-        // weights, no assembly.  Deterministic block sum, then the last CTA
-        // sums the per-CTA partials in CTA order into this rank's slot k & 3.
+        // weights, no assembly.  One deterministic partial per CTA; the
+        // consumers reduce them (see cg_device.cuh).
         const double bs = block_sum<Lo::NT>(pap, sred);
-        if (tid == 0) a.partials[blockIdx.x] = bs;
-        if (last_block(&a.st->ticket[0], &sflag)) {
-            const double tot = block_sum_array<Lo::NT>(a.partials, gridDim.x, sred);
-            if (tid == 0) {
-                if (a.nranks == 1) cg_finalize_pap(a.st, tot);
-                else a.pap_all[(kit & 3) * a.nranks + a.rank] = tot;
-                a.st->ticket[0] = 0;
-            }
-        }
+        if (tid == 0) a.part1[(kit & 1) * a.red.s1 + blockIdx.x] = bs;
     }
 }
 
@@ -475,12 +459,9 @@ cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, cudaStream_t s) 
     a.p = v.p;
     a.x = v.xw;
     a.w = v.w;
-    a.partials = v.partials;
-    a.rr_all = v.rr_all;
-    a.pap_all = v.pap_all;
+    a.red = make_red(m, v);
+    a.part1 = v.part1;
     a.st = v.st;
-    a.rank = m.rank;
-    a.nranks = m.nranks;
     cudaError_t e = cudaSuccess;
     SEM_TMA_DISPATCH(m.N, e = launch_pdl(ax_tma_kernel<NN, true>, tma_grid<NN, true>(m.E, m.nsm),
                                          TmaLayout<NN, true>::NT, TmaLayout<NN, true>::SMEM, s, a));

@@ -1,5 +1,16 @@
-// cg_device.cuh -- device-side CG bookkeeping shared by the two K1 kernels
-// (ax_kernel<N,true> and ax_tma_kernel<N,true>).  Included by .cu files only.
+// cg_device.cuh -- device-side CG bookkeeping shared by K1 (ax_kernel<N,true>,
+// ax_tma_kernel<N,true>) and K2 (k2_kernel).  Included by .cu files only.
+//
+// Reductions are DEFERRED to the consumer: a producing kernel only writes one
+// partial per block (no atomics, no last-block tail); every block of the
+// consuming kernel re-reduces the few hundred partials in the same fixed order
+// (so all blocks, and all runs, see bit-identical scalars) while its own bulk
+// loads are already in flight.  Scalars of iteration k:
+//     rho_k  = (r_k, r_k)_c   partials of K2(k-1)  (K2(-1) = the CG start)
+//     pap_k  = (p_k, A p_k)   partials of K1(k)
+//     alpha_k = rho_k / pap_k,  beta_k = rho_k / rho_{k-1}
+// With nranks > 1 a one-block kernel folds the partials into this rank's
+// value, NCCL all-gathers it, and consumers sum the ranks in ascending order.
 #pragma once
 #include <cstdlib>
 
@@ -7,17 +18,9 @@
 
 namespace sem {
 
-struct CgStep {
-    bool done;            // stopping rule fired (or fired earlier): kernel is a no-op
-    int k;                // current iteration
-    double beta;          // rho_k / rho_{k-1}  (0 at k = 0)
-    double alpha_prev;    // alpha_{k-1}        (0 at k = 0)
-};
-
 // Programmatic dependent launch: the CG kernels are launched with
-// programmaticStreamSerialization; each waits for its predecessor's memory
-// before touching data the predecessor produced, and lets its successor
-// launch early (its launch latency and static-data prologue then overlap).
+// programmaticStreamSerialization (opt-in, SEM_PDL=1); each waits for its
+// predecessor's memory before touching data the predecessor produced.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -45,128 +48,192 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-// Deterministic block reduction: fixed shuffle tree per warp, then thread 0
-// sums the warp results in warp order.  Valid in thread 0 only.
-template <int NT>
-__device__ __forceinline__ double block_sum(double v, double *red) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    constexpr int NW = (NT + 31) / 32;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    __syncthreads();
-    if (lane == 0) red[wid] = v;
-    __syncthreads();
-    double s = 0.0;
-    if (threadIdx.x == 0) {
-        for (int q = 0; q < NW; ++q) s += red[q];
-    }
-    return s;
-}
-
-// Fixed-order sum of cnt partials by one whole block (deterministic for a
-// fixed blockDim).  The first 16*NT partials are loaded in one unrolled batch
-// (one L2 round trip instead of a dependent chain).  Valid in thread 0.
-template <int NT>
-__device__ double block_sum_array(const double *a, int cnt, double *red) {
-    constexpr int PER = 16;
-    double v[PER];
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const int t = threadIdx.x + q * NT;
-        v[q] = (t < cnt) ? __ldcg(a + t) : 0.0;
-    }
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q < PER; ++q) s += v[q];
-    for (int t = threadIdx.x + PER * NT; t < cnt; t += NT) s += __ldcg(a + t);
-    return block_sum<NT>(s, red);
-}
-
-// Last-block-done protocol: every block has written its partial (thread 0);
-// returns true in the block that arrived last, which then sees all partials.
-// Only thread 0 fences: the other threads' stores need not be ordered.
-__device__ __forceinline__ bool last_block(uint32_t *ticket, int *sflag) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const uint32_t t = atomicAdd(ticket, 1u);
-        *sflag = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    const bool last = *sflag;
-    if (last) __threadfence();
-    return last;
-}
-
-// gpu-scope relaxed load of a state word written by an earlier kernel (or the
-// last block of this one): no system-scope strong access, no L1 reuse.
+// gpu-scope relaxed load of a state word written by an earlier kernel.
 __device__ __forceinline__ int32_t ld_state(const int32_t *p) {
     int32_t v;
     asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 
-__device__ __forceinline__ double sum_rank_slot(const double *rr_all, int slot, int nranks) {
-    double s = 0.0;
-    for (int q = 0; q < nranks; ++q) s += __ldcg(rr_all + slot * nranks + q);
-    return s;
+// Deterministic block reduction of NV values per thread: fixed shuffle tree
+// per warp, then the warp results summed in warp order.  Result in every
+// thread (broadcast through shared memory).  red: >= NV * (NT/32) doubles.
+template <int NT, int NV>
+__device__ __forceinline__ void block_sum_vec(double (&v)[NV], double *red) {
+    constexpr int NW = (NT + 31) / 32;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < NV; ++q) red[q * NW + wid] = v[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        double s = 0.0;
+        for (int w = 0; w < NW; ++w) s += red[q * NW + w];
+        v[q] = s;
+    }
+    __syncthreads();
 }
 
-// ---------------------------------------------------------------------------
-// CG scalar bookkeeping.  The kernel that completes a global reduction (its
-// last block, or a one-thread finaliser after the multi-rank all-gather)
-// derives the next scalars, so a consumer kernel needs ONE round trip of
-// independent loads, not a chain.
-// ---------------------------------------------------------------------------
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double *red) {
+    double a[1] = {v};
+    block_sum_vec<NT, 1>(a, red);
+    return a[0];
+}
 
-// End of iteration k (k_next = k + 1), or CG start (k_next = 0, rho = rho_0):
-// records rho_{k+1}, beta_{k+1} = rho_{k+1} / rho_k, alpha_k for K1's deferred
-// x update, advances k, and evaluates the stopping rule of SURVEY.md §8(c) O7
-// for iteration k_next: stop when k_next >= maxit or sqrt(rho) <= tol sqrt(rho_0)
-// (rho_0 == 0: stop with rel_res 0).  The done flag is sticky: every later
-// kernel of this solve is a no-op.  One thread.
-__device__ __forceinline__ void cg_finalize_rho(CgState *st, int k_next, double rho) {
-    double rho0;
-    if (k_next == 0) {
-        rho0 = rho;
-        st->rho0 = rho;
-        st->beta = 0.0;
-        st->alpha_km1 = 0.0;
+// Where the per-block partials of the two reductions live (see top).
+struct CgRed {
+    const double *part1;   // [2][s1] K1 partials of (p, A p), parity of k
+    const double *part2;   // [2][s2] K2 partials of (r, r), parity of the producing k
+    int nb1, s1, nb2, s2;
+    const double *pap_all; // nranks > 1: [4][nranks] all-gathered rank values
+    const double *rr_all;
+    int nranks;
+};
+
+inline CgRed make_red(const DevMesh &m, const CgVecs &v) {
+    CgRed R;
+    R.part1 = v.part1;
+    R.part2 = v.part2;
+    R.nb1 = v.nb1;
+    R.s1 = v.s1;
+    R.nb2 = v.nb2;
+    R.s2 = v.s2;
+    R.pap_all = v.pap_all;
+    R.rr_all = v.rr_all;
+    R.nranks = m.nranks;
+    return R;
+}
+
+// Location of the values whose ordered sum is rho_k / pap_k.
+__device__ __forceinline__ void rho_src(const CgRed &R, int k, const double *&p, int &n) {
+    if (R.nranks == 1) {
+        p = R.part2 + ((k - 1) & 1) * R.s2;
+        n = R.nb2;
     } else {
-        rho0 = st->rho0;
-        st->beta = rho / st->rho_cur;
-        st->alpha_km1 = st->alpha_k;
+        p = R.rr_all + (k & 3) * R.nranks;
+        n = R.nranks;
     }
-    st->rho_cur = rho;
-    bool done;
-    if (k_next == 0 && rho0 == 0.0) done = true;
-    else done = !(k_next < st->maxit && sqrt(rho) > st->tol * sqrt(rho0));
-    if (done) {
-        st->iters = k_next;
-        st->rel_res = (rho0 == 0.0) ? 0.0 : sqrt(rho) / sqrt(rho0);
-        st->converged = (rho0 == 0.0) || !(sqrt(rho) > st->tol * sqrt(rho0));
+}
+__device__ __forceinline__ void pap_src(const CgRed &R, int k, const double *&p, int &n) {
+    if (R.nranks == 1) {
+        p = R.part1 + (k & 1) * R.s1;
+        n = R.nb1;
+    } else {
+        p = R.pap_all + (k & 3) * R.nranks;
+        n = R.nranks;
     }
-    __threadfence();
-    st->kcur = k_next;
-    if (done) st->done = 1;
 }
 
-// After K1 of iteration k: alpha_k = rho_k / (p, A p).  One thread.
-__device__ __forceinline__ void cg_finalize_pap(CgState *st, double pap) {
-    st->alpha_k = st->rho_cur / pap;
+// Block-cooperative ordered sums of NV sources (each <= ~1000 values): every
+// thread loads its share of all sources in one batch (one round trip), then
+// one block reduction.  Identical result in every block.
+template <int NT, int NV>
+__device__ __forceinline__ void block_sums(const double *const (&src)[NV], const int (&cnt)[NV],
+                                           double (&out)[NV], double *red) {
+    constexpr int PER = 8;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        double v[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int t = threadIdx.x + u * NT;
+            v[u] = (t < cnt[q]) ? __ldcg(src[q] + t) : 0.0;
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int u = 0; u < PER; ++u) s += v[u];
+        for (int t = threadIdx.x + PER * NT; t < cnt[q]; t += NT) s += __ldcg(src[q] + t);
+        out[q] = s;
+    }
+    block_sum_vec<NT, NV>(out, red);
 }
 
-// K1 prologue: one round trip of independent state loads.
-__device__ __forceinline__ CgStep cg_k1_prologue(CgState *st) {
+// Stopping rule of SURVEY.md §8(c) O7 before iteration k: stop when
+// k >= maxit or sqrt(rho_k) <= tol sqrt(rho_0); rho_0 == 0 stops at once.
+__device__ __forceinline__ bool cg_stop(int k, double rho, double rho0, int maxit, double tol) {
+    if (k == 0 && rho0 == 0.0) return true;
+    return !(k < maxit && sqrt(rho) > tol * sqrt(rho0));
+}
+
+struct CgStep {
+    bool done;            // stop before this iteration (or stopped earlier): no-op
+    int k;                // current iteration
+    double beta;          // beta_k  (0 at k = 0)
+    double alpha_prev;    // alpha_{k-1} (0 at k = 0)
+};
+
+// K1 prologue (all threads of the block; contains __syncthreads): k, the
+// stopping decision, beta_k and alpha_{k-1}.  Block 0 records a stop for the
+// host (iters, rel_res, alpha_{it-1} for the final x update, the sticky flag)
+// and, at k = 0, rho_0.
+template <int NT>
+__device__ __forceinline__ CgStep cg_k1_prologue(CgState *st, const CgRed &R, double *red) {
     CgStep c{};
     const int done = ld_state(&st->done);
-    const int k = ld_state(&st->kcur);
-    const double beta = __ldcg(&st->beta);
-    const double am1 = __ldcg(&st->alpha_km1);
-    c.done = done != 0;
+    const int k = ld_state(&st->k1);
     c.k = k;
-    c.beta = beta;
-    c.alpha_prev = am1;
+    if (done) {
+        c.done = true;
+        return c;
+    }
+    const double *src[3];
+    int cnt[3];
+    rho_src(R, k, src[0], cnt[0]);          // rho_k
+    rho_src(R, k - 1, src[1], cnt[1]);      // rho_{k-1}
+    pap_src(R, k - 1, src[2], cnt[2]);      // pap_{k-1}
+    if (k == 0) cnt[1] = cnt[2] = 0;
+    double v[3];
+    block_sums<NT, 3>(src, cnt, v, red);
+    const double rho = v[0], rho_m1 = v[1], pap_m1 = v[2];
+    const double rho0 = (k == 0) ? rho : __ldcg(&st->rho0);
+    const double alpha_prev = (k == 0) ? 0.0 : rho_m1 / pap_m1;
+    c.beta = (k == 0) ? 0.0 : rho / rho_m1;
+    c.alpha_prev = alpha_prev;
+    c.done = cg_stop(k, rho, rho0, st->maxit, st->tol);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (k == 0) st->rho0 = rho0;
+        st->k2 = k;                      // for K2 of this iteration
+        if (c.done) {
+            st->iters = k;
+            st->rel_res = (rho0 == 0.0) ? 0.0 : sqrt(rho) / sqrt(rho0);
+            st->converged = (rho0 == 0.0) || !(sqrt(rho) > st->tol * sqrt(rho0));
+            st->alpha_km1 = alpha_prev;
+            __threadfence();
+            st->done = 1;
+        }
+    }
+    return c;
+}
+
+// K2 prologue (all threads): k, the same stopping decision, alpha_k.
+template <int NT>
+__device__ __forceinline__ CgStep cg_k2_prologue(CgState *st, const CgRed &R, double *red,
+                                                 double &alpha) {
+    CgStep c{};
+    const int done = ld_state(&st->done);
+    const int k = ld_state(&st->k2);
+    c.k = k;
+    if (done) {
+        c.done = true;
+        return c;
+    }
+    const double *src[2];
+    int cnt[2];
+    rho_src(R, k, src[0], cnt[0]);          // rho_k
+    pap_src(R, k, src[1], cnt[1]);          // pap_k
+    double v[2];
+    block_sums<NT, 2>(src, cnt, v, red);
+    const double rho0 = (k == 0) ? v[0] : __ldcg(&st->rho0);
+    c.done = cg_stop(k, v[0], rho0, st->maxit, st->tol);
+    alpha = v[0] / v[1];
+    if (blockIdx.x == 0 && threadIdx.x == 0 && !c.done) st->k1 = k + 1;   // for K1 of k+1
     return c;
 }
 

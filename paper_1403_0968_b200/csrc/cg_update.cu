@@ -26,14 +26,11 @@ struct K2Args {
     const double *w;
     const double *b;          // INIT only
     double *r;
-    double *partials;
-    double *rr_all;
-    const double *pap_all;
+    CgRed red;                // where the scalar reductions live
+    double *part2;            // this kernel's (r, r) partials, [2][s2]
     CgState *st;
-    int rank, nranks;
     int32_t cchunk[kMaxClasses + 1];   // first chunk of each class; cchunk[n] = interior
     int32_t nchunks;
-    int32_t dbg;                       // timing experiments only (SEM_K2_DEBUG), 0 in production
 };
 
 constexpr int kK2Threads = 256;
@@ -88,18 +85,15 @@ __device__ __forceinline__ double k2_groups(const K2Args &a, const int32_t *__re
 template <int N, bool INIT>
 __global__ void __launch_bounds__(kK2Threads) k2_kernel(const __grid_constant__ K2Args a) {
     constexpr int n = N + 1, n2 = n * n, n3 = n2 * n, ni = N - 1;   // interior extent
-    __shared__ double sred[kK2Threads / 32];
-    __shared__ int sflag;
+    __shared__ double sred[2 * (kK2Threads / 32)];
     if constexpr (!INIT) pdl_trigger();
     double alpha = 0.0;
-    int k = 0;
+    int k = -1;               // INIT produces the partials of rho_0 as "iteration -1"
     if constexpr (!INIT) {
         pdl_wait();
-        // one round trip of independent loads (alpha_k was derived by K1)
-        const int done = ld_state(&a.st->done);
-        k = ld_state(&a.st->kcur);
-        alpha = __ldcg(&a.st->alpha_k);
-        if (done) return;
+        const CgStep c = cg_k2_prologue<kK2Threads>(a.st, a.red, sred, alpha);
+        if (c.done) return;
+        k = c.k;
     }
 
     double part = 0.0;
@@ -110,8 +104,6 @@ __global__ void __launch_bounds__(kK2Threads) k2_kernel(const __grid_constant__ 
     // chunk is one dependent round trip (indices, then values).
     const int ncls = a.cls.n;
     for (int ch = blockIdx.x; ch < a.nchunks; ch += gridDim.x) {
-        if ((a.dbg & 1) && ch < a.cchunk[ncls]) continue;
-        if ((a.dbg & 2) && ch >= a.cchunk[ncls]) continue;
         if (ch < a.cchunk[ncls]) {
             int c = 0;
             while (ch >= a.cchunk[c + 1]) ++c;
@@ -180,24 +172,9 @@ __global__ void __launch_bounds__(kK2Threads) k2_kernel(const __grid_constant__ 
         }
     }
 
-    if (a.dbg & 4) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            const int kn = INIT ? 0 : k + 1;
-            if (a.nranks == 1) cg_finalize_rho(a.st, kn, part + 1.0);
-        }
-        return;
-    }
+    // one deterministic partial per block; consumers reduce (cg_device.cuh)
     const double bs = block_sum<kK2Threads>(part, sred);
-    if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
-    if (last_block(&a.st->ticket[1], &sflag)) {
-        const double tot = block_sum_array<kK2Threads>(a.partials, gridDim.x, sred);
-        if (threadIdx.x == 0) {
-            a.st->ticket[1] = 0;
-            const int kn = INIT ? 0 : k + 1;
-            if (a.nranks == 1) cg_finalize_rho(a.st, kn, tot);
-            else a.rr_all[(kn & 3) * a.nranks + a.rank] = tot;
-        }
-    }
+    if (threadIdx.x == 0) a.part2[(k & 1) * a.red.s2 + blockIdx.x] = bs;
 }
 
 #define SEM_K2_DISPATCH(N_, ...)                                             \
@@ -220,7 +197,8 @@ __global__ void __launch_bounds__(kK2Threads) k2_kernel(const __grid_constant__ 
     default: break;                                                          \
     }
 
-int k2_blocks(int nsm) { return nsm * kK2BlocksPerSM; }
+// Same grid for the start and the iterations: it is the count of (r,r) partials.
+int k2_blocks(const DevMesh &m, bool) { return m.nsm * kK2BlocksPerSM; }
 
 cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t s) {
     K2Args a{};
@@ -231,12 +209,9 @@ cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t
     a.w = v.w;
     a.b = v.b;
     a.r = v.r;
-    a.partials = v.partials;
-    a.rr_all = v.rr_all;
-    a.pap_all = v.pap_all;
+    a.red = make_red(m, v);
+    a.part2 = v.part2;
     a.st = v.st;
-    a.rank = m.rank;
-    a.nranks = m.nranks;
     // chunk table (Dirichlet classes only at INIT)
     int nch = 0;
     for (int c = 0; c < m.cls.n; ++c) {
@@ -249,13 +224,7 @@ cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t
     const int64_t nint = m.E * int64_t(m.N - 1) * (m.N - 1) * (m.N - 1);
     nch += (int)((nint + 4 * kK2Threads - 1) / (4 * kK2Threads));
     a.nchunks = nch;
-    static const int dbg = [] {
-        const char *e = getenv("SEM_K2_DEBUG");
-        return e ? atoi(e) : 0;
-    }();
-    a.dbg = init ? 0 : dbg;
-    int nb = k2_blocks(m.nsm);
-    if (nb > nch) nb = nch > 0 ? nch : 1;
+    const int nb = k2_blocks(m, init);
     cudaError_t e = cudaSuccess;
     if (init) {
         SEM_K2_DISPATCH(m.N, (k2_kernel<NN, true><<<nb, kK2Threads, 0, s>>>(a), e = cudaGetLastError()));

@@ -222,12 +222,8 @@ Layout make_layout(int N, int64_t E, int nranks) {
     const int64_t n = N + 1, n3 = n * n * n, L = E * n3;
     const int64_t ni = (n >= 2) ? (n - 2) : 0;
     Lo.nsurf_cap = E * (n3 - ni * ni * ni);
-    // partial slots for the Ax kernels: simple kernel blocks, or a persistent
-    // TMA grid (<= one CTA per SM, <= E)
-    const int nb_ax = std::max<int>(ax_blocks(N, E), (int)std::min<int64_t>(E, 1024));
-    const int64_t nb_gs = (Lo.nsurf_cap + kGsThreads - 1) / kGsThreads + 1;
-    // per-block partials: the Ax kernels, or K2 (group blocks + interior blocks)
-    Lo.partial_cap = std::max<int64_t>(nb_ax, nb_gs + 148 * 8) + 16;
+    // per-block partials of K1 / K2: both grids are <= 4 CTAs per SM
+    Lo.partial_cap = kMaxPartials;
     size_t o = 0;
     auto take = [&](size_t bytes) {
         size_t at = o;
@@ -242,7 +238,7 @@ Layout make_layout(int N, int64_t E, int nranks) {
     Lo.xw = take(sizeof(double) * L);
     Lo.D = take(sizeof(double) * (n * n + n));
     Lo.gs_idx = take(sizeof(int32_t) * Lo.nsurf_cap);
-    Lo.partials = take(sizeof(double) * Lo.partial_cap);
+    Lo.partials = take(sizeof(double) * 4 * Lo.partial_cap);   // part1[2][cap], part2[2][cap]
     Lo.rr_all = take(sizeof(double) * kRing * nranks);
     Lo.pap_all = take(sizeof(double) * kRing * nranks);
     Lo.st = take(sizeof(CgState));
@@ -484,7 +480,9 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
     cv.p = reinterpret_cast<double *>(ws + Lo.p);
     cv.w = reinterpret_cast<double *>(ws + Lo.w);
     cv.xw = reinterpret_cast<double *>(ws + Lo.xw);
-    cv.partials = reinterpret_cast<double *>(ws + Lo.partials);
+    cv.part1 = reinterpret_cast<double *>(ws + Lo.partials);
+    cv.part2 = cv.part1 + 2 * Lo.partial_cap;
+    cv.s1 = cv.s2 = (int)Lo.partial_cap;
     cv.rr_all = reinterpret_cast<double *>(ws + Lo.rr_all);
     cv.pap_all = reinterpret_cast<double *>(ws + Lo.pap_all);
     cv.st = reinterpret_cast<CgState *>(ws + Lo.st);
@@ -497,7 +495,12 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         const char *gr = getenv("SEM_CG_GRAPH");
         ctx->use_graph = !(gr && strcmp(gr, "0") == 0);
     }
-    ctx->nb_ax = dm.use_tma ? tma_blocks(N, ctx->E, dm.nsm, true) : ax_blocks(N, ctx->E);
+    cv.nb1 = ax_cg_blocks(dm);
+    cv.nb2 = k2_blocks(dm, false);
+    if (cv.nb1 > cv.s1 || cv.nb2 > cv.s2) {
+        fail(nullptr, SEM_EINVAL, "device has too many SMs for the partial buffers");
+        return bail(SEM_EINVAL);
+    }
 
     rc = [&]() -> int {
         const int n = ctx->n;
@@ -521,7 +524,7 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         CU(cudaMemsetAsync(cv.pap_all, 0, sizeof(double) * kRing * ctx->nranks, s));
         // xyz -> device (temporarily in r|p|w, exactly 3L doubles), then G^, B
         double *xyz_d = cv.r;
-        int *bad_d = reinterpret_cast<int *>(cv.partials);
+        int *bad_d = reinterpret_cast<int *>(cv.part1);
         CU(cudaMemcpyAsync(xyz_d, mesh->xyz, sizeof(double) * 3 * ctx->L, cudaMemcpyHostToDevice, s));
         CU(cudaMemsetAsync(bad_d, 0, sizeof(int), s));
         LAUNCH(launch_geom(dm, xyz_d, const_cast<double *>(dm.G), const_cast<double *>(dm.BM),
@@ -654,13 +657,13 @@ static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
     int rc;
     LAUNCHP(kProfAxCg, (k == 0 ? 72.0 : 96.0) * ctx->L, k, launch_ax_cg(ctx->dm, v, s));
     if (P > 1) {
+        LAUNCH(launch_cg_red_pap(ctx->dm, v, s));
         if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P, s))) return rc;
-        LAUNCH(launch_cg_fin_pap(ctx->dm, v, s));
     }
     LAUNCHP(kProfK2, k2_bytes(ctx), k, launch_k2(ctx->dm, v, false, s));
     if (P > 1) {
+        LAUNCH(launch_cg_red_rr(ctx->dm, v, s));
         if ((rc = allgather_scalar(ctx, v.rr_all + ((k + 1) & 3) * P, s))) return rc;
-        LAUNCH(launch_cg_fin_rho(ctx->dm, v, false, s));
     }
     return SEM_OK;
 }
@@ -712,8 +715,8 @@ extern "C" int sem_cg(sem_ctx *ctx, const double *b, double *x, double tol, int 
     LAUNCH(launch_cg_init(ctx->dm, v, s));
     LAUNCH(launch_k2(ctx->dm, v, true, s));
     if (P > 1) {
+        LAUNCH(launch_cg_red_rr(ctx->dm, v, s));
         if ((rc = allgather_scalar(ctx, v.rr_all + 0 * P, s))) return rc;
-        LAUNCH(launch_cg_fin_rho(ctx->dm, v, true, s));
     }
 
     // Iterations in chunks of kChunk (a multiple of 4: the all-gather slot of

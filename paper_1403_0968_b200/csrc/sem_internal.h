@@ -20,13 +20,9 @@ struct CgState {
     int32_t iters;              // iteration count at which it fired
     int32_t converged;          // 1 if sqrt(rho) <= tol sqrt(rho0) (or rho0 == 0)
     double rel_res;             // sqrt(rho_k / rho0)
-    double rho_cur;             // rho_k of the current iteration k
-    double beta;                // beta_k (0 at k = 0), for K1
-    double alpha_km1;           // alpha_{k-1} (0 at k = 0), for K1's deferred x update
-    double alpha_k;             // alpha_k, set after K1's (p, A p), for K2
-    uint32_t ticket[4];         // last-block-done counters: 0 = K1 (pAp), 1 = K2 (rr)
-    int32_t kcur;               // current CG iteration k (advanced at the end of K2)
-    int32_t pad_;
+    double alpha_km1;           // alpha_{it-1} at the stop, for the final x update
+    int32_t k1;                 // iteration of the next K1 (written by K2 / the CG start)
+    int32_t k2;                 // iteration of the next K2 (written by K1)
 };
 
 // Gather-scatter groups are stored by class (Dirichlet flag, multiplicity m):
@@ -65,22 +61,26 @@ struct CgVecs {
     double *x;                  // the caller's x of this solve (x0 in, solution out)
     double *xw;                 // workspace copy of x updated by K1 (graph-invariant pointer)
     double *r, *p, *w;
-    double *partials;           // [kPartialCap] per-block partial sums
-    double *rr_all;             // [kRing][nranks] rank partials of (r,r)_c
-    double *pap_all;            // [kRing][nranks] rank partials of (w,p)_c
+    double *part1;              // [2][s1] per-block partials of (p, A p) (K1)
+    double *part2;              // [2][s2] per-block partials of (r, r) (K2)
+    int nb1, s1, nb2, s2;       // grids of K1 / K2 and buffer strides
+    double *rr_all;             // [kRing][nranks] rank values of (r,r)_c (nranks > 1)
+    double *pap_all;            // [kRing][nranks] rank values of (p,Ap) (nranks > 1)
     CgState *st;
 };
 
 constexpr int kGsThreads = 256;
+constexpr int kMaxPartials = 1024;     // per-block partial slots of K1 / K2 (<= 4 CTAs/SM)
 
 // ---- launchers (sem_kernels.cu); all return cudaGetLastError() ----
 int ax_blocks(int N, int64_t E);      // grid size of the Ax kernels for E elements
 cudaError_t launch_geom(const DevMesh &m, const double *xyz, double *G, double *BM,
                         int *bad, cudaStream_t s);
 cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t s);
-// The CG kernels take the iteration k from CgState::kcur (device), so one
-// captured CUDA graph of a chunk of iterations is valid for every chunk.
+// The CG kernels take the iteration k from CgState (device), so one captured
+// CUDA graph of a chunk of iterations is valid for every chunk.
 cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+int ax_cg_blocks(const DevMesh &m);   // grid of K1 (= number of its partials)
 // mode: 0 = plain dssum, 1 = dssum + mask, 2 = CG iteration (dssum + mask,
 // programmatic dependent of K1, no-op after the stop; v needed)
 cudaError_t launch_gs(const DevMesh &m, double *w, int mode, const CgVecs *v, cudaStream_t s);
@@ -88,15 +88,15 @@ cudaError_t launch_mask(const DevMesh &m, double *w, cudaStream_t s);
 cudaError_t launch_mass(const DevMesh &m, const double *f, double *b, cudaStream_t s);
 // xw = x0, resets the CG state (k = 0)
 cudaError_t launch_cg_init(const DevMesh &m, const CgVecs &v, cudaStream_t s);
-// cg_update.cu, K2: Q Q^T w fused with the r update and (r,r)_c into
-// rr_all[(k+1) & 3][rank], k += 1; init: r0 = mask (b - Q Q^T w), rho_0 into slot 0
-int k2_blocks(int nsm);
+// cg_update.cu, K2: Q Q^T w + mask fused with the r update; per-block (r,r)
+// partials into part2[k & 1]; init: r0 = mask (b - Q Q^T w) into part2[1]
+int k2_blocks(const DevMesh &m, bool init);
 cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t s);
 cudaError_t launch_cg_finish(const DevMesh &m, const CgVecs &v, cudaStream_t s);
-// multi-rank: fold the all-gathered rank partials (ascending rank order) into
-// alpha_k, or into rho / beta / the stopping decision
-cudaError_t launch_cg_fin_pap(const DevMesh &m, const CgVecs &v, cudaStream_t s);
-cudaError_t launch_cg_fin_rho(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t s);
+// multi-rank: fold this rank's block partials (fixed order) into its slot of
+// pap_all / rr_all before the NCCL all-gather
+cudaError_t launch_cg_red_pap(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+cudaError_t launch_cg_red_rr(const DevMesh &m, const CgVecs &v, cudaStream_t s);
 
 // ax_tma.cu
 bool tma_supported(int N);

@@ -104,14 +104,13 @@ struct AxCfg {
 struct AxCgArgs {
     const double *r;
     double *p, *x;
-    double *partials;
-    double *pap_all;
-    int rank;
-    const double *rr_all;
+    CgRed red;
+    double *part1;
     CgState *st;
-    int nranks;
 };
 
+// Grid-stride over blocks of EPB elements (grid <= 4 CTAs per SM, so the
+// (p, A p) partials stay few).
 template <int N, bool CG>
 __global__ void __launch_bounds__(AxCfg<N>::NT)
 ax_kernel(int64_t E, const double *__restrict__ Dg, const double *__restrict__ G,
@@ -122,8 +121,7 @@ ax_kernel(int64_t E, const double *__restrict__ Dg, const double *__restrict__ G
     __shared__ double su[EPB][n3];
     __shared__ double sfr[EPB][n2];
     __shared__ double sfs[EPB][n2];
-    __shared__ int sflag;
-    __shared__ double sred[(NT + 31) / 32];
+    __shared__ double sred[3 * ((NT + 31) / 32)];
 
     double beta = 0.0, alpha_prev = 0.0;
     int kit = 0;
@@ -131,7 +129,7 @@ ax_kernel(int64_t E, const double *__restrict__ Dg, const double *__restrict__ G
     if constexpr (CG) {
         pdl_trigger();
         pdl_wait();
-        const CgStep c = cg_k1_prologue(cg.st);
+        const CgStep c = cg_k1_prologue<NT>(cg.st, cg.red, sred);
         if (c.done) return;
         beta = c.beta;
         alpha_prev = c.alpha_prev;
@@ -143,103 +141,99 @@ ax_kernel(int64_t E, const double *__restrict__ Dg, const double *__restrict__ G
     const int el = tid / n2;
     const int ij = tid - el * n2;
     const int i = ij % n, j = ij / n;
-    const int64_t e = (int64_t)blockIdx.x * EPB + el;
-    const bool active = e < E;
-    const int64_t base = e * n3 + ij;
+    const int64_t nblk = (E + EPB - 1) / EPB;
+    double part = 0.0;
+    for (int64_t eb = blockIdx.x; eb < nblk; eb += gridDim.x) {
+        const int64_t e = eb * EPB + el;
+        const bool active = e < E;
+        const int64_t base = e * n3 + ij;
 
-    double ru[n], rw[n];
-    if (active) {
-        if constexpr (CG) {
+        double ru[n], rw[n];
+        if (active) {
+            if constexpr (CG) {
 #pragma unroll
-            for (int k = 0; k < n; ++k) {
-                const int64_t l = base + k * n2;
-                const double rl = cg.r[l];
-                double pl;
-                if (kit == 0) {
-                    pl = rl;
-                } else {
-                    const double po = cg.p[l];
-                    xg[l] += alpha_prev * po;
-                    pl = rl + beta * po;
+                for (int k = 0; k < n; ++k) {
+                    const int64_t l = base + k * n2;
+                    const double rl = cg.r[l];
+                    double pl;
+                    if (kit == 0) {
+                        pl = rl;
+                    } else {
+                        const double po = cg.p[l];
+                        xg[l] += alpha_prev * po;
+                        pl = rl + beta * po;
+                    }
+                    cg.p[l] = pl;
+                    ru[k] = pl;
                 }
-                cg.p[l] = pl;
-                ru[k] = pl;
+            } else {
+#pragma unroll
+                for (int k = 0; k < n; ++k) ru[k] = u[base + k * n2];
             }
         } else {
 #pragma unroll
-            for (int k = 0; k < n; ++k) ru[k] = u[base + k * n2];
+            for (int k = 0; k < n; ++k) ru[k] = 0.0;
         }
-    } else {
+        __syncthreads();   // previous element block done with su / sfr / sfs
 #pragma unroll
-        for (int k = 0; k < n; ++k) ru[k] = 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < n; ++k) {
-        su[el][k * n2 + ij] = ru[k];
-        rw[k] = 0.0;
-    }
-    __syncthreads();
-
-    const double *Ge = G + e * 6 * n3 + ij;
-#pragma unroll
-    for (int k = 0; k < n; ++k) {
-        double ur = 0.0, us = 0.0, ut = 0.0;
-#pragma unroll
-        for (int m = 0; m < n; ++m) {
-            ur += sD[i * n + m] * su[el][k * n2 + j * n + m];
-            us += sD[j * n + m] * su[el][k * n2 + m * n + i];
-            ut += sD[k * n + m] * ru[m];
+        for (int k = 0; k < n; ++k) {
+            su[el][k * n2 + ij] = ru[k];
+            rw[k] = 0.0;
         }
-        double g0 = 0, g1 = 0, g2 = 0, g3 = 0, g4 = 0, g5 = 0;
-        if (active) {
-            const double *Gk = Ge + k * n2;
-            g0 = __ldg(Gk + 0 * n3);
-            g1 = __ldg(Gk + 1 * n3);
-            g2 = __ldg(Gk + 2 * n3);
-            g3 = __ldg(Gk + 3 * n3);
-            g4 = __ldg(Gk + 4 * n3);
-            g5 = __ldg(Gk + 5 * n3);
-        }
-        const double fr = g0 * ur + g1 * us + g2 * ut;
-        const double fs = g1 * ur + g3 * us + g4 * ut;
-        const double ft = g2 * ur + g4 * us + g5 * ut;
-        sfr[el][ij] = fr;
-        sfs[el][ij] = fs;
-#pragma unroll
-        for (int m = 0; m < n; ++m) rw[m] += sD[k * n + m] * ft;
         __syncthreads();
-        double acc = 0.0;
-#pragma unroll
-        for (int m = 0; m < n; ++m) {
-            acc += sD[m * n + i] * sfr[el][j * n + m];
-            acc += sD[m * n + j] * sfs[el][m * n + i];
-        }
-        rw[k] += acc;
-        __syncthreads();
-    }
 
-    if (active) {
+        const double *Ge = G + e * 6 * n3 + ij;
 #pragma unroll
-        for (int k = 0; k < n; ++k) wout[base + k * n2] = rw[k];
-    }
-    if constexpr (CG) {
-        // (p, mask Q Q^T A_L p)_c = sum_e p_e^T A_e p_e (p continuous, zero on
-        // the Dirichlet boundary); last block folds the partials in order.
-        double part = 0.0;
+        for (int k = 0; k < n; ++k) {
+            double ur = 0.0, us = 0.0, ut = 0.0;
+#pragma unroll
+            for (int m = 0; m < n; ++m) {
+                ur += sD[i * n + m] * su[el][k * n2 + j * n + m];
+                us += sD[j * n + m] * su[el][k * n2 + m * n + i];
+                ut += sD[k * n + m] * ru[m];
+            }
+            double g0 = 0, g1 = 0, g2 = 0, g3 = 0, g4 = 0, g5 = 0;
+            if (active) {
+                const double *Gk = Ge + k * n2;
+                g0 = __ldg(Gk + 0 * n3);
+                g1 = __ldg(Gk + 1 * n3);
+                g2 = __ldg(Gk + 2 * n3);
+                g3 = __ldg(Gk + 3 * n3);
+                g4 = __ldg(Gk + 4 * n3);
+                g5 = __ldg(Gk + 5 * n3);
+            }
+            const double fr = g0 * ur + g1 * us + g2 * ut;
+            const double fs = g1 * ur + g3 * us + g4 * ut;
+            const double ft = g2 * ur + g4 * us + g5 * ut;
+            sfr[el][ij] = fr;
+            sfs[el][ij] = fs;
+#pragma unroll
+            for (int m = 0; m < n; ++m) rw[m] += sD[k * n + m] * ft;
+            __syncthreads();
+            double acc = 0.0;
+#pragma unroll
+            for (int m = 0; m < n; ++m) {
+                acc += sD[m * n + i] * sfr[el][j * n + m];
+                acc += sD[m * n + j] * sfs[el][m * n + i];
+            }
+            rw[k] += acc;
+            __syncthreads();
+        }
+
         if (active) {
 #pragma unroll
-            for (int k = 0; k < n; ++k) part += rw[k] * ru[k];
-        }
-        const double s = block_sum<NT>(part, sred);
-        if (tid == 0) cg.partials[blockIdx.x] = s;
-        if (last_block(&cg.st->ticket[0], &sflag)) {
-            const double tot = block_sum_array<NT>(cg.partials, gridDim.x, sred);
-            if (tid == 0) {
-                if (cg.nranks == 1) cg_finalize_pap(cg.st, tot);
-                else cg.pap_all[(kit & 3) * cg.nranks + cg.rank] = tot;
-                cg.st->ticket[0] = 0;
+            for (int k = 0; k < n; ++k) wout[base + k * n2] = rw[k];
+            if constexpr (CG) {
+                // (p, mask Q Q^T A_L p)_c = sum_e p_e^T A_e p_e (p continuous,
+                // zero on the Dirichlet boundary)
+#pragma unroll
+                for (int k = 0; k < n; ++k) part += rw[k] * ru[k];
             }
         }
+    }
+    if constexpr (CG) {
+        const double s = block_sum<NT>(part, sred);
+        if (tid == 0) cg.part1[(kit & 1) * cg.red.s1 + blockIdx.x] = s;
     }
 }
 
@@ -357,24 +351,27 @@ __global__ void cg_init_kernel(int64_t L, CgState *st, const double *__restrict_
         st->iters = 0;
         st->converged = 0;
         st->rel_res = 0.0;
-        st->rho_cur = st->beta = st->alpha_km1 = st->alpha_k = 0.0;
-        st->ticket[0] = st->ticket[1] = 0;
-        st->kcur = 0;
+        st->alpha_km1 = 0.0;
+        st->k1 = 0;
+        st->k2 = 0;
     }
 }
 
-// Multi-rank finalisers (one thread), after the all-gather of the rank partials:
-// sum them in ascending rank order and derive the next scalars.
-__global__ void cg_fin_pap_kernel(CgState *st, const double *pap_all, int nranks) {
+// Multi-rank: this rank's value = ordered sum of its block partials, into its
+// slot of the all-gather buffer (slot k & 3 for (p,Ap)_k, k_next & 3 for rho).
+constexpr int kRedThreads = 256;
+__global__ void __launch_bounds__(kRedThreads) cg_red_kernel(const double *part, int s, int nb,
+                                                             double *all, const CgState *st,
+                                                             int which, int rank, int nranks) {
+    __shared__ double sred[kRedThreads / 32];
     if (ld_state(&st->done)) return;
-    const int k = ld_state(&st->kcur);
-    cg_finalize_pap(st, sum_rank_slot(pap_all, k & 3, nranks));
-}
-
-__global__ void cg_fin_rho_kernel(CgState *st, const double *rr_all, int nranks, int init) {
-    if (ld_state(&st->done)) return;
-    const int kn = init ? 0 : ld_state(&st->kcur) + 1;
-    cg_finalize_rho(st, kn, sum_rank_slot(rr_all, kn & 3, nranks));
+    // (p,Ap): K1 of iteration k = st->k2.  rho: K2 of iteration k1 - 1 (k1 = k_next).
+    const int kk = (which == 0) ? ld_state(&st->k2) : ld_state(&st->k1);
+    const double *src = part + ((which == 0 ? kk : kk - 1) & 1) * s;
+    double v = 0.0;
+    for (int t = threadIdx.x; t < nb; t += kRedThreads) v += __ldcg(src + t);
+    v = block_sum<kRedThreads>(v, sred);
+    if (threadIdx.x == 0) all[(kk & 3) * nranks + rank] = v;
 }
 
 // x = xw + alpha_{it-1} p_{it-1}: the update K1 would have applied next.
@@ -421,6 +418,16 @@ int ax_blocks(int N, int64_t E) {
     return nb;
 }
 
+// grid of the simple Ax kernels: grid-stride, at most 4 CTAs per SM
+static int ax_grid(int N, int64_t E, int nsm) {
+    const int nb = ax_blocks(N, E);
+    return nb < 4 * nsm ? (nb < 1 ? 1 : nb) : 4 * nsm;
+}
+
+int ax_cg_blocks(const DevMesh &m) {
+    return m.use_tma ? tma_blocks(m.N, m.E, m.nsm, true) : ax_grid(m.N, m.E, m.nsm);
+}
+
 static int grid_for(int64_t L, int threads) {
     int64_t b = (L + threads - 1) / threads;
     if (b > 148 * 16) b = 148 * 16;
@@ -439,16 +446,16 @@ cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t
     if (m.E == 0) return cudaSuccess;
     if (m.use_tma) return launch_ax_tma(m, u, w, s);
     AxCgArgs none{};
-    SEM_DISPATCH_N(m.N, (ax_kernel<NN, false><<<ax_blocks_t<NN>(m.E), AxCfg<NN>::NT, 0, s>>>(
+    SEM_DISPATCH_N(m.N, (ax_kernel<NN, false><<<ax_grid(m.N, m.E, m.nsm), AxCfg<NN>::NT, 0, s>>>(
                              m.E, m.D, m.G, u, w, none)));
     return cudaGetLastError();
 }
 
 cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
     if (m.use_tma) return launch_ax_cg_tma(m, v, s);
-    AxCgArgs a{v.r, v.p, v.xw, v.partials, v.pap_all, m.rank, v.rr_all, v.st, m.nranks};
+    AxCgArgs a{v.r, v.p, v.xw, make_red(m, v), v.part1, v.st};
     cudaError_t e = cudaSuccess;
-    SEM_DISPATCH_N(m.N, (e = launch_pdl(ax_kernel<NN, true>, ax_blocks_t<NN>(m.E), AxCfg<NN>::NT,
+    SEM_DISPATCH_N(m.N, (e = launch_pdl(ax_kernel<NN, true>, ax_grid(m.N, m.E, m.nsm), AxCfg<NN>::NT,
                                         0, s, m.E, m.D, m.G, (const double *)nullptr, v.w, a)));
     return e;
 }
@@ -488,13 +495,15 @@ cudaError_t launch_cg_init(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_cg_fin_pap(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
-    cg_fin_pap_kernel<<<1, 1, 0, s>>>(v.st, v.pap_all, m.nranks);
+cudaError_t launch_cg_red_pap(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
+    cg_red_kernel<<<1, kRedThreads, 0, s>>>(v.part1, v.s1, v.nb1, v.pap_all, v.st, 0, m.rank,
+                                             m.nranks);
     return cudaGetLastError();
 }
 
-cudaError_t launch_cg_fin_rho(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t s) {
-    cg_fin_rho_kernel<<<1, 1, 0, s>>>(v.st, v.rr_all, m.nranks, init ? 1 : 0);
+cudaError_t launch_cg_red_rr(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
+    cg_red_kernel<<<1, kRedThreads, 0, s>>>(v.part2, v.s2, v.nb2, v.rr_all, v.st, 1, m.rank,
+                                             m.nranks);
     return cudaGetLastError();
 }
 
