@@ -29,12 +29,13 @@ struct K2Args {
     CgRed red;                // where the scalar reductions live
     double *part2;            // this kernel's (r, r) partials, [2][s2]
     CgState *st;
-    int32_t cchunk[kMaxClasses + 1];   // first chunk of each class; cchunk[n] = interior
+    int32_t nich;                      // element-interior chunks (first)
+    int32_t cchunk[kMaxClasses + 1];   // then: first group chunk of each class
     int32_t nchunks;
 };
 
 constexpr int kK2Threads = 256;
-constexpr int kK2BlocksPerSM = 4;
+constexpr int kK2BlocksPerSM = 3;
 
 // groups per thread in one chunk, by multiplicity
 __host__ __device__ constexpr int k2_upb(int m) {
@@ -82,78 +83,45 @@ __device__ __forceinline__ double k2_groups(const K2Args &a, const int32_t *__re
     return part;
 }
 
+// Element-interior nodes of one chunk (m = 1, never Dirichlet): local
+// indices of this thread's U nodes (-1 past the end), i fastest.
+template <int N, int U>
+__device__ __forceinline__ void k2_interior_idx(int64_t E, int chunk, int (&l)[U]) {
+    constexpr int n = N + 1, n2 = n * n, n3 = n2 * n, ni = N - 1, NI3 = ni * ni * ni;
+    const int nint = (int)(E * NI3);
+    const int t0 = chunk * kK2Threads * U + threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int t = t0 + u * kK2Threads;
+        const int tt = t < nint ? t : 0;
+        const int e = tt / NI3;
+        const int q = tt - e * NI3;
+        const int ii = q % ni, jj = (q / ni) % ni, kk = q / (ni * ni);
+        l[u] = (t < nint) ? e * n3 + (kk + 1) * n2 + (jj + 1) * n + (ii + 1) : -1;
+    }
+}
+
 template <int N, bool INIT>
-__global__ void __launch_bounds__(kK2Threads) k2_kernel(const __grid_constant__ K2Args a) {
-    constexpr int n = N + 1, n2 = n * n, n3 = n2 * n, ni = N - 1;   // interior extent
+__global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __grid_constant__ K2Args a) {
+    constexpr int ni = N - 1;
+    constexpr int U = 4;
     __shared__ double sred[2 * (kK2Threads / 32)];
     if constexpr (!INIT) pdl_trigger();
-    double alpha = 0.0;
-    int k = -1;               // INIT produces the partials of rho_0 as "iteration -1"
-    if constexpr (!INIT) {
-        pdl_wait();
-        const CgStep c = cg_k2_prologue<kK2Threads>(a.st, a.red, sred, alpha);
-        if (c.done) return;
-        k = c.k;
-    }
+    if constexpr (!INIT) pdl_wait();
 
-    double part = 0.0;
-    // Work is cut into chunks of one thread-batch per block: chunks
-    // [cchunk[c], cchunk[c+1]) cover class c (kK2Threads * U_m groups each),
-    // chunks from cchunk[n] on cover the element-interior nodes (kK2Threads * 4
-    // nodes each).  A block walks chunks blockIdx.x, +gridDim.x, ...; every
-    // chunk is one dependent round trip (indices, then values).
-    const int ncls = a.cls.n;
-    for (int ch = blockIdx.x; ch < a.nchunks; ch += gridDim.x) {
-        if (ch < a.cchunk[ncls]) {
-            int c = 0;
-            while (ch >= a.cchunk[c + 1]) ++c;
-            const int cnt = a.cls.start[c + 1] - a.cls.start[c];
-            const int m = a.cls.m[c];
-            const int32_t *ix = a.idx + a.cls.idxoff[c];
-            const int base = (ch - a.cchunk[c]) * kK2Threads * k2_upb(m) + threadIdx.x;
-            if (a.cls.dir[c]) {
-                // Dirichlet (INIT only): r0 = 0 at every copy (mask)
-                for (int u = 0; u < k2_upb(m); ++u) {
-                    const int q = base + u * kK2Threads;
-                    if (q < cnt)
-                        for (int t = 0; t < m; ++t) a.r[__ldg(ix + t * cnt + q)] = 0.0;
-                }
-                continue;
-            }
-            switch (m) {
-            case 1: part += k2_groups<1, 4, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
-            case 2: part += k2_groups<2, 4, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
-            case 4: part += k2_groups<4, 2, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
-            case 8: part += k2_groups<8, 1, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
-            default: {
-                const int q = base;
-                if (q < cnt) {
-                    double s = a.w[__ldg(ix + q)];
-                    for (int t = 1; t < m; ++t) s += a.w[__ldg(ix + t * cnt + q)];
-                    const double r0 = INIT ? a.b[__ldg(ix + q)] : a.r[__ldg(ix + q)];
-                    const double rn = INIT ? r0 - s : r0 - alpha * s;
-                    for (int t = 0; t < m; ++t) a.r[__ldg(ix + t * cnt + q)] = rn;
-                    part += rn * rn;
-                }
-            } break;
-            }
-        } else if constexpr (ni > 0) {
-            // element-interior nodes (m = 1, never Dirichlet), i fastest
-            constexpr int U = 4;
-            constexpr int NI3 = ni * ni * ni;
-            const int nint = (int)(a.E * NI3);
-            const int t0 = (ch - a.cchunk[ncls]) * kK2Threads * U + threadIdx.x;
-            int l[U];
-            double rv[U], wv[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int t = t0 + u * kK2Threads;
-                const int tt = t < nint ? t : 0;
-                const int e = tt / NI3;
-                const int q = tt - e * NI3;
-                const int ii = q % ni, jj = (q / ni) % ni, kk = q / (ni * ni);
-                l[u] = (t < nint) ? e * n3 + (kk + 1) * n2 + (jj + 1) * n + (ii + 1) : -1;
-            }
+    // Chunks: [0, nich) element-interior nodes (kK2Threads * U each), then
+    // [nich + cchunk[c], nich + cchunk[c+1]) the groups of class c
+    // (kK2Threads * U_m each).  A block walks chunks blockIdx.x, +gridDim.x, ...
+    // Its first chunk is interior whenever there are enough of them, and its
+    // loads are issued BEFORE the scalar prologue so they overlap it.
+    const int nich = a.nich;
+    int ch = blockIdx.x;
+    int l[U];
+    double rv[U], wv[U];
+    bool staged = false;
+    if constexpr (ni > 0) {
+        if (ch < nich) {
+            k2_interior_idx<N, U>(a.E, ch, l);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (l[u] >= 0) {
@@ -161,14 +129,76 @@ __global__ void __launch_bounds__(kK2Threads) k2_kernel(const __grid_constant__ 
                     wv[u] = __ldcs(a.w + l[u]);
                 }
             }
+            staged = true;
+        }
+    }
+
+    double alpha = 0.0;
+    int k = -1;               // INIT produces the partials of rho_0 as "iteration -1"
+    if constexpr (!INIT) {
+        const CgStep c = cg_k2_prologue<kK2Threads>(a.st, a.red, sred, alpha);
+        if (c.done) return;
+        k = c.k;
+    }
+
+    double part = 0.0;
+    for (; ch < a.nchunks; ch += gridDim.x) {
+        if (ch < nich) {
+            if constexpr (ni > 0) {
+                if (!staged) {
+                    k2_interior_idx<N, U>(a.E, ch, l);
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (l[u] >= 0) {
-                    const double rn = INIT ? rv[u] - wv[u] : rv[u] - alpha * wv[u];
-                    a.r[l[u]] = rn;
-                    part += rn * rn;
+                    for (int u = 0; u < U; ++u) {
+                        if (l[u] >= 0) {
+                            rv[u] = INIT ? a.b[l[u]] : a.r[l[u]];
+                            wv[u] = __ldcs(a.w + l[u]);
+                        }
+                    }
+                }
+                staged = false;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (l[u] >= 0) {
+                        const double rn = INIT ? rv[u] - wv[u] : rv[u] - alpha * wv[u];
+                        a.r[l[u]] = rn;
+                        part += rn * rn;
+                    }
                 }
             }
+            continue;
+        }
+        const int cg = ch - nich;
+        int c = 0;
+        while (cg >= a.cchunk[c + 1]) ++c;
+        const int cnt = a.cls.start[c + 1] - a.cls.start[c];
+        const int m = a.cls.m[c];
+        const int32_t *ix = a.idx + a.cls.idxoff[c];
+        const int base = (cg - a.cchunk[c]) * kK2Threads * k2_upb(m) + threadIdx.x;
+        if (a.cls.dir[c]) {
+            // Dirichlet (INIT only): r0 = 0 at every copy (mask)
+            for (int u = 0; u < k2_upb(m); ++u) {
+                const int q = base + u * kK2Threads;
+                if (q < cnt)
+                    for (int t = 0; t < m; ++t) a.r[__ldg(ix + t * cnt + q)] = 0.0;
+            }
+            continue;
+        }
+        switch (m) {
+        case 1: part += k2_groups<1, 4, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
+        case 2: part += k2_groups<2, 4, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
+        case 4: part += k2_groups<4, 2, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
+        case 8: part += k2_groups<8, 1, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
+        default: {
+            const int q = base;
+            if (q < cnt) {
+                double s = a.w[__ldg(ix + q)];
+                for (int t = 1; t < m; ++t) s += a.w[__ldg(ix + t * cnt + q)];
+                const double r0 = INIT ? a.b[__ldg(ix + q)] : a.r[__ldg(ix + q)];
+                const double rn = INIT ? r0 - s : r0 - alpha * s;
+                for (int t = 0; t < m; ++t) a.r[__ldg(ix + t * cnt + q)] = rn;
+                part += rn * rn;
+            }
+        } break;
         }
     }
 
@@ -212,7 +242,10 @@ cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t
     a.red = make_red(m, v);
     a.part2 = v.part2;
     a.st = v.st;
-    // chunk table (Dirichlet classes only at INIT)
+    // chunk table: interior chunks first, then the group classes (Dirichlet
+    // classes only at INIT)
+    const int64_t nint = m.E * int64_t(m.N - 1) * (m.N - 1) * (m.N - 1);
+    a.nich = (int)((nint + 4 * kK2Threads - 1) / (4 * kK2Threads));
     int nch = 0;
     for (int c = 0; c < m.cls.n; ++c) {
         a.cchunk[c] = nch;
@@ -221,9 +254,7 @@ cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t
         if (!m.cls.dir[c] || init) nch += (cnt + per - 1) / per;
     }
     a.cchunk[m.cls.n] = nch;
-    const int64_t nint = m.E * int64_t(m.N - 1) * (m.N - 1) * (m.N - 1);
-    nch += (int)((nint + 4 * kK2Threads - 1) / (4 * kK2Threads));
-    a.nchunks = nch;
+    a.nchunks = a.nich + nch;
     const int nb = k2_blocks(m, init);
     cudaError_t e = cudaSuccess;
     if (init) {
