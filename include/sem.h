@@ -159,6 +159,14 @@ int sem_nccl_get_unique_id(void *id_out);
  * non-Dirichlet surface group + 24 B per element-interior node; gather-scatter
  * 16 B per surface copy). */
 int sem_profile(sem_ctx *ctx, int enable);
+
+/* Benchmark helper (one rank): enqueue, as ONE CUDA graph on the context
+ * stream, `reps` back-to-back launches of one kernel of the CG iteration on the
+ * context's internal work vectors (which = 1: K1, 2: K2, 0: the Ax kernel),
+ * from a mid-solve state, so the caller can time the kernel with CUDA events
+ * around the call.  The caller's vectors are untouched; the internal CG state
+ * is left undefined until the next sem_cg.  Asynchronous. */
+int sem_kernel_replay(sem_ctx *ctx, int which, int reps);
 int sem_profile_read(sem_ctx *ctx, int which, double *ms, int64_t *launches, double *bytes);
 
 /* Number of kernels this context has launched so far (all entry points). */

@@ -52,6 +52,7 @@ struct sem_ctx {
     cudaStream_t cap_stream = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
     int64_t graph_kernels = 0;
+    cudaGraphExec_t replay_exec = nullptr;   // sem_kernel_replay
 };
 
 static constexpr int kChunk = 8;     // CG iterations per graph launch / poll (multiple of 4)
@@ -551,7 +552,9 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
 
 extern "C" void sem_free(sem_ctx *ctx) {
     if (!ctx) return;
+    if (ctx->graph_exec || ctx->replay_exec) cudaStreamSynchronize(ctx->stream);
     if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+    if (ctx->replay_exec) cudaGraphExecDestroy(ctx->replay_exec);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->comm) comm_free(ctx->comm);
     if (ctx->host_state) cudaFreeHost(ctx->host_state);
@@ -766,6 +769,53 @@ extern "C" int sem_cg(sem_ctx *ctx, const double *b, double *x, double tol, int 
 // ---------------------------------------------------------------------------
 // profiling (benchmark roofline)
 // ---------------------------------------------------------------------------
+extern "C" int sem_kernel_replay(sem_ctx *ctx, int which, int reps) {
+    CHECK_CTX();
+    if (reps < 1 || (which != 1 && which != 2 && which != 0))
+        return fail(ctx, SEM_EINVAL, "sem_kernel_replay: which in {0,1,2}, reps >= 1");
+    if (ctx->nranks != 1) return fail(ctx, SEM_EINVAL, "sem_kernel_replay: single rank only");
+    cudaStream_t s = ctx->stream;
+    CgVecs &v = ctx->cv;
+    // a mid-solve state: not done, iteration 1 (both the x and the p update
+    // are live); the partial buffers hold the scalars of the last solve
+    {
+        CgState h{};
+        h.tol = 0.0;
+        h.maxit = 1 << 30;
+        h.k1 = 1;
+        h.k2 = 1;
+        CU(cudaMemcpyAsync(&v.st->tol, &h.tol, sizeof(double), cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(&v.st->maxit, &h.maxit, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(&v.st->done, &h.done, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(&v.st->k1, &h.k1, 2 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    }
+    if (!ctx->cap_stream) CU(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    CU(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t e = cudaSuccess;
+    for (int q = 0; q < reps && e == cudaSuccess; ++q) {
+        if (which == 1) e = launch_ax_cg(ctx->dm, v, ctx->cap_stream);
+        else if (which == 2) e = launch_k2(ctx->dm, v, false, ctx->cap_stream);
+        else e = launch_ax(ctx->dm, v.r, v.w, ctx->cap_stream);
+    }
+    cudaGraph_t g = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(ctx->cap_stream, &g);
+    if (e != cudaSuccess || e2 != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        CU(e != cudaSuccess ? e : e2);
+    }
+    if (ctx->replay_exec) {     // the previous replay must be finished first
+        CU(cudaStreamSynchronize(s));
+        cudaGraphExecDestroy(ctx->replay_exec);
+        ctx->replay_exec = nullptr;
+    }
+    e = cudaGraphInstantiate(&ctx->replay_exec, g, 0);
+    cudaGraphDestroy(g);
+    CU(e);
+    CU(cudaGraphLaunch(ctx->replay_exec, s));
+    ctx->launches += reps;
+    return SEM_OK;
+}
+
 extern "C" int sem_profile(sem_ctx *ctx, int enable) {
     CHECK_CTX();
     if (!ctx->recs.empty()) {

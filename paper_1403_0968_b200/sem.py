@@ -41,7 +41,7 @@ class SemMesh(ctypes.Structure):
 EXPORTS = ["sem_version", "sem_gll", "sem_workspace_bytes", "sem_setup", "sem_sizes",
            "sem_ax", "sem_dssum", "sem_mask", "sem_mass", "sem_cg", "sem_launch_count",
            "sem_free", "sem_strerror", "sem_last_error", "sem_nccl_id_bytes",
-           "sem_nccl_get_unique_id", "sem_profile", "sem_profile_read"]
+           "sem_nccl_get_unique_id", "sem_profile", "sem_profile_read", "sem_kernel_replay"]
 
 _lib = None
 
@@ -88,9 +88,10 @@ def lib():
     L.sem_profile_read.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                    ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double)]
     L.sem_nccl_get_unique_id.argtypes = [P]
+    L.sem_kernel_replay.argtypes = [P, ctypes.c_int, ctypes.c_int]
     for f in ("sem_gll", "sem_workspace_bytes", "sem_setup", "sem_sizes", "sem_ax", "sem_dssum",
               "sem_mask", "sem_mass", "sem_cg", "sem_nccl_get_unique_id", "sem_profile",
-              "sem_profile_read"):
+              "sem_profile_read", "sem_kernel_replay"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
@@ -233,6 +234,13 @@ class Context:
                                           ctypes.byref(by)), self._ctx)
             out[nm] = (ms.value, n.value, by.value)
         return out
+
+    KERNELS = {"ax": 0, "k1": 1, "k2": 2}
+
+    def kernel_replay(self, which: str, reps: int):
+        """Enqueue `reps` back-to-back launches of one CG kernel as one graph on
+        the context stream (benchmark helper; internal CG state left undefined)."""
+        _check(lib().sem_kernel_replay(self._ctx, self.KERNELS[which], int(reps)), self._ctx)
 
     @property
     def launch_count(self) -> int:
