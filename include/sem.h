@@ -169,6 +169,16 @@ int sem_profile(sem_ctx *ctx, int enable);
 int sem_kernel_replay(sem_ctx *ctx, int which, int reps);
 int sem_profile_read(sem_ctx *ctx, int which, double *ms, int64_t *launches, double *bytes);
 
+/* Host-only and collective over mesh->allgather: the interface exchange plan
+ * sem_setup builds for nranks > 1, without touching a GPU.
+ * counts[q] (HOST, [nranks]) = number of global ids this rank shares with rank
+ * q; ids (HOST, [cap]) = those ids, peers in ascending rank order, ids
+ * ascending within a peer (the order both sides pack and unpack in);
+ * *nslot = total; *nglobal = distinct global ids over all ranks.  Returns
+ * SEM_EINVAL (with *nslot set) if cap < *nslot.  For tests and tooling. */
+int sem_exchange_plan(const sem_mesh *mesh, int N, int64_t *counts, int64_t *ids, int64_t cap,
+                      int64_t *nslot, int64_t *nglobal);
+
 /* Number of kernels this context has launched so far (all entry points). */
 int64_t sem_launch_count(const sem_ctx *ctx);
 

@@ -21,6 +21,7 @@ namespace sem {
 struct K2Args {
     GsClasses cls;
     const int32_t *idx;       // class-transposed copies of every surface group
+    const uint32_t *own;      // nranks > 1: groups counted in (r,r) on this rank
     int32_t ngroups;
     int64_t E;
     const double *w;
@@ -45,9 +46,14 @@ __host__ __device__ constexpr int k2_upb(int m) {
 // One batch of U groups of a class with compile-time multiplicity M (M = 0:
 // runtime m, up to 8).  All index loads, then all value loads, are issued
 // before any use, so a thread keeps U*M requests in flight.
+__device__ __forceinline__ bool k2_owned(const K2Args &a, int g) {
+    return !a.own || ((__ldg(a.own + (g >> 5)) >> (g & 31)) & 1u);
+}
+
 template <int M, int U, bool INIT>
 __device__ __forceinline__ double k2_groups(const K2Args &a, const int32_t *__restrict__ ix, int m,
-                                            int cnt, int q0, int qstride, double alpha) {
+                                            int cnt, int q0, int qstride, double alpha,
+                                            int gstart) {
     constexpr int MM = M ? M : 8;
     const int mm = M ? M : m;
     int li[U][MM];
@@ -78,7 +84,7 @@ __device__ __forceinline__ double k2_groups(const K2Args &a, const int32_t *__re
 #pragma unroll
         for (int t = 0; t < MM; ++t)
             if (t < mm) a.r[li[u][t]] = rn;
-        part += rn * rn;
+        if (k2_owned(a, gstart + q0 + u * qstride)) part += rn * rn;
     }
     return part;
 }
@@ -173,6 +179,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
         const int cnt = a.cls.start[c + 1] - a.cls.start[c];
         const int m = a.cls.m[c];
         const int32_t *ix = a.idx + a.cls.idxoff[c];
+        const int gs0 = a.cls.start[c];
         const int base = (cg - a.cchunk[c]) * kK2Threads * k2_upb(m) + threadIdx.x;
         if (a.cls.dir[c]) {
             // Dirichlet (INIT only): r0 = 0 at every copy (mask)
@@ -184,10 +191,10 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
             continue;
         }
         switch (m) {
-        case 1: part += k2_groups<1, 4, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
-        case 2: part += k2_groups<2, 4, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
-        case 4: part += k2_groups<4, 2, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
-        case 8: part += k2_groups<8, 1, INIT>(a, ix, m, cnt, base, kK2Threads, alpha); break;
+        case 1: part += k2_groups<1, 4, INIT>(a, ix, m, cnt, base, kK2Threads, alpha, gs0); break;
+        case 2: part += k2_groups<2, 4, INIT>(a, ix, m, cnt, base, kK2Threads, alpha, gs0); break;
+        case 4: part += k2_groups<4, 2, INIT>(a, ix, m, cnt, base, kK2Threads, alpha, gs0); break;
+        case 8: part += k2_groups<8, 1, INIT>(a, ix, m, cnt, base, kK2Threads, alpha, gs0); break;
         default: {
             const int q = base;
             if (q < cnt) {
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
                 const double r0 = INIT ? a.b[__ldg(ix + q)] : a.r[__ldg(ix + q)];
                 const double rn = INIT ? r0 - s : r0 - alpha * s;
                 for (int t = 0; t < m; ++t) a.r[__ldg(ix + t * cnt + q)] = rn;
-                part += rn * rn;
+                if (k2_owned(a, gs0 + q)) part += rn * rn;
             }
         } break;
         }
@@ -234,6 +241,7 @@ cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t
     K2Args a{};
     a.cls = m.cls;
     a.idx = m.gs_idx;
+    a.own = m.own;
     a.ngroups = m.ngroups;
     a.E = m.E;
     a.w = v.w;

@@ -1,4 +1,13 @@
-// sem_comm.h -- multi-rank plumbing (NCCL over NVLink) for libsem.  Internal.
+// sem_comm.h -- multi-rank plumbing for libsem.  Internal.
+//
+// Elements are partitioned across ranks; global ids are consistent.  A global
+// node on a partition interface has local copies on several ranks.  Q Q^T
+// over all ranks = (1) each rank sums its own copies (ascending local order),
+// (2) the per-rank partial sums are exchanged with every peer sharing the node
+// (grouped ncclSend/ncclRecv over NVLink), (3) every rank adds the partials in
+// ASCENDING RANK ORDER, so all ranks hold bit-identical values, and writes the
+// total into the node's first local copy (the others zeroed), after which the
+// ordinary local gather-scatter (or K2) completes the operator.
 #pragma once
 #include <string>
 #include <vector>
@@ -8,16 +17,38 @@
 
 namespace sem {
 
+// Host-side exchange plan of one rank (pure host; uses mesh->allgather).
+struct ExchangePlan {
+    int rank = 0, nranks = 1;
+    std::vector<int> peer;                // peers with a non-empty shared set, ascending
+    std::vector<int64_t> peer_off;        // [npeer + 1] offsets into send/recv slots
+    std::vector<int64_t> shared_ids;      // [nslot] global ids, ascending per peer
+    std::vector<int32_t> send_group;      // [nslot] local group of each slot
+    // interface groups: local group, and its sources in ascending rank order
+    // (-1 = this rank's own partial, else a recv slot)
+    std::vector<int32_t> if_group;
+    std::vector<int32_t> if_off;          // [nif + 1]
+    std::vector<int32_t> if_src;
+    std::vector<int32_t> not_owned;       // interface groups a lower rank also holds:
+                                          // counted there, not here, in (r,r)
+    int64_t nglobal = 0;                  // distinct global ids over all ranks
+};
+
+// surf_ids: this rank's distinct element-surface global ids (ascending) with
+// their local group (surf_group); ndistinct: distinct ids on this rank.
+int build_exchange_plan(const sem_mesh *mesh, const std::vector<int64_t> &surf_ids,
+                        const std::vector<int32_t> &surf_group, int64_t ndistinct,
+                        ExchangePlan &ep, std::string &err);
+
 struct Comm;
 
-// Build the NCCL communicator and the per-peer interface exchange lists.
-int comm_setup(Comm *&c, const sem_mesh *mesh, const std::vector<int64_t> &surf_ids,
-               const std::vector<int32_t> &surf_group, const std::vector<int32_t> &off,
-               const std::vector<int32_t> &idx, int64_t &nglobal, cudaStream_t s,
-               std::string &err);
-// Q Q^T across ranks (mode as launch_gs).  nlaunch receives the kernel count.
-int comm_dssum(Comm *c, const DevMesh &m, double *w, int mode, CgVecs *v,
-               cudaStream_t s, int64_t &nlaunch, std::string &err);
+// NCCL communicator + device copies of the plan.  cudaMalloc's its buffers.
+int comm_setup(Comm *&c, const sem_mesh *mesh, const ExchangePlan &ep, const DevMesh &dm,
+               cudaStream_t s, std::string &err);
+// Cross-rank part of Q Q^T on w (pack, exchange, ordered combine into the first
+// copy).  nlaunch receives the kernel count.
+int comm_exchange(Comm *c, const DevMesh &m, double *w, cudaStream_t s, int64_t &nlaunch,
+                  std::string &err);
 // In-place all-gather of one double per rank at slot_base[0..nranks).
 int comm_allgather_scalar(Comm *c, double *slot_base, cudaStream_t s, std::string &err);
 void comm_free(Comm *c);

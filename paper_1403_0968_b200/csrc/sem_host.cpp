@@ -212,7 +212,7 @@ static void diff_matrix(int N, const double *x, double *D) {
 // ---------------------------------------------------------------------------
 namespace {
 struct Layout {
-    size_t G, BM, r, p, w, xw, D, gs_idx, partials, rr_all, pap_all, st, total;
+    size_t G, BM, r, p, w, xw, D, gs_idx, own, partials, rr_all, pap_all, st, total;
     int64_t nsurf_cap, partial_cap;
 };
 
@@ -239,6 +239,7 @@ Layout make_layout(int N, int64_t E, int nranks) {
     Lo.xw = take(sizeof(double) * L);
     Lo.D = take(sizeof(double) * (n * n + n));
     Lo.gs_idx = take(sizeof(int32_t) * Lo.nsurf_cap);
+    Lo.own = take(sizeof(uint32_t) * ((Lo.nsurf_cap + 31) / 32 + 1));
     Lo.partials = take(sizeof(double) * 4 * Lo.partial_cap);   // part1[2][cap], part2[2][cap]
     Lo.rr_all = take(sizeof(double) * kRing * nranks);
     Lo.pap_all = take(sizeof(double) * kRing * nranks);
@@ -536,9 +537,20 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         if (bad) return fail(ctx, SEM_EINVAL, "non-positive Jacobian in the mesh");
         if (ctx->nranks > 1) {
             std::string cerr;
-            int crc = comm_setup(ctx->comm, mesh, hp.surf_ids, hp.surf_group, hp.off, hp.idx,
-                                 ctx->nglobal, s, cerr);
+            ExchangePlan ep;
+            int crc = build_exchange_plan(mesh, hp.surf_ids, hp.surf_group, hp.ndistinct, ep, cerr);
             if (crc) return fail(ctx, crc, "%s", cerr.c_str());
+            ctx->nglobal = ep.nglobal;
+            crc = comm_setup(ctx->comm, mesh, ep, dm, s, cerr);
+            if (crc) return fail(ctx, crc, "%s", cerr.c_str());
+            // (r,r) ownership of interface groups: the lowest sharing rank counts them
+            std::vector<uint32_t> own((hp.ngroups + 31) / 32 + 1, 0xffffffffu);
+            for (int32_t g : ep.not_owned) own[g >> 5] &= ~(1u << (g & 31));
+            uint32_t *own_d = reinterpret_cast<uint32_t *>(ws + Lo.own);
+            CU(cudaMemcpyAsync(own_d, own.data(), sizeof(uint32_t) * own.size(),
+                               cudaMemcpyHostToDevice, s));
+            CU(cudaStreamSynchronize(s));
+            dm.own = own_d;
         }
         return SEM_OK;
     }();
@@ -547,6 +559,30 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         return bail(rc);
     }
     *out = ctx;
+    return SEM_OK;
+}
+
+extern "C" int sem_exchange_plan(const sem_mesh *mesh, int N, int64_t *counts, int64_t *ids,
+                                 int64_t cap, int64_t *nslot, int64_t *nglobal) {
+    int rc = check_mesh(mesh, N);
+    if (rc) return rc;
+    if (!mesh->glo || !mesh->dirichlet || !counts || !nslot || !nglobal)
+        return fail(nullptr, SEM_EINVAL, "NULL argument to sem_exchange_plan");
+    HostPlan hp;
+    std::string err;
+    rc = build_plan(mesh, N, hp, err);
+    if (rc) return fail(nullptr, rc, "%s", err.c_str());
+    ExchangePlan ep;
+    rc = build_exchange_plan(mesh, hp.surf_ids, hp.surf_group, hp.ndistinct, ep, err);
+    if (rc) return fail(nullptr, rc, "%s", err.c_str());
+    *nslot = (int64_t)ep.shared_ids.size();
+    *nglobal = ep.nglobal;
+    for (int q = 0; q < mesh->nranks; ++q) counts[q] = 0;
+    for (size_t p = 0; p < ep.peer.size(); ++p) counts[ep.peer[p]] = ep.peer_off[p + 1] - ep.peer_off[p];
+    if (*nslot > cap || (*nslot > 0 && !ids))
+        return fail(nullptr, SEM_EINVAL, "sem_exchange_plan: ids capacity %lld < %lld",
+                    (long long)cap, (long long)*nslot);
+    std::copy(ep.shared_ids.begin(), ep.shared_ids.end(), ids);
     return SEM_OK;
 }
 
@@ -593,20 +629,26 @@ extern "C" int sem_ax(sem_ctx *ctx, const double *u, double *w) {
     return SEM_OK;
 }
 
-static int dssum_impl(sem_ctx *ctx, double *w, int mode, int k, cudaStream_t s) {
-    if (ctx->nranks == 1) {
-        const double by = 16.0 * ctx->dm.nsurf;
-        LAUNCHP(kProfGs, by, mode == 2 ? k : -1, launch_gs(ctx->dm, w, mode, &ctx->cv, s));
-        return SEM_OK;
-    }
+// Cross-rank part of Q Q^T (no-op on one rank): after it, every interface
+// node's first local copy holds the rank-ordered total and the others 0.
+static int exchange_impl(sem_ctx *ctx, double *w, cudaStream_t s) {
+    if (ctx->nranks == 1) return SEM_OK;
     std::string cerr;
     int64_t nl = 0;
-    int rc = comm_dssum(ctx->comm, ctx->dm, w, mode, &ctx->cv, s, nl, cerr);
+    int rc = comm_exchange(ctx->comm, ctx->dm, w, s, nl, cerr);
     ctx->launches += nl;
     if (rc) {
         if (rc == SEM_ECUDA) ctx->broken = true;
         return fail(ctx, rc, "%s", cerr.c_str());
     }
+    return SEM_OK;
+}
+
+static int dssum_impl(sem_ctx *ctx, double *w, int mode, int k, cudaStream_t s) {
+    int rc = exchange_impl(ctx, w, s);
+    if (rc) return rc;
+    const double by = 16.0 * ctx->dm.nsurf;
+    LAUNCHP(kProfGs, by, mode == 2 ? k : -1, launch_gs(ctx->dm, w, mode, &ctx->cv, s));
     return SEM_OK;
 }
 
@@ -660,6 +702,7 @@ static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
     int rc;
     LAUNCHP(kProfAxCg, (k == 0 ? 72.0 : 96.0) * ctx->L, k, launch_ax_cg(ctx->dm, v, s));
     if (P > 1) {
+        if ((rc = exchange_impl(ctx, v.w, s))) return rc;
         LAUNCH(launch_cg_red_pap(ctx->dm, v, s));
         if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P, s))) return rc;
     }
@@ -715,6 +758,7 @@ extern "C" int sem_cg(sem_ctx *ctx, const double *b, double *x, double tol, int 
     }
     // r = mask (b - Q Q^T A_L x0)
     LAUNCH(launch_ax(ctx->dm, x, v.w, s));
+    if ((rc = exchange_impl(ctx, v.w, s))) return rc;
     LAUNCH(launch_cg_init(ctx->dm, v, s));
     LAUNCH(launch_k2(ctx->dm, v, true, s));
     if (P > 1) {

@@ -50,6 +50,8 @@ struct DevMesh {
     // local order, stored by class (see GsClasses).
     GsClasses cls;
     const int32_t *gs_idx;      // [nsurf], class-transposed
+    const uint32_t *own;        // nranks > 1: bit g set = group g counted in (r,r) here
+                                // (its lowest sharing rank is this one); nullptr on one rank
     int32_t ngroups, ndir, nsurf;
     int rank, nranks;
     int nsm;                    // SM count of the device (persistent grids)

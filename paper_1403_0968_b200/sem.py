@@ -41,7 +41,7 @@ class SemMesh(ctypes.Structure):
 EXPORTS = ["sem_version", "sem_gll", "sem_workspace_bytes", "sem_setup", "sem_sizes",
            "sem_ax", "sem_dssum", "sem_mask", "sem_mass", "sem_cg", "sem_launch_count",
            "sem_free", "sem_strerror", "sem_last_error", "sem_nccl_id_bytes",
-           "sem_nccl_get_unique_id", "sem_profile", "sem_profile_read", "sem_kernel_replay"]
+           "sem_nccl_get_unique_id", "sem_profile", "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan"]
 
 _lib = None
 
@@ -89,9 +89,11 @@ def lib():
                                    ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double)]
     L.sem_nccl_get_unique_id.argtypes = [P]
     L.sem_kernel_replay.argtypes = [P, ctypes.c_int, ctypes.c_int]
+    L.sem_exchange_plan.argtypes = [ctypes.POINTER(SemMesh), ctypes.c_int, P, P, i64,
+                                    ctypes.POINTER(i64), ctypes.POINTER(i64)]
     for f in ("sem_gll", "sem_workspace_bytes", "sem_setup", "sem_sizes", "sem_ax", "sem_dssum",
               "sem_mask", "sem_mass", "sem_cg", "sem_nccl_get_unique_id", "sem_profile",
-              "sem_profile_read", "sem_kernel_replay"):
+              "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
