@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
     const int g = tid / GT;                 // group
     const int gt = tid - g * GT;            // thread in group
     const int el = gt / n2;                 // element within unit
+    const int elc = (el < EPG) ? el : 0;    // spare lanes address element 0 (results unused)
     const int ij = gt - el * n2;
     const int i = ij % n, j = ij / n;
     const bool lane_on = el < EPG;
@@ -291,9 +292,9 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
         double col[n];  // input column (i,j,0..N)
         const int64_t gbase = e * n3 + ij;
         if constexpr (CG) {
-            double *sr = sb + 0 * VL + sh + el * n3;
-            double *sp = sb + 1 * VL + sh + el * n3;
-            double *sx = sb + 2 * VL + sh + el * n3;
+            double *sr = sb + 0 * VL + sh + elc * n3;
+            double *sp = sb + 1 * VL + sh + elc * n3;
+            double *sx = sb + 2 * VL + sh + elc * n3;
             su = sp;
             if (on) {
 #pragma unroll
@@ -318,11 +319,11 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
             }
             group_bar(1 + g, GT);  // p visible to the group
         } else {
-            su = sb + sh + el * n3;
+            su = sb + sh + elc * n3;
 #pragma unroll
             for (int k = 0; k < n; ++k) col[k] = on ? su[k * n2 + ij] : 0.0;
         }
-        double *sG = sb + NV * VL + el * 6 * n3;
+        double *sG = sb + NV * VL + elc * 6 * n3;
 
         // ---- phase A: gradient, geometric factors ----
         double ft[n];

@@ -66,7 +66,10 @@ def test_ax_parity_all_orders(dev, impl, N, eps):
 
 
 @pytest.mark.parametrize("N,elems", [(7, (8, 8, 8)), (3, (13, 7, 5)), (4, (9, 5, 3)),
-                                     (6, (7, 5, 3)), (2, (11, 9, 7)), (10, (3, 3, 3))])
+                                     (6, (7, 5, 3)), (2, (11, 9, 7)), (10, (3, 3, 3)),
+                                     # many persistent-CTA rounds; spare lanes in every
+                                     # group (EPG n^2 < GT) on the last CTA's last group
+                                     (4, (21, 21, 21)), (5, (17, 17, 17)), (6, (15, 15, 13))])
 def test_ax_parity_many_elements(dev, impl, N, elems):
     m, G, J, ctx = make(N, elems, 0.05)
     u = meshgen.random_field(m.nlocal, 11)
