@@ -389,6 +389,222 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
 }
 
 // ---------------------------------------------------------------------------
+// High orders: a whole element's G^ (6 n^3 doubles, up to 196 KB) does not fit
+// a double-buffered stage, so the hi kernel streams G^ by k-SLICES: G^ is laid
+// out slice-major ([E][n][6][n^2], chosen at setup for this kernel) so one
+// 48 n^2-byte bulk copy fetches slice k, into a ring of R slots per group with
+// one mbarrier each; the leader keeps R slices in flight across element
+// boundaries.  The Ax input vector (r and p for K1) is staged per element,
+// double-buffered, as in the low-order kernel.  f_r, f_s live in a
+// double-buffered k-slice (one barrier per slice); D comes from shared memory
+// (lane-dependent rows/columns) and constant memory (uniform k, m).
+// ---------------------------------------------------------------------------
+template <int N, bool CG>
+struct HiCfg {
+    static constexpr int n = N + 1, n2 = n * n, n3 = n2 * n;
+    static constexpr int GT = ((n2 + 31) / 32) * 32;
+    static constexpr int VL = ((n3 + 2 + 1) / 2) * 2;
+    static constexpr int NV = CG ? 2 : 1;                  // r, p | u
+    static constexpr int STAGE = NV * VL;                  // doubles per element buffer
+    static constexpr int SL = 6 * n2;                      // doubles per G^ slice
+    static constexpr int R = 4;                            // G^ slices in flight per group
+    static constexpr int PERG = 2 * STAGE + R * SL + 4 * n2;
+    static constexpr int SMEM_MAX = 227 * 1024 - 2048;
+    static constexpr int NG_FIT = SMEM_MAX / (PERG * 8);
+    static constexpr int NG = NG_FIT > 3 ? 3 : NG_FIT;
+    static constexpr int NT = NG * GT;
+    static constexpr size_t SMEM = size_t(NG) * PERG * 8 + size_t(NG) * (2 + R) * 8 + 64;
+};
+
+template <int N, bool CG>
+__global__ void __launch_bounds__(HiCfg<N, CG>::NT, 1) ax_hi_kernel(TmaArgs a) {
+    using C = HiCfg<N, CG>;
+    constexpr int n = C::n, n2 = C::n2, n3 = C::n3, GT = C::GT, VL = C::VL, NV = C::NV;
+    constexpr int STAGE = C::STAGE, PERG = C::PERG, NG = C::NG, SL = C::SL, R = C::R;
+    constexpr int DO = d_off(N);
+    extern __shared__ __align__(128) double smem[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + size_t(NG) * PERG);   // [NG][2 + R]
+    constexpr int DS = n | 1;                  // odd row stride: conflict-free lane-indexed rows
+    __shared__ double sD[n * DS];
+    __shared__ double sred[3 * ((C::NT + 31) / 32)];
+
+    const int tid = threadIdx.x;
+    const int g = tid / GT;
+    const int ij = tid - g * GT;
+    const bool lane_on = ij < n2;
+    const int ijc = lane_on ? ij : 0;
+    const int i = ijc % n, j = ijc / n;
+    const bool leader = (ij == 0);
+    double *base_g = smem + size_t(g) * PERG;
+    double *ring = base_g + 2 * STAGE;                      // [R][6][n2]
+    double *sf = ring + R * SL;                             // [2 slices][f_r, f_s][n2]
+    uint64_t *vbar = bars + (2 + R) * g;                    // element stages
+    uint64_t *gbar = vbar + 2;                              // G^ ring slots
+    const int64_t TG = int64_t(gridDim.x) * NG;
+    const int64_t e0 = int64_t(blockIdx.x) * NG + g;
+    const int64_t L = a.E * n3;
+    const int64_t nel = (e0 < a.E) ? (a.E - e0 + TG - 1) / TG : 0;   // elements of this group
+    const int64_t nsl = nel * n;                                     // G^ slices of this group
+    for (int t = tid; t < n2; t += C::NT) sD[(t / n) * DS + t % n] = c_D[DO + t];
+    if (leader) {
+        for (int q = 0; q < 2 + R; ++q) mbar_init(vbar + q, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if constexpr (CG) pdl_trigger();
+    const uint64_t pol_v = CG ? policy_evict_last() : policy_evict_first();
+    const uint64_t pol_g = policy_evict_first();
+    // G^ slice gs of this group's stream (element e0 + (gs / n) TG, slice gs % n)
+    auto issue_slice = [&](int64_t gs) {
+        const int slot = (int)(gs % R);
+        const int64_t e = e0 + (gs / n) * TG;
+        const int k = (int)(gs % n);
+        mbar_expect_tx_only(gbar + slot, SL * 8);
+        mbar_arrive(gbar + slot);
+        bulk_g2s(ring + slot * SL, a.G + e * 6 * n3 + (int64_t)k * SL, SL * 8, gbar + slot, pol_g);
+    };
+    auto issue_vec = [&](int64_t e, int s) {
+        double *sb = base_g + size_t(s) * STAGE;
+        const int64_t first = e * n3;
+        const VecRange vr = vec_range(first, n3, L);
+        const double *vsrc[2];
+        if constexpr (CG) {
+            vsrc[0] = a.r;
+            vsrc[1] = a.p;
+        } else {
+            vsrc[0] = a.u;
+        }
+        const uint32_t vb = (uint32_t)((vr.a1 - vr.a0) * 8);
+        mbar_expect_tx_only(vbar + s, NV * vb);
+        for (int v = 0; v < NV; ++v)
+            for (int64_t q = vr.a1; q < first + n3; ++q) sb[v * VL + (q - vr.a0)] = __ldg(vsrc[v] + q);
+        mbar_arrive(vbar + s);
+        for (int v = 0; v < NV; ++v) bulk_g2s(sb + v * VL, vsrc[v] + vr.a0, vb, vbar + s, pol_v);
+    };
+    if (leader)
+        for (int64_t gs = 0; gs < R && gs < nsl; ++gs) issue_slice(gs);   // static data first
+    if constexpr (CG) pdl_wait();
+    if (leader) {
+        if (nel > 0) issue_vec(e0, 0);
+        if (nel > 1) issue_vec(e0 + TG, 1);
+    }
+    double beta = 0.0, alpha_prev = 0.0;
+    int kit = 0;
+    if constexpr (CG) {
+        const CgStep c = cg_k1_prologue<C::NT>(a.st, a.red, sred);
+        if (c.done) {
+            if (leader) {       // drain everything in flight
+                for (int64_t gs = 0; gs < R && gs < nsl; ++gs) mbar_wait(gbar + gs, 0);
+                if (nel > 0) mbar_wait(vbar + 0, 0);
+                if (nel > 1) mbar_wait(vbar + 1, 0);
+            }
+            return;
+        }
+        beta = c.beta;
+        alpha_prev = c.alpha_prev;
+        kit = c.k;
+    }
+
+    double pap = 0.0;
+    int64_t gs = 0;                                          // slice stream position
+    for (int64_t t = 0; t < nel; ++t) {
+        const int64_t e = e0 + t * TG;
+        const int s = (int)(t & 1);
+        double *sb = base_g + size_t(s) * STAGE;
+        const int sh = (int)((e * n3) & 1);
+        const int64_t gb = e * n3 + ijc;
+        double xc[CG ? n : 1];
+        if constexpr (CG) {
+            if (kit > 0) {
+#pragma unroll
+                for (int k = 0; k < n; ++k) xc[k] = a.x[gb + k * n2];
+            }
+        }
+        mbar_wait(vbar + s, (int)((t >> 1) & 1));
+        double col[n];
+        double *su;
+        if constexpr (CG) {
+            double *sr = sb + sh;
+            double *sp = sb + VL + sh;
+            su = sp;
+#pragma unroll
+            for (int k = 0; k < n; ++k) {
+                const int q = k * n2 + ijc;
+                const double rl = sr[q];
+                double pl = rl;
+                if (kit > 0) {
+                    const double po = sp[q];
+                    if (lane_on) a.x[gb + k * n2] = xc[k] + alpha_prev * po;
+                    pl = rl + beta * po;
+                }
+                if (lane_on) {
+                    sp[q] = pl;
+                    a.p[gb + k * n2] = pl;
+                }
+                col[k] = pl;
+            }
+            group_bar(1 + g, GT);
+        } else {
+            su = sb + sh;
+#pragma unroll
+            for (int k = 0; k < n; ++k) col[k] = su[k * n2 + ijc];
+        }
+        double rw[n];
+#pragma unroll
+        for (int k = 0; k < n; ++k) rw[k] = 0.0;
+#pragma unroll
+        for (int k = 0; k < n; ++k, ++gs) {
+            const int slot = (int)(gs % R);
+            mbar_wait(gbar + slot, (int)((gs / R) & 1));
+            const double *gk = ring + slot * SL + ijc;
+            const double g0 = gk[0 * n2], g1 = gk[1 * n2], g2 = gk[2 * n2];
+            const double g3 = gk[3 * n2], g4 = gk[4 * n2], g5 = gk[5 * n2];
+            const double *uk = su + k * n2;
+            double ur = 0.0, us = 0.0, ut = 0.0;
+#pragma unroll
+            for (int m = 0; m < n; ++m) {
+                ur = fma(sD[i * DS + m], uk[j * n + m], ur);
+                us = fma(sD[j * DS + m], uk[m * n + i], us);
+                ut = fma(c_D[DO + k * n + m], col[m], ut);
+            }
+            const double fr = g0 * ur + g1 * us + g2 * ut;
+            const double fs = g1 * ur + g3 * us + g4 * ut;
+            const double ft = g2 * ur + g4 * us + g5 * ut;
+            double *sfk = sf + (k & 1) * 2 * n2;
+            if (lane_on) {
+                sfk[ij] = fr;
+                sfk[n2 + ij] = fs;
+            }
+#pragma unroll
+            for (int m = 0; m < n; ++m) rw[m] = fma(c_D[DO + k * n + m], ft, rw[m]);
+            group_bar(1 + g, GT);   // f slice visible; every thread is done with G^ slot
+            if (leader && gs + R < nsl) issue_slice(gs + R);
+            double acc = 0.0;
+#pragma unroll
+            for (int m = 0; m < n; ++m) {
+                acc = fma(sD[m * DS + i], sfk[j * n + m], acc);
+                acc = fma(sD[m * DS + j], sfk[n2 + m * n + i], acc);
+            }
+            rw[k] += acc;
+        }
+        if (lane_on) {
+#pragma unroll
+            for (int k = 0; k < n; ++k) {
+                a.w[gb + k * n2] = rw[k];
+                if constexpr (CG) pap = fma(rw[k], col[k], pap);
+            }
+        }
+        fence_proxy_async();
+        group_bar(1 + g, GT);    // stage s and both f slices consumed
+        if (leader && t + 2 < nel) issue_vec(e + 2 * TG, s);
+    }
+    if constexpr (CG) {
+        const double bs = block_sum<C::NT>(pap, sred);
+        if (tid == 0) a.part1[(kit & 1) * a.red.s1 + blockIdx.x] = bs;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 #define SEM_TMA_DISPATCH(N_, ...)                                            \
@@ -450,6 +666,82 @@ cudaError_t launch_ax_tma(const DevMesh &m, const double *u, double *w, cudaStre
                                                       TmaLayout<NN, false>::NT,
                                                       TmaLayout<NN, false>::SMEM, s>>>(a)));
     return cudaGetLastError();
+}
+
+// ---- high-order kernel ----
+#define SEM_HI_DISPATCH(N_, ...)                                             \
+    switch (N_) {                                                            \
+    case 6: { constexpr int NN = 6; __VA_ARGS__; } break;                    \
+    case 7: { constexpr int NN = 7; __VA_ARGS__; } break;                    \
+    case 8: { constexpr int NN = 8; __VA_ARGS__; } break;                    \
+    case 9: { constexpr int NN = 9; __VA_ARGS__; } break;                    \
+    case 10: { constexpr int NN = 10; __VA_ARGS__; } break;                  \
+    case 11: { constexpr int NN = 11; __VA_ARGS__; } break;                  \
+    case 12: { constexpr int NN = 12; __VA_ARGS__; } break;                  \
+    case 13: { constexpr int NN = 13; __VA_ARGS__; } break;                  \
+    case 14: { constexpr int NN = 14; __VA_ARGS__; } break;                  \
+    case 15: { constexpr int NN = 15; __VA_ARGS__; } break;                  \
+    default: break;                                                          \
+    }
+
+bool hi_supported(int N) { return N >= 6 && N <= 15; }
+
+template <int N, bool CG>
+static int hi_grid(int64_t E, int nsm) {
+    int64_t need = (E + HiCfg<N, CG>::NG - 1) / HiCfg<N, CG>::NG;
+    return (int)(need < nsm ? (need < 1 ? 1 : need) : nsm);
+}
+
+int hi_blocks(int N, int64_t E, int nsm, bool cg) {
+    int nb = 0;
+    if (cg) {
+        SEM_HI_DISPATCH(N, nb = hi_grid<NN, true>(E, nsm));
+    } else {
+        SEM_HI_DISPATCH(N, nb = hi_grid<NN, false>(E, nsm));
+    }
+    return nb;
+}
+
+template <int N, bool CG>
+static cudaError_t hi_attr() {
+    static_assert(HiCfg<N, CG>::NG >= 1, "element stage does not fit in shared memory");
+    return cudaFuncSetAttribute(ax_hi_kernel<N, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)HiCfg<N, CG>::SMEM);
+}
+
+cudaError_t hi_prepare(int N) {
+    cudaError_t e = cudaSuccess;
+    SEM_HI_DISPATCH(N, (e = hi_attr<NN, false>(), e = (e == cudaSuccess ? hi_attr<NN, true>() : e)));
+    return e;
+}
+
+cudaError_t launch_ax_hi(const DevMesh &m, const double *u, double *w, cudaStream_t s) {
+    TmaArgs a{};
+    a.E = m.E;
+    a.G = m.G;
+    a.u = u;
+    a.w = w;
+    SEM_HI_DISPATCH(m.N, (ax_hi_kernel<NN, false><<<hi_grid<NN, false>(m.E, m.nsm),
+                                                    HiCfg<NN, false>::NT, HiCfg<NN, false>::SMEM,
+                                                    s>>>(a)));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ax_cg_hi(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
+    TmaArgs a{};
+    a.E = m.E;
+    a.G = m.G;
+    a.r = v.r;
+    a.p = v.p;
+    a.x = v.xw;
+    a.w = v.w;
+    a.red = make_red(m, v);
+    a.part1 = v.part1;
+    a.st = v.st;
+    cudaError_t e = cudaSuccess;
+    SEM_HI_DISPATCH(m.N, e = launch_pdl(ax_hi_kernel<NN, true>, hi_grid<NN, true>(m.E, m.nsm),
+                                        HiCfg<NN, true>::NT, HiCfg<NN, true>::SMEM, s, a));
+    return e;
 }
 
 cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, cudaStream_t s) {

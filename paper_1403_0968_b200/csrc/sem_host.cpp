@@ -492,8 +492,19 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         int nsm = 148;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, mesh->device);
         dm.nsm = nsm;
+        // Ax kernel family: element-staged TMA (low N), vector-staged TMA +
+        // register-streamed G^ (high N), or the simple kernel (SEM_AX_KERNEL=
+        // simple|tma|hi forces one; SEM_HI_MIN_N moves the automatic switch)
         const char *impl = getenv("SEM_AX_KERNEL");
-        dm.use_tma = tma_supported(N) && !(impl && strcmp(impl, "simple") == 0);
+        const char *himin = getenv("SEM_HI_MIN_N");
+        // measured c4 sweep (profiles/order_sweep_r01*.json): element-staged
+        // TMA wins up to N = 10, slice-streamed from N = 11
+        const int hi_min = himin ? atoi(himin) : 11;
+        const bool force_simple = impl && strcmp(impl, "simple") == 0;
+        const bool force_tma = impl && strcmp(impl, "tma") == 0;
+        const bool force_hi = impl && strcmp(impl, "hi") == 0;
+        dm.use_hi = !force_simple && !force_tma && hi_supported(N) && (force_hi || N >= hi_min);
+        dm.use_tma = !force_simple && !dm.use_hi && tma_supported(N);
         const char *gr = getenv("SEM_CG_GRAPH");
         ctx->use_graph = !(gr && strcmp(gr, "0") == 0);
     }
@@ -514,6 +525,7 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         CU(cudaHostAlloc(&ctx->host_state, 2 * sizeof(CgState), cudaHostAllocDefault));
         CU(upload_const_D(N, Dh.data()));
         if (dm.use_tma) CU(tma_prepare(N));
+        if (dm.use_hi) CU(hi_prepare(N));
         CU(cudaEventCreateWithFlags(&ctx->ev[0], cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&ctx->ev[1], cudaEventDisableTiming));
         CU(cudaMemcpyAsync((void *)dm.D, Dh.data(), sizeof(double) * Dh.size(),

@@ -55,7 +55,8 @@ struct DevMesh {
     int32_t ngroups, ndir, nsurf;
     int rank, nranks;
     int nsm;                    // SM count of the device (persistent grids)
-    bool use_tma;               // TMA-pipelined Ax kernels (N <= kTmaMaxN)
+    bool use_tma;               // TMA element-staged Ax kernels (N <= kTmaMaxN)
+    bool use_hi;                // TMA vector + register-streamed G^ kernels (high N)
 };
 
 struct CgVecs {
@@ -107,5 +108,10 @@ cudaError_t tma_prepare(int N);
 cudaError_t upload_const_D(int N, const double *D_host);
 cudaError_t launch_ax_tma(const DevMesh &m, const double *u, double *w, cudaStream_t s);
 cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+bool hi_supported(int N);
+int hi_blocks(int N, int64_t E, int nsm, bool cg);
+cudaError_t hi_prepare(int N);
+cudaError_t launch_ax_hi(const DevMesh &m, const double *u, double *w, cudaStream_t s);
+cudaError_t launch_ax_cg_hi(const DevMesh &m, const CgVecs &v, cudaStream_t s);
 
 }  // namespace sem

@@ -31,7 +31,8 @@ __device__ __forceinline__ double sum_ranks(const double *a, int nranks) {
 // --------------------------------------------------------------------------
 __global__ void geom_kernel(int n, int64_t E, const double *__restrict__ D,
                             const double *__restrict__ wq, const double *__restrict__ xyz,
-                            double *__restrict__ G, double *__restrict__ BM, int *bad) {
+                            double *__restrict__ G, double *__restrict__ BM, int *bad,
+                            bool slice_major) {
     const int n3 = n * n * n;
     const int64_t L = E * n3;
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L;
@@ -74,8 +75,13 @@ __global__ void geom_kernel(int n, int64_t E, const double *__restrict__ D,
         for (int f = 0; f < 6; ++f)
             g[f] = s * (C[0][pd[f]] * C[0][pe[f]] + C[1][pd[f]] * C[1][pe[f]] +
                         C[2][pd[f]] * C[2][pe[f]]);
-        double *Ge = G + e * 6 * n3 + q;
-        for (int f = 0; f < 6; ++f) Ge[f * n3] = g[f];
+        if (slice_major) {      // [E][n][6][n^2]: one contiguous block per k-slice
+            double *Ge = G + e * 6 * n3 + (int64_t)k * 6 * n * n + (i + n * j);
+            for (int f = 0; f < 6; ++f) Ge[f * n * n] = g[f];
+        } else {                // [E][6][n^3]
+            double *Ge = G + e * 6 * n3 + q;
+            for (int f = 0; f < 6; ++f) Ge[f * n3] = g[f];
+        }
         BM[l] = wJ;
     }
 }
@@ -425,6 +431,7 @@ static int ax_grid(int N, int64_t E, int nsm) {
 }
 
 int ax_cg_blocks(const DevMesh &m) {
+    if (m.use_hi) return hi_blocks(m.N, m.E, m.nsm, true);
     return m.use_tma ? tma_blocks(m.N, m.E, m.nsm, true) : ax_grid(m.N, m.E, m.nsm);
 }
 
@@ -437,13 +444,15 @@ static int grid_for(int64_t L, int threads) {
 cudaError_t launch_geom(const DevMesh &m, const double *xyz, double *G, double *BM,
                         int *bad, cudaStream_t s) {
     // D and the 1-D weights live at the start of the D buffer: [n*n] D, [n] w
+    // the high-order kernel streams G^ by k-slices: slice-major layout
     geom_kernel<<<grid_for(m.L, 256), 256, 0, s>>>(m.n, m.E, m.D, m.D + m.n * m.n, xyz, G, BM,
-                                                   bad);
+                                                   bad, m.use_hi);
     return cudaGetLastError();
 }
 
 cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t s) {
     if (m.E == 0) return cudaSuccess;
+    if (m.use_hi) return launch_ax_hi(m, u, w, s);
     if (m.use_tma) return launch_ax_tma(m, u, w, s);
     AxCgArgs none{};
     SEM_DISPATCH_N(m.N, (ax_kernel<NN, false><<<ax_grid(m.N, m.E, m.nsm), AxCfg<NN>::NT, 0, s>>>(
@@ -452,6 +461,7 @@ cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t
 }
 
 cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
+    if (m.use_hi) return launch_ax_cg_hi(m, v, s);
     if (m.use_tma) return launch_ax_cg_tma(m, v, s);
     AxCgArgs a{v.r, v.p, v.xw, make_red(m, v), v.part1, v.st};
     cudaError_t e = cudaSuccess;

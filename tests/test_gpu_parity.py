@@ -28,12 +28,13 @@ def relerr(a, b):
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
-@pytest.fixture(params=["tma", "simple", "tma-nograph"])
+@pytest.fixture(params=["tma", "hi", "simple", "tma-nograph"])
 def impl(request, monkeypatch):
-    """Both Ax kernel paths -- the TMA-pipelined persistent kernel (N <= 10) and
-    the simple one-block-per-element kernel (all N) -- and the CG driver with
-    and without CUDA-graph chunks."""
-    monkeypatch.setenv("SEM_AX_KERNEL", "simple" if request.param == "simple" else "tma")
+    """All Ax kernel families -- element-staged TMA (N <= 10), vector-staged TMA
+    with register-streamed G^ ("hi", N >= 6; lower N fall back to TMA), the
+    simple one-block-per-element kernel (all N) -- and the CG driver with and
+    without CUDA-graph chunks."""
+    monkeypatch.setenv("SEM_AX_KERNEL", request.param.split("-")[0])
     monkeypatch.setenv("SEM_CG_GRAPH", "0" if request.param.endswith("nograph") else "1")
     return request.param
 
