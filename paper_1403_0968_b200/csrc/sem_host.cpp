@@ -53,6 +53,10 @@ struct sem_ctx {
     cudaGraphExec_t graph_exec = nullptr;
     int64_t graph_kernels = 0;
     cudaGraphExec_t replay_exec = nullptr;   // sem_kernel_replay
+    // boundary/interior K1 split (k1_split): the exchange runs on `side`
+    // between fork (boundary K1 done) and join (before the pap all-gather)
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
 };
 
 static constexpr int kChunk = 8;     // CG iterations per graph launch / poll (multiple of 4)
@@ -508,6 +512,12 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         const char *gr = getenv("SEM_CG_GRAPH");
         ctx->use_graph = !(gr && strcmp(gr, "0") == 0);
     }
+    // one rank: SEM_K1_SPLIT=<fraction of E> exercises the boundary/interior
+    // K1 split without an exchange (testing only; multi-rank sets nbnd below)
+    if (ctx->nranks == 1) {
+        const char *sp = getenv("SEM_K1_SPLIT");
+        dm.nbnd = sp ? (int64_t)(atof(sp) * (double)dm.E) : 0;
+    }
     cv.nb1 = ax_cg_blocks(dm);
     cv.nb2 = k2_blocks(dm, false);
     if (cv.nb1 > cv.s1 || cv.nb2 > cv.s2) {
@@ -563,6 +573,24 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
                                cudaMemcpyHostToDevice, s));
             CU(cudaStreamSynchronize(s));
             dm.own = own_d;
+            // boundary elements: every element holding a copy of a node the
+            // exchange reads or writes lies in [0, nbnd) -- derived here from
+            // the plan (mesh->nboundary is only an ordering hint)
+            int64_t nbnd = 0;
+            auto cover = [&](int32_t g) {
+                for (int32_t t = hp.off[g]; t < hp.off[g + 1]; ++t)
+                    nbnd = std::max<int64_t>(nbnd, hp.idx[t] / ctx->n3 + 1);
+            };
+            for (int32_t g : ep.send_group) cover(g);
+            for (int32_t g : ep.if_group) cover(g);
+            dm.nbnd = nbnd;
+            cv.nb1 = ax_cg_blocks(dm);
+            if (cv.nb1 > cv.s1) return fail(ctx, SEM_EINVAL, "too many K1 partials");
+        }
+        if (k1_split(dm)) {
+            CU(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, -1));
+            CU(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
         }
         return SEM_OK;
     }();
@@ -604,6 +632,9 @@ extern "C" void sem_free(sem_ctx *ctx) {
     if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
     if (ctx->replay_exec) cudaGraphExecDestroy(ctx->replay_exec);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+    if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
     if (ctx->comm) comm_free(ctx->comm);
     if (ctx->host_state) cudaFreeHost(ctx->host_state);
     for (auto &r : ctx->recs) {
@@ -712,11 +743,33 @@ static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
     CgVecs &v = ctx->cv;
     const int P = ctx->nranks;
     int rc;
-    LAUNCHP(kProfAxCg, (k == 0 ? 72.0 : 96.0) * ctx->L, k, launch_ax_cg(ctx->dm, v, s));
-    if (P > 1) {
-        if ((rc = exchange_impl(ctx, v.w, s))) return rc;
-        LAUNCH(launch_cg_red_pap(ctx->dm, v, s));
-        if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P, s))) return rc;
+    const double k1_bpn = k == 0 ? 72.0 : 96.0;    // K1 algorithmic bytes per local node
+    if (k1_split(ctx->dm)) {
+        // boundary elements first; the exchange of their w runs on the side
+        // stream while the interior elements' K1 runs here
+        const DevMesh &m = ctx->dm;
+        const int64_t nb = m.nbnd, ni = m.E - m.nbnd;
+        const int gA = ax_cg_range_blocks(m, nb);
+        LAUNCHP(kProfAxCg, k1_bpn * m.n3 * nb, k, launch_ax_cg_range(m, v, 0, nb, 0, s));
+        if (P > 1) {
+            CU(cudaEventRecord(ctx->fork_ev, s));
+            CU(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
+            if ((rc = exchange_impl(ctx, v.w, ctx->side))) return rc;
+            CU(cudaEventRecord(ctx->join_ev, ctx->side));
+        }
+        LAUNCHP(kProfAxCg, k1_bpn * m.n3 * ni, k, launch_ax_cg_range(m, v, nb, ni, gA, s));
+        if (P > 1) {
+            LAUNCH(launch_cg_red_pap(ctx->dm, v, s));
+            CU(cudaStreamWaitEvent(s, ctx->join_ev, 0));
+            if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P, s))) return rc;
+        }
+    } else {
+        LAUNCHP(kProfAxCg, k1_bpn * ctx->L, k, launch_ax_cg(ctx->dm, v, s));
+        if (P > 1) {
+            if ((rc = exchange_impl(ctx, v.w, s))) return rc;
+            LAUNCH(launch_cg_red_pap(ctx->dm, v, s));
+            if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P, s))) return rc;
+        }
     }
     LAUNCHP(kProfK2, k2_bytes(ctx), k, launch_k2(ctx->dm, v, false, s));
     if (P > 1) {

@@ -42,6 +42,7 @@ struct GsClasses {
 struct DevMesh {
     int N, n, n3;
     int64_t E, L;
+    int64_t nbnd;               // elements [0, nbnd) touch a shared (inter-rank) node
     const double *D;            // [n][n] row-major, D[i*n+m] = phi'_m(xi_i)
     const double *G;            // [E][6][n3] rr rs rt ss st tt (w J folded in)
     const double *BM;           // [L] lumped mass w_i w_j w_k J
@@ -84,6 +85,12 @@ cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t
 // CUDA graph of a chunk of iterations is valid for every chunk.
 cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, cudaStream_t s);
 int ax_cg_blocks(const DevMesh &m);   // grid of K1 (= number of its partials)
+// multi-rank TMA/high-order K1 runs as two launches, boundary elements [0, nbnd)
+// first, so the DSSUM exchange overlaps the interior launch
+bool k1_split(const DevMesh &m);
+int ax_cg_range_blocks(const DevMesh &m, int64_t ne);
+cudaError_t launch_ax_cg_range(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne,
+                               int pidx0, cudaStream_t s);
 // mode: 0 = plain dssum, 1 = dssum + mask, 2 = CG iteration (dssum + mask,
 // programmatic dependent of K1, no-op after the stop; v needed)
 cudaError_t launch_gs(const DevMesh &m, double *w, int mode, const CgVecs *v, cudaStream_t s);
@@ -107,11 +114,13 @@ int tma_blocks(int N, int64_t E, int nsm, bool cg);
 cudaError_t tma_prepare(int N);
 cudaError_t upload_const_D(int N, const double *D_host);
 cudaError_t launch_ax_tma(const DevMesh &m, const double *u, double *w, cudaStream_t s);
-cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne,
+                             int pidx0, cudaStream_t s);
 bool hi_supported(int N);
 int hi_blocks(int N, int64_t E, int nsm, bool cg);
 cudaError_t hi_prepare(int N);
 cudaError_t launch_ax_hi(const DevMesh &m, const double *u, double *w, cudaStream_t s);
-cudaError_t launch_ax_cg_hi(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+cudaError_t launch_ax_cg_hi(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne,
+                            int pidx0, cudaStream_t s);
 
 }  // namespace sem

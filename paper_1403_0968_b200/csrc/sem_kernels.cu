@@ -430,9 +430,19 @@ static int ax_grid(int N, int64_t E, int nsm) {
     return nb < 4 * nsm ? (nb < 1 ? 1 : nb) : 4 * nsm;
 }
 
+// grid of K1 over ne elements (range launches: TMA / high-order kernels only)
+int ax_cg_range_blocks(const DevMesh &m, int64_t ne) {
+    if (m.use_hi) return hi_blocks(m.N, ne, m.nsm, true);
+    return m.use_tma ? tma_blocks(m.N, ne, m.nsm, true) : ax_grid(m.N, ne, m.nsm);
+}
+
+bool k1_split(const DevMesh &m) {
+    return m.nranks > 1 && (m.use_tma || m.use_hi) && m.nbnd > 0 && m.nbnd < m.E;
+}
+
 int ax_cg_blocks(const DevMesh &m) {
-    if (m.use_hi) return hi_blocks(m.N, m.E, m.nsm, true);
-    return m.use_tma ? tma_blocks(m.N, m.E, m.nsm, true) : ax_grid(m.N, m.E, m.nsm);
+    if (k1_split(m)) return ax_cg_range_blocks(m, m.nbnd) + ax_cg_range_blocks(m, m.E - m.nbnd);
+    return ax_cg_range_blocks(m, m.E);
 }
 
 static int grid_for(int64_t L, int threads) {
@@ -461,13 +471,20 @@ cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t
 }
 
 cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
-    if (m.use_hi) return launch_ax_cg_hi(m, v, s);
-    if (m.use_tma) return launch_ax_cg_tma(m, v, s);
+    if (m.use_hi) return launch_ax_cg_hi(m, v, 0, m.E, 0, s);
+    if (m.use_tma) return launch_ax_cg_tma(m, v, 0, m.E, 0, s);
     AxCgArgs a{v.r, v.p, v.xw, make_red(m, v), v.part1, v.st};
     cudaError_t e = cudaSuccess;
     SEM_DISPATCH_N(m.N, (e = launch_pdl(ax_kernel<NN, true>, ax_grid(m.N, m.E, m.nsm), AxCfg<NN>::NT,
                                         0, s, m.E, m.D, m.G, (const double *)nullptr, v.w, a)));
     return e;
+}
+
+cudaError_t launch_ax_cg_range(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne, int pidx0,
+                               cudaStream_t s) {
+    if (m.use_hi) return launch_ax_cg_hi(m, v, eb, ne, pidx0, s);
+    if (m.use_tma) return launch_ax_cg_tma(m, v, eb, ne, pidx0, s);
+    return cudaErrorInvalidValue;   // the simple kernel covers all elements only
 }
 
 cudaError_t launch_gs(const DevMesh &m, double *w, int mode, const CgVecs *v, cudaStream_t s) {

@@ -28,14 +28,19 @@ def relerr(a, b):
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
-@pytest.fixture(params=["tma", "hi", "simple", "tma-nograph"])
+@pytest.fixture(params=["tma", "hi", "simple", "tma-nograph", "tma-split", "hi-split"])
 def impl(request, monkeypatch):
     """All Ax kernel families -- element-staged TMA (N <= 10), vector-staged TMA
     with register-streamed G^ ("hi", N >= 6; lower N fall back to TMA), the
     simple one-block-per-element kernel (all N) -- and the CG driver with and
-    without CUDA-graph chunks."""
+    without CUDA-graph chunks.  "-split": K1 as two element-range launches
+    (the multi-rank boundary/interior schedule, here without an exchange)."""
     monkeypatch.setenv("SEM_AX_KERNEL", request.param.split("-")[0])
     monkeypatch.setenv("SEM_CG_GRAPH", "0" if request.param.endswith("nograph") else "1")
+    if request.param.endswith("split"):
+        monkeypatch.setenv("SEM_K1_SPLIT", "0.37")
+    else:
+        monkeypatch.delenv("SEM_K1_SPLIT", raising=False)
     return request.param
 
 
