@@ -145,10 +145,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 }
 
 struct TmaArgs {
-    int64_t E;            // elements of this launch: [eb, eb + E)
-    int64_t eb;
-    int64_t Ltot;         // length of the E-vectors (all elements of the rank)
-    int pidx0;            // first (p, A p) partial slot of this launch
+    int64_t E;
     const double *G;
     // plain: u -> w.  CG: r, p (in/out), x (in/out, the solve's x work vector) -> w
     const double *u;
@@ -183,10 +180,9 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
     uint64_t *gbar = bars + 2 * g;
 
     const int64_t nunits = (a.E + EPG - 1) / EPG;
-    const int64_t eend = a.eb + a.E;
     const int64_t TG = int64_t(gridDim.x) * NG;
     const int64_t u0 = int64_t(blockIdx.x) * NG + g;
-    const int64_t L = a.Ltot;
+    const int64_t L = a.E * n3;
 
     if (leader) {
         mbar_init(gbar + 0, 1);
@@ -205,8 +201,8 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
     // memory, the arrival (release), then the vector bulk copies.
     auto unit_bytes = [&](int64_t unit, VecRange &vr, int64_t &first, int64_t &nd, uint32_t &vb,
                           uint32_t &gb) {
-        const int64_t e0 = a.eb + unit * EPG;
-        const int64_t ne = (eend - e0 < EPG) ? (eend - e0) : EPG;
+        const int64_t e0 = unit * EPG;
+        const int64_t ne = (a.E - e0 < EPG) ? (a.E - e0) : EPG;
         first = e0 * n3;
         nd = ne * n3;
         vr = vec_range(first, nd, L);
@@ -220,7 +216,7 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
         unit_bytes(unit, vr, first, nd, vb, gb);
         double *sb = stage0 + size_t(s) * STAGE;
         mbar_expect_tx_only(gbar + s, NV * vb + gb);
-        bulk_g2s(sb + NV * VL, a.G + (a.eb + unit * EPG) * 6 * n3, gb, gbar + s, pol_g);
+        bulk_g2s(sb + NV * VL, a.G + unit * EPG * 6 * n3, gb, gbar + s, pol_g);
     };
     auto issue_V = [&](int64_t unit, int s) {
         VecRange vr;
@@ -286,9 +282,9 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
     for (int64_t unit = u0; unit < nunits; unit += TG, ++t) {
         const int s = t & 1;
         double *sb = stage0 + size_t(s) * STAGE;
-        const int64_t e0 = a.eb + unit * EPG;
+        const int64_t e0 = unit * EPG;
         const int64_t e = e0 + el;
-        const bool on = lane_on && (e < eend);
+        const bool on = lane_on && (e < a.E);
         const int sh = (int)((e0 * n3) & 1);  // element data offset in each vector slot
         mbar_wait(gbar + s, (t >> 1) & 1);
 
@@ -388,7 +384,7 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
         // weights, no assembly.  One deterministic partial per CTA; the
         // consumers reduce them (see cg_device.cuh).
         const double bs = block_sum<Lo::NT>(pap, sred);
-        if (tid == 0) a.part1[(kit & 1) * a.red.s1 + a.pidx0 + blockIdx.x] = bs;
+        if (tid == 0) a.part1[(kit & 1) * a.red.s1 + blockIdx.x] = bs;
     }
 }
 
@@ -445,10 +441,9 @@ __global__ void __launch_bounds__(HiCfg<N, CG>::NT, 1) ax_hi_kernel(TmaArgs a) {
     uint64_t *vbar = bars + (2 + R) * g;                    // element stages
     uint64_t *gbar = vbar + 2;                              // G^ ring slots
     const int64_t TG = int64_t(gridDim.x) * NG;
-    const int64_t e0 = a.eb + int64_t(blockIdx.x) * NG + g;
-    const int64_t eend = a.eb + a.E;
-    const int64_t L = a.Ltot;
-    const int64_t nel = (e0 < eend) ? (eend - e0 + TG - 1) / TG : 0;   // elements of this group
+    const int64_t e0 = int64_t(blockIdx.x) * NG + g;
+    const int64_t L = a.E * n3;
+    const int64_t nel = (e0 < a.E) ? (a.E - e0 + TG - 1) / TG : 0;   // elements of this group
     const int64_t nsl = nel * n;                                     // G^ slices of this group
     for (int t = tid; t < n2; t += C::NT) sD[(t / n) * DS + t % n] = c_D[DO + t];
     if (leader) {
@@ -605,7 +600,7 @@ __global__ void __launch_bounds__(HiCfg<N, CG>::NT, 1) ax_hi_kernel(TmaArgs a) {
     }
     if constexpr (CG) {
         const double bs = block_sum<C::NT>(pap, sred);
-        if (tid == 0) a.part1[(kit & 1) * a.red.s1 + a.pidx0 + blockIdx.x] = bs;
+        if (tid == 0) a.part1[(kit & 1) * a.red.s1 + blockIdx.x] = bs;
     }
 }
 
@@ -664,8 +659,6 @@ cudaError_t tma_prepare(int N) {
 cudaError_t launch_ax_tma(const DevMesh &m, const double *u, double *w, cudaStream_t s) {
     TmaArgs a{};
     a.E = m.E;
-    a.eb = 0;
-    a.Ltot = m.L;
     a.G = m.G;
     a.u = u;
     a.w = w;
@@ -725,8 +718,6 @@ cudaError_t hi_prepare(int N) {
 cudaError_t launch_ax_hi(const DevMesh &m, const double *u, double *w, cudaStream_t s) {
     TmaArgs a{};
     a.E = m.E;
-    a.eb = 0;
-    a.Ltot = m.L;
     a.G = m.G;
     a.u = u;
     a.w = w;
@@ -736,21 +727,21 @@ cudaError_t launch_ax_hi(const DevMesh &m, const double *u, double *w, cudaStrea
     return cudaGetLastError();
 }
 
-// K1 over the element range [eb, eb + ne); its per-CTA (p, A p) partials go
-// to slots [pidx0, pidx0 + grid) of part1.
+// K1 over the element range [eb, eb + ne): the kernels see a mesh of ne
+// elements through pointers offset by eb (eb * n^3 must be even: the bulk
+// copies of the vectors need 16-byte aligned sources), and write their
+// per-CTA (p, A p) partials to slots [pidx0, pidx0 + grid) of part1.
 static TmaArgs cg_args(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne, int pidx0) {
+    const int64_t o = eb * m.n3;
     TmaArgs a{};
     a.E = ne;
-    a.eb = eb;
-    a.Ltot = m.L;
-    a.pidx0 = pidx0;
-    a.G = m.G;
-    a.r = v.r;
-    a.p = v.p;
-    a.x = v.xw;
-    a.w = v.w;
+    a.G = m.G + 6 * o;
+    a.r = v.r + o;
+    a.p = v.p + o;
+    a.x = v.xw + o;
+    a.w = v.w + o;
     a.red = make_red(m, v);
-    a.part1 = v.part1;
+    a.part1 = v.part1 + pidx0;
     a.st = v.st;
     return a;
 }

@@ -517,6 +517,7 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
     if (ctx->nranks == 1) {
         const char *sp = getenv("SEM_K1_SPLIT");
         dm.nbnd = sp ? (int64_t)(atof(sp) * (double)dm.E) : 0;
+        if (dm.n3 & 1) dm.nbnd += dm.nbnd & 1;     // range launches need eb n^3 even
     }
     cv.nb1 = ax_cg_blocks(dm);
     cv.nb2 = k2_blocks(dm, false);
@@ -583,6 +584,7 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
             };
             for (int32_t g : ep.send_group) cover(g);
             for (int32_t g : ep.if_group) cover(g);
+            if (dm.n3 & 1) nbnd += nbnd & 1;            // range launches need eb n^3 even
             dm.nbnd = nbnd;
             cv.nb1 = ax_cg_blocks(dm);
             if (cv.nb1 > cv.s1) return fail(ctx, SEM_EINVAL, "too many K1 partials");
