@@ -48,8 +48,11 @@ def lib():
         L.ora_multiplicity.argtypes = [i64, P, P]
         L.ora_cg.argtypes = [ctypes.c_int, i64, P, P, P, P, P, ctypes.c_double,
                              ctypes.c_int, P, P]
+        L.ora_ax_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P, P]
+        L.ora_cg_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P, P, P, P,
+                                      ctypes.c_double, ctypes.c_int, P, P]
         for f in (L.ora_gll, L.ora_deriv, L.ora_geom, L.ora_ax, L.ora_dssum,
-                  L.ora_multiplicity, L.ora_cg):
+                  L.ora_multiplicity, L.ora_cg, L.ora_ax_screened, L.ora_cg_screened):
             f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -57,6 +60,19 @@ def lib():
 
 def _p(a: np.ndarray):
     return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _opt(a, size):
+    """Optional per-node coefficient array -> contiguous float64 (or None)."""
+    if a is None:
+        return None
+    a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+    assert a.size == size
+    return a
+
+
+def _po(a):
+    return None if a is None else _p(a)
 
 
 class OracleError(RuntimeError):
@@ -98,15 +114,22 @@ def geom(N: int, xyz: np.ndarray):
     return G, J
 
 
-def ax(N: int, G: np.ndarray, u: np.ndarray) -> np.ndarray:
-    """O4: local unassembled unmasked w = A_L u (eq:semOperator)."""
+def ax(N: int, G: np.ndarray, u: np.ndarray, J=None, kappa=None, alpha=None) -> np.ndarray:
+    """O4: local unassembled unmasked w = A_L u (eq:semOperator).
+    With kappa / alpha (per local node; NEXT-1, eq:semPDE :580-586) the
+    screened-Coulomb operator D^T (kappa G^) D + alpha W J (J needed with alpha)."""
     n3 = (N + 1) ** 3
     G = np.ascontiguousarray(G, dtype=np.float64)
     E = G.size // (6 * n3)
     u = np.ascontiguousarray(u, dtype=np.float64).reshape(-1)
     assert u.size == E * n3
     w = np.zeros(E * n3)
-    _check(lib().ora_ax(N, E, _p(G), _p(u), _p(w)), "ora_ax")
+    if J is None and kappa is None and alpha is None:
+        _check(lib().ora_ax(N, E, _p(G), _p(u), _p(w)), "ora_ax")
+        return w
+    J, kappa, alpha = (_opt(a, E * n3) for a in (J, kappa, alpha))
+    _check(lib().ora_ax_screened(N, E, _p(G), _po(J), _po(kappa), _po(alpha), _p(u), _p(w)),
+           "ora_ax_screened")
     return w
 
 
@@ -126,9 +149,11 @@ def multiplicity(glo: np.ndarray) -> np.ndarray:
     return m
 
 
-def cg(N: int, glo, dirichlet, G, b, x0=None, tol=1e-8, maxit=1000):
+def cg(N: int, glo, dirichlet, G, b, x0=None, tol=1e-8, maxit=1000, J=None, kappa=None,
+       alpha=None):
     """O7: CG (PCG of PAPER.md:672-673, identity preconditioner).
-    Returns (x, iters, rel_res, status) with status 0 = converged, 4 = maxit."""
+    Returns (x, iters, rel_res, status) with status 0 = converged, 4 = maxit.
+    kappa / alpha (+ J): the screened-Coulomb operator of ax() (NEXT-1)."""
     n3 = (N + 1) ** 3
     glo = np.ascontiguousarray(glo, dtype=np.int64).reshape(-1)
     dirichlet = np.ascontiguousarray(dirichlet, dtype=np.uint8).reshape(-1)
@@ -138,8 +163,14 @@ def cg(N: int, glo, dirichlet, G, b, x0=None, tol=1e-8, maxit=1000):
     x = np.zeros(E * n3) if x0 is None else np.array(x0, dtype=np.float64).reshape(-1).copy()
     iters = ctypes.c_int(0)
     rel = ctypes.c_double(0.0)
-    rc = lib().ora_cg(N, E, _p(glo), _p(dirichlet), _p(G), _p(b), _p(x), float(tol),
-                      int(maxit), ctypes.byref(iters), ctypes.byref(rel))
+    if J is None and kappa is None and alpha is None:
+        rc = lib().ora_cg(N, E, _p(glo), _p(dirichlet), _p(G), _p(b), _p(x), float(tol),
+                          int(maxit), ctypes.byref(iters), ctypes.byref(rel))
+    else:
+        J, kappa, alpha = (_opt(a, E * n3) for a in (J, kappa, alpha))
+        rc = lib().ora_cg_screened(N, E, _p(glo), _p(dirichlet), _p(G), _po(J), _po(kappa),
+                                   _po(alpha), _p(b), _p(x), float(tol), int(maxit),
+                                   ctypes.byref(iters), ctypes.byref(rel))
     if rc not in (0, 4):
         raise OracleError(f"ora_cg failed with status {rc}")
     return x, iters.value, rel.value, rc

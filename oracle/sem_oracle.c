@@ -186,10 +186,22 @@ int ora_geom(int N, int64_t E, const double *xyz, double *G, double *Jout)
  *   u_r[ijk] = sum_m D_im u[mjk],  u_s[ijk] = sum_m D_jm u[imk],
  *   u_t[ijk] = sum_m D_km u[ijm]
  *   (f_r, f_s, f_t) = G^ (u_r, u_s, u_t)      (G^ symmetric, 6 factors)
- *   w[ijk] = sum_m D_mi f_r[mjk] + sum_m D_mj f_s[imk] + sum_m D_mk f_t[ijm]  */
-int ora_ax(int N, int64_t E, const double *G, const double *u, double *w)
+ *   w[ijk] = sum_m D_mi f_r[mjk] + sum_m D_mj f_s[imk] + sum_m D_mk f_t[ijm]
+ *
+ * NEXT-1, the full screened-Coulomb operator of eq:semPDE (PAPER.md:580-586,
+ * -div(kappa grad u) + alpha u = f) in the weak form eq:semOperator
+ * (:593-596) = stiffness + mass:
+ *   - kappa(x) weights the flux at each quadrature node (reading G2: the
+ *     paper's u^ = kappa u at :664 is read as kappa multiplying G^ pointwise):
+ *       (f_r, f_s, f_t) = kappa_ijk G^ (u_r, u_s, u_t)
+ *   - the mass operator is the lumped diagonal J w_abc of :605-614, scaled by
+ *     alpha(x) at the node:  w[ijk] += alpha_ijk w_i w_j w_k J_ijk u[ijk]
+ * kappa == NULL means kappa = 1; alpha == NULL means alpha = 0 (J unused).  */
+int ora_ax_screened(int N, int64_t E, const double *G, const double *J, const double *kappa,
+                    const double *alpha, const double *u, double *w)
 {
     if (N < 1 || N > 32 || E < 0 || (E > 0 && (!G || !u || !w))) return ORA_EINVAL;
+    if (E > 0 && alpha && !J) return ORA_EINVAL;
     int n = N + 1, n3 = n * n * n;
     double xi[33], wq[33];
     double *D = (double *)malloc(sizeof(double) * n * n);
@@ -217,6 +229,12 @@ int ora_ax(int N, int64_t E, const double *G, const double *u, double *w)
                     fr[q] = grr * ur + grs * us + grt * ut;
                     fs[q] = grs * ur + gss * us + gst * ut;
                     ft[q] = grt * ur + gst * us + gtt * ut;
+                    if (kappa) {
+                        double kq = kappa[e * n3 + q];
+                        fr[q] = kq * fr[q];
+                        fs[q] = kq * fs[q];
+                        ft[q] = kq * ft[q];
+                    }
                 }
         for (int k = 0; k < n; ++k)
             for (int j = 0; j < n; ++j)
@@ -225,7 +243,10 @@ int ora_ax(int N, int64_t E, const double *G, const double *u, double *w)
                     for (int m = 0; m < n; ++m) s += D[m * n + i] * fr[m + n * j + n * n * k];
                     for (int m = 0; m < n; ++m) s += D[m * n + j] * fs[i + n * m + n * n * k];
                     for (int m = 0; m < n; ++m) s += D[m * n + k] * ft[i + n * j + n * n * m];
-                    we[i + n * j + n * n * k] = s;
+                    int q = i + n * j + n * n * k;
+                    if (alpha)
+                        s += alpha[e * n3 + q] * (wq[i] * wq[j] * wq[k] * J[e * n3 + q]) * ue[q];
+                    we[q] = s;
                 }
     }
     free(D);
@@ -233,6 +254,11 @@ int ora_ax(int N, int64_t E, const double *G, const double *u, double *w)
     free(fs);
     free(ft);
     return ORA_OK;
+}
+
+int ora_ax(int N, int64_t E, const double *G, const double *u, double *w)
+{
+    return ora_ax_screened(N, E, G, NULL, NULL, NULL, u, w);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -304,21 +330,31 @@ static double dot_c(int64_t L, const double *c, const double *a, const double *b
     return s;
 }
 
-static void apply_op(int N, int64_t E, const double *G, const int64_t *glo,
+/* the operator's coefficients (NULL: Poisson) */
+typedef struct {
+    const double *J, *kappa, *alpha;
+} ora_coef;
+
+static void apply_op(int N, int64_t E, const double *G, const ora_coef *cf, const int64_t *glo,
                      const int64_t *order, const double *mask, const double *in,
                      double *out)
 {
     int64_t L = E * (N + 1) * (N + 1) * (N + 1);
-    ora_ax(N, E, G, in, out);
+    ora_ax_screened(N, E, G, cf->J, cf->kappa, cf->alpha, in, out);
     dssum_sorted(L, glo, order, out);
     for (int64_t l = 0; l < L; ++l) out[l] = mask[l] * out[l];
 }
 
-int ora_cg(int N, int64_t E, const int64_t *glo, const uint8_t *dirichlet,
-           const double *G, const double *b, double *x, double tol, int maxit,
-           int *iters, double *rel_res)
+/* CG on the screened-Coulomb operator (NEXT-1; same recurrence as O7, the
+ * operator is ora_ax_screened's).  ora_cg is the Poisson case. */
+int ora_cg_screened(int N, int64_t E, const int64_t *glo, const uint8_t *dirichlet,
+                    const double *G, const double *J, const double *kappa, const double *alpha,
+                    const double *b, double *x, double tol, int maxit, int *iters,
+                    double *rel_res)
 {
     if (N < 1 || N > 32 || E < 0 || maxit < 0 || !(tol >= 0.0)) return ORA_EINVAL;
+    if (alpha && !J) return ORA_EINVAL;
+    const ora_coef cf = {J, kappa, alpha};
     int64_t L = E * (N + 1) * (N + 1) * (N + 1);
     double *mask = (double *)malloc(sizeof(double) * (L + 1));
     double *c = (double *)malloc(sizeof(double) * (L + 1));
@@ -333,7 +369,7 @@ int ora_cg(int N, int64_t E, const int64_t *glo, const uint8_t *dirichlet,
     dssum_sorted(L, glo, order, c);             /* c = multiplicity m */
     for (int64_t l = 0; l < L; ++l) c[l] = mask[l] / c[l];
 
-    apply_op(N, E, G, glo, order, mask, x, w);  /* w = mask QQ^T A_L x0 */
+    apply_op(N, E, G, &cf, glo, order, mask, x, w);  /* w = mask QQ^T A_L x0 */
     for (int64_t l = 0; l < L; ++l) r[l] = mask[l] * b[l] - w[l];
     for (int64_t l = 0; l < L; ++l) p[l] = 0.0;
     double rho = dot_c(L, c, r, r), rho0 = rho, rho_old = 0.0;
@@ -346,7 +382,7 @@ int ora_cg(int N, int64_t E, const int64_t *glo, const uint8_t *dirichlet,
         while (k < maxit && sqrt(rho) > tol * sqrt(rho0)) {
             double beta = (k == 0) ? 0.0 : rho / rho_old;
             for (int64_t l = 0; l < L; ++l) p[l] = r[l] + beta * p[l];
-            apply_op(N, E, G, glo, order, mask, p, w);
+            apply_op(N, E, G, &cf, glo, order, mask, p, w);
             double alpha = rho / dot_c(L, c, w, p);
             for (int64_t l = 0; l < L; ++l) x[l] += alpha * p[l];
             for (int64_t l = 0; l < L; ++l) r[l] -= alpha * w[l];
@@ -365,4 +401,12 @@ int ora_cg(int N, int64_t E, const int64_t *glo, const uint8_t *dirichlet,
     free(w);
     free(order);
     return status;
+}
+
+int ora_cg(int N, int64_t E, const int64_t *glo, const uint8_t *dirichlet,
+           const double *G, const double *b, double *x, double tol, int maxit,
+           int *iters, double *rel_res)
+{
+    return ora_cg_screened(N, E, glo, dirichlet, G, NULL, NULL, NULL, b, x, tol, maxit, iters,
+                           rel_res);
 }

@@ -78,7 +78,10 @@ def default_parts(nranks: int):
 
 
 def box_mesh(N: int, r1d, elems=(2, 2, 2), lengths=(1.0, 1.0, 1.0), eps: float = 0.0,
-             parts=(1, 1, 1), rank: int = 0, boundary_first: bool = False) -> Mesh:
+             parts=(1, 1, 1), rank: int = 0, boundary_first: bool = False,
+             dirichlet_faces: bool = True) -> Mesh:
+    """dirichlet_faces=False: no Dirichlet nodes (natural boundary; the
+    screened operator with alpha > 0 is SPD without a mask)."""
     r1d = np.asarray(r1d, dtype=np.float64)
     n = N + 1
     assert r1d.shape == (n,), "r1d must hold the N+1 reference node positions"
@@ -114,6 +117,8 @@ def box_mesh(N: int, r1d, elems=(2, 2, 2), lengths=(1.0, 1.0, 1.0), eps: float =
     glo = (I + nx * (J + ny * K)).astype(np.int64)
     dirichlet = ((I == 0) | (I == ex * N) | (J == 0) | (J == ey * N) |
                  (K == 0) | (K == ez * N)).astype(np.uint8)
+    if not dirichlet_faces:
+        dirichlet[:] = 0
     # affine placement: x = (a + (1 + r_i)/2) * hx  (exact at shared faces)
     x = (a[:, None] + (1.0 + r1d[i])[None, :] / 2.0) * (Lx / ex)
     y = (b[:, None] + (1.0 + r1d[j])[None, :] / 2.0) * (Ly / ey)
@@ -152,3 +157,18 @@ def cube_poly(mesh: Mesh):
     us = gx * gy * gz
     f = 2.0 * (gy * gz + gx * gz + gx * gy)
     return us.reshape(-1), f.reshape(-1)
+
+
+def coefficients(mesh: Mesh, kappa_amp: float = 0.5, alpha0: float = 1.0):
+    """Smooth material coefficients of the screened-Coulomb workload (NEXT-1,
+    eq:semPDE kappa(x), alpha(x)), evaluated at the node coordinates (so every
+    copy of a shared node gets the same values):
+        kappa = 1 + a sin(2 pi x/Lx) cos(pi y/Ly) cos(2 pi z/Lz)   in [1-a, 1+a]
+        alpha = alpha0 (1 + 0.5 cos(pi x/Lx) cos(pi y/Ly))          in [alpha0/2, 3 alpha0/2]
+    Returns (kappa, alpha), each [E * n^3]."""
+    Lx, Ly, Lz = mesh.lengths
+    x, y, z = mesh.xyz[:, 0], mesh.xyz[:, 1], mesh.xyz[:, 2]
+    kappa = 1.0 + kappa_amp * (np.sin(2 * np.pi * x / Lx) * np.cos(np.pi * y / Ly)
+                               * np.cos(2 * np.pi * z / Lz))
+    alpha = alpha0 * (1.0 + 0.5 * np.cos(np.pi * x / Lx) * np.cos(np.pi * y / Ly))
+    return np.ascontiguousarray(kappa.reshape(-1)), np.ascontiguousarray(alpha.reshape(-1))

@@ -62,9 +62,12 @@ def ref_grad_ops(Dv):
     return Dr, Ds, Dt
 
 
-def element_stiffness_physical(xyz_e, xi, w):
+def element_stiffness_physical(xyz_e, xi, w, kappa=None, alpha=None):
     """Dense n^3 x n^3 element stiffness by the physical-gradient route.
-    xyz_e: [3, n^3] node coordinates.  Returns (A, J)."""
+    xyz_e: [3, n^3] node coordinates.  Returns (A, J).
+    kappa / alpha ([n^3], optional): the screened-Coulomb element matrix
+        sum_c Grad_c^T diag(w J kappa) Grad_c + diag(w J alpha)
+    (quadrature of (kappa grad u, grad v) + (alpha u, v) at the GLL nodes)."""
     n = len(xi)
     Dv = deriv_vandermonde(xi)
     Dr, Ds, Dt = ref_grad_ops(Dv)
@@ -78,9 +81,12 @@ def element_stiffness_physical(xyz_e, xi, w):
     inv = np.linalg.inv(jac)          # inv[q, a, c] = d r_a / d x_c
     w3 = np.einsum("k,j,i->kji", w, w, w).reshape(-1)
     A = np.zeros((n ** 3, n ** 3))
+    wk = w3 * J if kappa is None else w3 * J * np.asarray(kappa)
     for c in range(3):
         Gc = sum(inv[:, a, c][:, None] * ops[a] for a in range(3))
-        A += Gc.T @ ((w3 * J)[:, None] * Gc)
+        A += Gc.T @ (wk[:, None] * Gc)
+    if alpha is not None:
+        A += np.diag(w3 * J * np.asarray(alpha))
     return A, J
 
 
