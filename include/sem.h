@@ -84,6 +84,15 @@ typedef struct {
     sem_allgather_fn allgather;/* setup-time host all-gather, required if nranks > 1         */
     void *allgather_user;
     int32_t device;            /* CUDA device ordinal                                        */
+    /* Screened-Coulomb coefficients (eq:semPDE -div(kappa grad u) + alpha u = f,
+     * PAPER.md:580-586).  HOST [E][(N+1)^3] values at the
+     * GLL nodes, read during sem_setup only.  NULL: kappa = 1 / alpha = 0 (the
+     * Poisson operator).  kappa must be > 0 and finite, alpha >= 0 and finite,
+     * else SEM_EINVAL.  kappa weights the flux pointwise (folded into G^ at setup,
+     * DESIGN.md reading G2); alpha adds the lumped mass alpha w_i w_j w_k J
+     * to the local operator (+8 B per node per apply).      */
+    const double *kappa;
+    const double *alpha;
 } sem_mesh;
 
 typedef struct sem_ctx sem_ctx;  /* opaque; created by sem_setup, destroyed by sem_free */

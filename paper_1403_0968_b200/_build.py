@@ -10,8 +10,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libsem.so")
-SOURCES = ["sem_kernels.cu", "ax_tma.cu", "cg_update.cu", "sem_host.cpp", "sem_comm.cu"]
-HEADERS = ["sem_internal.h", "sem_comm.h", "cg_device.cuh"]
+SOURCES = ["sem_kernels.cu", "ax_tma.cu", "ax_tma_mass.cu", "cg_update.cu", "sem_host.cpp",
+           "sem_comm.cu"]
+HEADERS = ["sem_internal.h", "sem_comm.h", "cg_device.cuh", "ax_tma.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -36,20 +37,36 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = True) -> str:
+    """Compile every translation unit in parallel (nvcc -c), then link."""
     if not force and not needs_build():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+    import tempfile
     inc, lib = nccl_dirs()
-    tmp = LIB + ".tmp"
-    cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-O2", "--shared", "-Xptxas", "-warn-spills",
-           "-I", os.path.join(ROOT, "include"), "-I", inc,
-           *[os.path.join(CSRC, f) for f in SOURCES],
-           "-o", tmp, "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}",
-           "-lcudart"]
+    tmpdir = tempfile.mkdtemp(prefix="semobj_")
+    common = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-Xcompiler", "-O2", "-Xptxas", "-warn-spills",
+              "-I", os.path.join(ROOT, "include"), "-I", inc]
+    objs = [os.path.join(tmpdir, os.path.splitext(f)[0] + ".o") for f in SOURCES]
+    cmds = [common + ["-c", os.path.join(CSRC, f), "-o", o] for f, o in zip(SOURCES, objs)]
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd, cwd=CSRC)
+        print(" ".join(cmds[0]), "... (x%d, parallel)" % len(cmds), file=sys.stderr)
+    with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+        procs = list(ex.map(lambda c: subprocess.run(c, cwd=CSRC, capture_output=True, text=True),
+                            cmds))
+    for c, p in zip(cmds, procs):
+        if verbose and p.stderr:
+            sys.stderr.write(p.stderr)
+        if p.returncode != 0:
+            raise subprocess.CalledProcessError(p.returncode, c, p.stdout, p.stderr)
+    tmp = LIB + ".tmp"
+    link = ["nvcc", *ARCH, "--shared", *objs, "-o", tmp, "-L", lib, "-l:libnccl.so.2",
+            "-Xlinker", f"-rpath={lib}", "-lcudart"]
+    subprocess.check_call(link, cwd=CSRC)
     os.replace(tmp, LIB)
+    for o in objs:
+        os.remove(o)
+    os.rmdir(tmpdir)
     return LIB
 
 

@@ -216,13 +216,13 @@ static void diff_matrix(int N, const double *x, double *D) {
 // ---------------------------------------------------------------------------
 namespace {
 struct Layout {
-    size_t G, BM, r, p, w, xw, D, gs_idx, own, partials, rr_all, pap_all, st, total;
+    size_t G, BM, H, r, p, w, xw, D, gs_idx, own, partials, rr_all, pap_all, st, total;
     int64_t nsurf_cap, partial_cap;
 };
 
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
-Layout make_layout(int N, int64_t E, int nranks) {
+Layout make_layout(int N, int64_t E, int nranks, bool mass) {
     Layout Lo{};
     const int64_t n = N + 1, n3 = n * n * n, L = E * n3;
     const int64_t ni = (n >= 2) ? (n - 2) : 0;
@@ -237,6 +237,7 @@ Layout make_layout(int N, int64_t E, int nranks) {
     };
     Lo.G = take(sizeof(double) * 6 * L);
     Lo.BM = take(sizeof(double) * L);
+    Lo.H = mass ? take(sizeof(double) * L) : 0;
     Lo.r = take(sizeof(double) * L);
     Lo.p = take(sizeof(double) * L);
     Lo.w = take(sizeof(double) * L);
@@ -269,7 +270,7 @@ extern "C" int sem_workspace_bytes(const sem_mesh *m, int N, size_t *bytes) {
     int rc = check_mesh(m, N);
     if (rc) return rc;
     if (!bytes) return fail(nullptr, SEM_EINVAL, "bytes is NULL");
-    *bytes = make_layout(N, m->nelem, m->nranks).total;
+    *bytes = make_layout(N, m->nelem, m->nranks, m->alpha != nullptr).total;
     return SEM_OK;
 }
 
@@ -431,7 +432,16 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         return fail(nullptr, SEM_EINVAL, "workspace must be 256-byte aligned");
     if (mesh->nranks > 1 && (!mesh->nccl_id || !mesh->allgather))
         return fail(nullptr, SEM_EINVAL, "nranks > 1 needs nccl_id and allgather");
-    const Layout Lo = make_layout(N, mesh->nelem, mesh->nranks);
+    const Layout Lo = make_layout(N, mesh->nelem, mesh->nranks, mesh->alpha != nullptr);
+    {
+        const int64_t Lh = int64_t(mesh->nelem) * (N + 1) * (N + 1) * (N + 1);
+        for (int64_t l = 0; mesh->kappa && l < Lh; ++l)
+            if (!(mesh->kappa[l] > 0.0) || !std::isfinite(mesh->kappa[l]))
+                return fail(nullptr, SEM_EINVAL, "kappa[%lld] must be > 0 and finite", (long long)l);
+        for (int64_t l = 0; mesh->alpha && l < Lh; ++l)
+            if (!(mesh->alpha[l] >= 0.0) || !std::isfinite(mesh->alpha[l]))
+                return fail(nullptr, SEM_EINVAL, "alpha[%lld] must be >= 0 and finite", (long long)l);
+    }
     if (bytes < Lo.total)
         return fail(nullptr, SEM_EINVAL, "workspace too small: %zu < %zu", bytes, Lo.total);
     *out = nullptr;
@@ -474,6 +484,7 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
     dm.D = reinterpret_cast<double *>(ws + Lo.D);
     dm.G = reinterpret_cast<double *>(ws + Lo.G);
     dm.BM = reinterpret_cast<double *>(ws + Lo.BM);
+    dm.H = mesh->alpha ? reinterpret_cast<double *>(ws + Lo.H) : nullptr;
     dm.cls = hp.cls;
     dm.gs_idx = reinterpret_cast<int32_t *>(ws + Lo.gs_idx);
     dm.ngroups = hp.ngroups;
@@ -504,11 +515,17 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         // measured c4 sweep (profiles/order_sweep_r01*.json): element-staged
         // TMA wins up to N = 10, slice-streamed from N = 11
         const int hi_min = himin ? atoi(himin) : 11;
-        const bool force_simple = impl && strcmp(impl, "simple") == 0;
+        // (the simple kernel has no mass term: not used for screened operators)
+        const bool force_simple = impl && strcmp(impl, "simple") == 0 && !dm.H;
         const bool force_tma = impl && strcmp(impl, "tma") == 0;
         const bool force_hi = impl && strcmp(impl, "hi") == 0;
         dm.use_hi = !force_simple && !force_tma && hi_supported(N) && (force_hi || N >= hi_min);
         dm.use_tma = !force_simple && !dm.use_hi && tma_supported(N);
+        if (dm.H && !dm.use_tma && !dm.use_hi) {   // only TMA / hi carry the mass term
+            dm.use_hi = hi_supported(N) && N >= hi_min;
+            dm.use_tma = !dm.use_hi && tma_supported(N);
+            if (!dm.use_tma && !dm.use_hi) dm.use_hi = hi_supported(N);
+        }
         const char *gr = getenv("SEM_CG_GRAPH");
         ctx->use_graph = !(gr && strcmp(gr, "0") == 0);
     }
@@ -535,8 +552,8 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         cudaStream_t s = ctx->stream;
         CU(cudaHostAlloc(&ctx->host_state, 2 * sizeof(CgState), cudaHostAllocDefault));
         CU(upload_const_D(N, Dh.data()));
-        if (dm.use_tma) CU(tma_prepare(N));
-        if (dm.use_hi) CU(hi_prepare(N));
+        if (dm.use_tma) CU(tma_prepare(N, dm.H != nullptr));
+        if (dm.use_hi) CU(hi_prepare(N, dm.H != nullptr));
         CU(cudaEventCreateWithFlags(&ctx->ev[0], cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&ctx->ev[1], cudaEventDisableTiming));
         CU(cudaMemcpyAsync((void *)dm.D, Dh.data(), sizeof(double) * Dh.size(),
@@ -552,8 +569,15 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         int *bad_d = reinterpret_cast<int *>(cv.part1);
         CU(cudaMemcpyAsync(xyz_d, mesh->xyz, sizeof(double) * 3 * ctx->L, cudaMemcpyHostToDevice, s));
         CU(cudaMemsetAsync(bad_d, 0, sizeof(int), s));
-        LAUNCH(launch_geom(dm, xyz_d, const_cast<double *>(dm.G), const_cast<double *>(dm.BM),
-                           bad_d, s));
+        // kappa -> xw (scratch at setup); alpha -> H (scaled in place by w J)
+        double *kappa_d = mesh->kappa ? cv.xw : nullptr;
+        if (kappa_d)
+            CU(cudaMemcpyAsync(kappa_d, mesh->kappa, sizeof(double) * ctx->L, cudaMemcpyHostToDevice, s));
+        if (dm.H)
+            CU(cudaMemcpyAsync(const_cast<double *>(dm.H), mesh->alpha, sizeof(double) * ctx->L,
+                               cudaMemcpyHostToDevice, s));
+        LAUNCH(launch_geom(dm, xyz_d, kappa_d, const_cast<double *>(dm.G), const_cast<double *>(dm.BM),
+                           const_cast<double *>(dm.H), bad_d, s));
         int bad = 0;
         CU(cudaMemcpyAsync(&bad, bad_d, sizeof(int), cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
@@ -670,7 +694,7 @@ extern "C" int sem_ax(sem_ctx *ctx, const double *u, double *w) {
     CHECK_CTX();
     if (!u || !w || !aligned8(u) || !aligned8(w)) return fail(ctx, SEM_EINVAL, "sem_ax: bad pointer");
     if (u == w) return fail(ctx, SEM_EINVAL, "sem_ax: u and w must not alias");
-    LAUNCHP(kProfAx, 64.0 * ctx->L, -1, launch_ax(ctx->dm, u, w, ctx->stream));
+    LAUNCHP(kProfAx, (ctx->dm.H ? 72.0 : 64.0) * ctx->L, -1, launch_ax(ctx->dm, u, w, ctx->stream));
     return SEM_OK;
 }
 
@@ -745,7 +769,8 @@ static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
     CgVecs &v = ctx->cv;
     const int P = ctx->nranks;
     int rc;
-    const double k1_bpn = k == 0 ? 72.0 : 96.0;    // K1 algorithmic bytes per local node
+    // K1 algorithmic bytes per local node (+8: the mass diagonal, screened operator)
+    const double k1_bpn = (k == 0 ? 72.0 : 96.0) + (ctx->dm.H ? 8.0 : 0.0);
     if (k1_split(ctx->dm)) {
         // boundary elements first; the exchange of their w runs on the side
         // stream while the interior elements' K1 runs here

@@ -46,6 +46,8 @@ struct DevMesh {
     const double *D;            // [n][n] row-major, D[i*n+m] = phi'_m(xi_i)
     const double *G;            // [E][6][n3] rr rs rt ss st tt (w J folded in)
     const double *BM;           // [L] lumped mass w_i w_j w_k J
+    const double *H;            // [L] alpha w_i w_j w_k J (screened-Coulomb mass term) or
+                                // nullptr (Poisson); kappa is folded into G
     // gather-scatter plan over element-SURFACE nodes: groups of local copies of
     // one global id, Dirichlet groups first ([0, ndir)), copies in ascending
     // local order, stored by class (see GsClasses).
@@ -78,8 +80,10 @@ constexpr int kMaxPartials = 1024;     // per-block partial slots of K1 / K2 (<=
 
 // ---- launchers (sem_kernels.cu); all return cudaGetLastError() ----
 int ax_blocks(int N, int64_t E);      // grid size of the Ax kernels for E elements
-cudaError_t launch_geom(const DevMesh &m, const double *xyz, double *G, double *BM,
-                        int *bad, cudaStream_t s);
+// kappa: [L] or nullptr (G *= kappa); H: [L] holding alpha on entry (-> alpha w J)
+// or nullptr
+cudaError_t launch_geom(const DevMesh &m, const double *xyz, const double *kappa, double *G,
+                        double *BM, double *H, int *bad, cudaStream_t s);
 cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t s);
 // The CG kernels take the iteration k from CgState (device), so one captured
 // CUDA graph of a chunk of iterations is valid for every chunk.
@@ -111,14 +115,14 @@ cudaError_t launch_cg_red_rr(const DevMesh &m, const CgVecs &v, cudaStream_t s);
 // ax_tma.cu
 bool tma_supported(int N);
 int tma_blocks(int N, int64_t E, int nsm, bool cg);
-cudaError_t tma_prepare(int N);
+cudaError_t tma_prepare(int N, bool mass);
 cudaError_t upload_const_D(int N, const double *D_host);
 cudaError_t launch_ax_tma(const DevMesh &m, const double *u, double *w, cudaStream_t s);
 cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne,
                              int pidx0, cudaStream_t s);
 bool hi_supported(int N);
 int hi_blocks(int N, int64_t E, int nsm, bool cg);
-cudaError_t hi_prepare(int N);
+cudaError_t hi_prepare(int N, bool mass);
 cudaError_t launch_ax_hi(const DevMesh &m, const double *u, double *w, cudaStream_t s);
 cudaError_t launch_ax_cg_hi(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne,
                             int pidx0, cudaStream_t s);

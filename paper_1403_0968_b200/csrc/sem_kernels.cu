@@ -31,7 +31,8 @@ __device__ __forceinline__ double sum_ranks(const double *a, int nranks) {
 // --------------------------------------------------------------------------
 __global__ void geom_kernel(int n, int64_t E, const double *__restrict__ D,
                             const double *__restrict__ wq, const double *__restrict__ xyz,
-                            double *__restrict__ G, double *__restrict__ BM, int *bad,
+                            const double *__restrict__ kappa, double *__restrict__ G,
+                            double *__restrict__ BM, double *__restrict__ H, int *bad,
                             bool slice_major) {
     const int n3 = n * n * n;
     const int64_t L = E * n3;
@@ -75,6 +76,13 @@ __global__ void geom_kernel(int n, int64_t E, const double *__restrict__ D,
         for (int f = 0; f < 6; ++f)
             g[f] = s * (C[0][pd[f]] * C[0][pe[f]] + C[1][pd[f]] * C[1][pe[f]] +
                         C[2][pd[f]] * C[2][pe[f]]);
+        // screened Coulomb (NEXT-1): kappa weights the flux at the node
+        // (reading G2), the mass term is alpha w J (lumped)
+        if (kappa) {
+            const double kq = kappa[l];
+            for (int f = 0; f < 6; ++f) g[f] *= kq;
+        }
+        if (H) H[l] = H[l] * wJ;
         if (slice_major) {      // [E][n][6][n^2]: one contiguous block per k-slice
             double *Ge = G + e * 6 * n3 + (int64_t)k * 6 * n * n + (i + n * j);
             for (int f = 0; f < 6; ++f) Ge[f * n * n] = g[f];
@@ -451,12 +459,12 @@ static int grid_for(int64_t L, int threads) {
     return (int)(b < 1 ? 1 : b);
 }
 
-cudaError_t launch_geom(const DevMesh &m, const double *xyz, double *G, double *BM,
-                        int *bad, cudaStream_t s) {
+cudaError_t launch_geom(const DevMesh &m, const double *xyz, const double *kappa, double *G,
+                        double *BM, double *H, int *bad, cudaStream_t s) {
     // D and the 1-D weights live at the start of the D buffer: [n*n] D, [n] w
     // the high-order kernel streams G^ by k-slices: slice-major layout
-    geom_kernel<<<grid_for(m.L, 256), 256, 0, s>>>(m.n, m.E, m.D, m.D + m.n * m.n, xyz, G, BM,
-                                                   bad, m.use_hi);
+    geom_kernel<<<grid_for(m.L, 256), 256, 0, s>>>(m.n, m.E, m.D, m.D + m.n * m.n, xyz, kappa, G,
+                                                   BM, H, bad, m.use_hi);
     return cudaGetLastError();
 }
 
@@ -464,6 +472,7 @@ cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t
     if (m.E == 0) return cudaSuccess;
     if (m.use_hi) return launch_ax_hi(m, u, w, s);
     if (m.use_tma) return launch_ax_tma(m, u, w, s);
+    if (m.H) return cudaErrorInvalidValue;      // the simple kernel has no mass term
     AxCgArgs none{};
     SEM_DISPATCH_N(m.N, (ax_kernel<NN, false><<<ax_grid(m.N, m.E, m.nsm), AxCfg<NN>::NT, 0, s>>>(
                              m.E, m.D, m.G, u, w, none)));
@@ -473,6 +482,7 @@ cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t
 cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
     if (m.use_hi) return launch_ax_cg_hi(m, v, 0, m.E, 0, s);
     if (m.use_tma) return launch_ax_cg_tma(m, v, 0, m.E, 0, s);
+    if (m.H) return cudaErrorInvalidValue;
     AxCgArgs a{v.r, v.p, v.xw, make_red(m, v), v.part1, v.st};
     cudaError_t e = cudaSuccess;
     SEM_DISPATCH_N(m.N, (e = launch_pdl(ax_kernel<NN, true>, ax_grid(m.N, m.E, m.nsm), AxCfg<NN>::NT,

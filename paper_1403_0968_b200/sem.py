@@ -35,6 +35,8 @@ class SemMesh(ctypes.Structure):
         ("allgather", ALLGATHER_FN),
         ("allgather_user", ctypes.c_void_p),
         ("device", ctypes.c_int32),
+        ("kappa", ctypes.c_void_p),
+        ("alpha", ctypes.c_void_p),
     ]
 
 
@@ -125,9 +127,12 @@ def _dptr(t, n, name):
 class Context:
     """sem_setup() on one rank.  ``mesh`` is a meshgen.Mesh (or any object with
     xyz [E,3,n^3] f64, glo [E,n^3] i64, dirichlet [E,n^3] u8 and optional
-    nboundary).  ``group``: torch.distributed process group for nranks > 1."""
+    nboundary).  ``group``: torch.distributed process group for nranks > 1.
+    ``kappa`` / ``alpha``: per-local-node screened-Coulomb coefficients
+    (host arrays, [E*n^3]; None = Poisson), see include/sem.h."""
 
-    def __init__(self, mesh, N: int | None = None, device: int | None = None, group=None):
+    def __init__(self, mesh, N: int | None = None, device: int | None = None, group=None,
+                 kappa=None, alpha=None):
         import torch
         L = lib()
         self.N = int(mesh.N if N is None else N)
@@ -145,6 +150,13 @@ class Context:
         m.dirichlet = self._dir.ctypes.data
         m.nboundary = int(getattr(mesh, "nboundary", 0) or 0)
         m.device = self.device
+        self._kappa = None if kappa is None else np.ascontiguousarray(kappa, dtype=np.float64).reshape(-1)
+        self._alpha = None if alpha is None else np.ascontiguousarray(alpha, dtype=np.float64).reshape(-1)
+        for name, a in (("kappa", self._kappa), ("alpha", self._alpha)):
+            if a is not None and a.size != self._glo.size:
+                raise ValueError(f"{name} must hold {self._glo.size} values, got {a.size}")
+        m.kappa = None if self._kappa is None else self._kappa.ctypes.data
+        m.alpha = None if self._alpha is None else self._alpha.ctypes.data
         self._group = group
         self._keep = []
         if group is not None and torch.distributed.get_world_size(group) > 1:

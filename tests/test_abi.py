@@ -86,14 +86,25 @@ def test_workspace_bytes_and_validation(L):
     Lloc = m.nlocal
     # G (6L) + B (L) + r, p, w, xw (4L) doubles dominate
     assert 88 * Lloc <= nb.value <= 110 * Lloc
+    # the screened operator's mass diagonal adds one L-vector
+    alpha = np.ones(m.nlocal)
+    s.alpha = alpha.ctypes.data
+    nb2 = ctypes.c_size_t(0)
+    assert L.sem_workspace_bytes(ctypes.byref(s), N, ctypes.byref(nb2)) == 0
+    assert 8 * Lloc <= nb2.value - nb.value <= 8 * Lloc + 256
+    s.alpha = None
     assert L.sem_workspace_bytes(ctypes.byref(s), 0, ctypes.byref(nb)) == sem.SEM_EINVAL
     assert L.sem_workspace_bytes(ctypes.byref(s), 16, ctypes.byref(nb)) == sem.SEM_EINVAL
     s.nelem = 0
     assert L.sem_workspace_bytes(ctypes.byref(s), N, ctypes.byref(nb)) == sem.SEM_EINVAL
 
 
-def _setup_rc(L, m, N):
+def _setup_rc(L, m, N, kappa=None, alpha=None):
     s = _mesh_struct(m)
+    if kappa is not None:
+        s.kappa = kappa.ctypes.data
+    if alpha is not None:
+        s.alpha = alpha.ctypes.data
     ws = ctypes.create_string_buffer(1024)  # never reached: validation fails first
     ctx = ctypes.c_void_p()
     nb = ctypes.c_size_t(0)
@@ -127,6 +138,12 @@ def test_setup_rejects_malformed_meshes(L):
     bad3.glo[0, 0] = -5
     rc, msg = _setup_rc(L, bad3, N)
     assert rc == sem.SEM_EINVAL
+    # screened-Coulomb coefficients: kappa > 0, alpha >= 0, finite
+    kappa, alpha = meshgen.coefficients(m)
+    for kap, alp, what in ((kappa * 0.0, alpha, "kappa"), (kappa, -alpha, "alpha"),
+                           (kappa * np.inf, alpha, "kappa"), (kappa, alpha * np.nan, "alpha")):
+        rc, msg = _setup_rc(L, m, N, kap, alp)
+        assert rc == sem.SEM_EINVAL and what in msg, (what, msg)
     # misaligned workspace
     s = _mesh_struct(m)
     ctx = ctypes.c_void_p()
