@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--maxit", type=int, default=5000)
     ap.add_argument("--ax-reps", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--operator", choices=["poisson", "screened"], default="poisson",
+                    help="screened: -div(kappa grad u) + alpha u (NEXT-1) with meshgen.coefficients")
     ap.add_argument("--cpu-its", type=int, default=100,
                     help="oracle CG iterations timed for cpu_baseline (bounded sample)")
     ap.add_argument("--ref-its", type=int, default=3,
@@ -153,8 +155,15 @@ def rank_mesh(args, rank, world, r1d):
 
 def workload_name(args, world):
     E = args.elems[0] * args.elems[1] * args.elems[2]
+    op = ("" if args.operator == "poisson" else
+          ", screened Coulomb -div(kappa grad u) + alpha u (meshgen.coefficients)")
     return (f"c3/c5: {E} hex elements ({'x'.join(map(str, args.elems))}) of order N={args.N} "
-            f"per GPU, eps={args.eps} deformed box, full CG to {args.tol:g} from x0=0")
+            f"per GPU, eps={args.eps} deformed box, full CG to {args.tol:g} from x0=0{op}")
+
+
+def coefficients(args, m):
+    from paper_1403_0968_b200 import meshgen
+    return meshgen.coefficients(m) if args.operator == "screened" else (None, None)
 
 
 def oracle_sample(args, its_per_call, calls):
@@ -167,10 +176,12 @@ def oracle_sample(args, its_per_call, calls):
     G, J = oracle.geom(args.N, m.xyz)
     _, f = meshgen.manufactured(m)
     b = oracle.mass_rhs(args.N, m.glo, m.dirichlet, J, f)
+    kappa, alpha = coefficients(args, m)
+    co = {} if kappa is None else {"J": J, "kappa": kappa, "alpha": alpha}
     times = []
     for _ in range(calls):
         t0 = time.perf_counter()
-        oracle.cg(args.N, m.glo, m.dirichlet, G, b, tol=0.0, maxit=its_per_call)
+        oracle.cg(args.N, m.glo, m.dirichlet, G, b, tol=0.0, maxit=its_per_call, **co)
         times.append(time.perf_counter() - t0)
     return times, m.nlocal
 
@@ -231,8 +242,13 @@ def main():
 
     xi, _ = sem.gll(args.N)
     m, parts = rank_mesh(args, rank, world, xi)
-    ctx = sem.Context(m, args.N, device=local_rank, group=group)
+    kappa, alpha = coefficients(args, m)
+    ctx = sem.Context(m, args.N, device=local_rank, group=group, kappa=kappa, alpha=alpha)
     L = ctx.nlocal
+    # algorithmic bytes per local node: K1 96, Ax 64; the screened
+    # operator's mass diagonal adds 8 to both
+    bpn_k1 = 96.0 + (8.0 if alpha is not None else 0.0)
+    bpn_ax = 64.0 + (8.0 if alpha is not None else 0.0)
     L_all = L * world
     _, f = meshgen.manufactured(m)
     b = ctx.rhs(torch.from_numpy(f).to(dev))
@@ -294,7 +310,7 @@ def main():
     peak, peak_src = peaks()
     k2_bytes = prof["k2"][2] / prof["k2"][1] if prof["k2"][1] else None
     kern = {}
-    for name, by in (("k1", 96.0 * L), ("k2", k2_bytes), ("ax", 64.0 * L)):
+    for name, by in (("k1", bpn_k1 * L), ("k2", k2_bytes), ("ax", bpn_ax * L)):
         if world > 1 or by is None:
             continue
         reps = 50
@@ -337,12 +353,12 @@ def main():
     ax_kernel_ms = pa[0] / pa[1]
     ax = {"gdof_s": L_all / (ax_ms / 1e3) / 1e9, "ms_per_apply": ax_ms,
           "kernel_ms": ax_kernel_ms,
-          "achieved_gbs": 64.0 * L / (ax_kernel_ms / 1e3) / 1e9,
-          "frac": 64.0 * L / (ax_kernel_ms / 1e3) / 1e9 / peak,
+          "achieved_gbs": bpn_ax * L / (ax_kernel_ms / 1e3) / 1e9,
+          "frac": bpn_ax * L / (ax_kernel_ms / 1e3) / 1e9 / peak,
           "gflops": (12 * (args.N + 1) ** 4 + 15 * (args.N + 1) ** 3) * (L / (args.N + 1) ** 3)
           / (ax_kernel_ms / 1e3) / 1e9,
-          "bytes_per_apply": 64 * L,
-          "l2_note": "working set 64 B/node; at c3 (134 MB) partly L2-resident"}
+          "bytes_per_apply": bpn_ax * L,
+          "l2_note": f"working set {bpn_ax:.0f} B/node; at c3 partly L2-resident"}
 
     # ---- end to end through the public API with host buffers ----
     b_host = b.cpu().pin_memory()
@@ -392,7 +408,7 @@ def main():
             "config": {"workload": workload_name(args, world), "N": args.N,
                        "elements_per_gpu": m.nelem, "local_dof_per_gpu": L,
                        "unique_dof_total": ctx.nglobal, "cg_iters": its, "tol": args.tol,
-                       "partition": "x".join(map(str, parts)),
+                       "partition": "x".join(map(str, parts)), "operator": args.operator,
                        "parallelism": f"element partition over {world} GPU(s)",
                        "l2": f"inputs larger than L2: {ws / 2**20:.0f} MiB resident working set "
                              f"> {L2_BYTES / 2**20:.0f} MiB L2, streamed every iteration"},
@@ -402,14 +418,15 @@ def main():
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
                          "peak_source": peak_src,
-                         "bytes_per_node": "96 (x,r,p,G read; x,p,w write), 72 at k=0",
+                         "bytes_per_node": f"{bpn_k1:.0f} (x,r,p,G{',H' if alpha is not None else ''} "
+                                           "read; x,p,w write)",
                          "avg_launch_us": k1_in_solve_us,
                          "launches": k1_n,
                          "kernels_replayed": kern,
                          "step_share": shares,
                          "iteration": {"us": 1e3 * ms / args.steps / its,
-                                       "algorithmic_bytes": 96.0 * L + (k2_bytes or 0.0),
-                                       "frac": (96.0 * L + (k2_bytes or 0.0)) /
+                                       "algorithmic_bytes": bpn_k1 * L + (k2_bytes or 0.0),
+                                       "frac": (bpn_k1 * L + (k2_bytes or 0.0)) /
                                                (ms / args.steps / its * 1e-3) / 1e9 / peak},
                          "timing": "achieved: CUDA events around every K1 launch on the library "
                                    f"stream over {prof_steps} solves of the same workload run right "
