@@ -64,9 +64,10 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
-    --set full summary (profiles/ncu_summary_*.json), or None."""
+def ncu_traffic(kernels=("ax_tma_kernel<7, true, false>", "ax_tma_kernel<7, 1>")):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of
+    the dominant kernel from the newest committed ncu --set full summary
+    (profiles/ncu_summary_*.json) that captured THAT kernel, or None."""
     d = os.path.join(ROOT, "profiles")
     if not os.path.isdir(d):
         return None
@@ -76,8 +77,9 @@ def ncu_traffic():
             s = json.load(open(os.path.join(d, f)))
         except Exception:
             continue
-        if "dominant" in s:
-            return s["dominant"].get("dram_bytes_per_launch")
+        dom = s.get("dominant") or {}
+        if any(k in dom.get("kernel", "") for k in kernels):
+            return dom.get("dram_bytes_per_launch")
     return None
 
 
@@ -328,7 +330,8 @@ def main():
     k1_ms, k1_n, k1_bytes = prof["k1"]
     achieved = (k1_bytes / k1_n) / (k1_ms / k1_n * 1e-3) / 1e9 if k1_n else None
     k1_in_solve_us = 1e3 * k1_ms / k1_n if k1_n else None
-    traffic = ncu_traffic()
+    traffic = ncu_traffic((f"ax_tma_kernel<{args.N}, true, false>", f"ax_tma_kernel<{args.N}, 1>")) \
+        if alpha is None else None
     shares = {k: v[0] / prof_ms for k, v in prof.items() if v[1]}
     # the work vectors were clobbered by the replays; the next solve re-inits
     x.zero_()

@@ -51,8 +51,12 @@ def lib():
         L.ora_ax_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P, P]
         L.ora_cg_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P, P, P, P,
                                       ctypes.c_double, ctypes.c_int, P, P]
+        L.ora_diag_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P]
+        L.ora_pcg_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P, P, ctypes.c_int, P, P,
+                                       ctypes.c_double, ctypes.c_int, P, P]
         for f in (L.ora_gll, L.ora_deriv, L.ora_geom, L.ora_ax, L.ora_dssum,
-                  L.ora_multiplicity, L.ora_cg, L.ora_ax_screened, L.ora_cg_screened):
+                  L.ora_multiplicity, L.ora_cg, L.ora_ax_screened, L.ora_cg_screened,
+                  L.ora_diag_screened, L.ora_pcg_screened):
             f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -149,11 +153,29 @@ def multiplicity(glo: np.ndarray) -> np.ndarray:
     return m
 
 
+PRECOND = {"none": 0, "jacobi": 1}
+
+
+def diag(N: int, G: np.ndarray, J=None, kappa=None, alpha=None) -> np.ndarray:
+    """NEXT-2: local diagonal d_L = diag(A^e) of the (screened) operator, the
+    input of the Jacobi preconditioner (PCG); unassembled."""
+    n3 = (N + 1) ** 3
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    E = G.size // (6 * n3)
+    J, kappa, alpha = (_opt(a, E * n3) for a in (J, kappa, alpha))
+    d = np.zeros(E * n3)
+    _check(lib().ora_diag_screened(N, E, _p(G), _po(J), _po(kappa), _po(alpha), _p(d)),
+           "ora_diag_screened")
+    return d
+
+
 def cg(N: int, glo, dirichlet, G, b, x0=None, tol=1e-8, maxit=1000, J=None, kappa=None,
-       alpha=None):
+       alpha=None, precond: str = "none"):
     """O7: CG (PCG of PAPER.md:672-673, identity preconditioner).
     Returns (x, iters, rel_res, status) with status 0 = converged, 4 = maxit.
-    kappa / alpha (+ J): the screened-Coulomb operator of ax() (NEXT-1)."""
+    kappa / alpha (+ J): the screened-Coulomb operator of ax() (NEXT-1).
+    precond="jacobi": the Jacobi-preconditioned recurrence (NEXT-2,
+    ora_pcg_screened); the stopping rule stays on (r,r)_c."""
     n3 = (N + 1) ** 3
     glo = np.ascontiguousarray(glo, dtype=np.int64).reshape(-1)
     dirichlet = np.ascontiguousarray(dirichlet, dtype=np.uint8).reshape(-1)
@@ -163,14 +185,15 @@ def cg(N: int, glo, dirichlet, G, b, x0=None, tol=1e-8, maxit=1000, J=None, kapp
     x = np.zeros(E * n3) if x0 is None else np.array(x0, dtype=np.float64).reshape(-1).copy()
     iters = ctypes.c_int(0)
     rel = ctypes.c_double(0.0)
-    if J is None and kappa is None and alpha is None:
+    pc = PRECOND[precond]
+    if J is None and kappa is None and alpha is None and pc == 0:
         rc = lib().ora_cg(N, E, _p(glo), _p(dirichlet), _p(G), _p(b), _p(x), float(tol),
                           int(maxit), ctypes.byref(iters), ctypes.byref(rel))
     else:
         J, kappa, alpha = (_opt(a, E * n3) for a in (J, kappa, alpha))
-        rc = lib().ora_cg_screened(N, E, _p(glo), _p(dirichlet), _p(G), _po(J), _po(kappa),
-                                   _po(alpha), _p(b), _p(x), float(tol), int(maxit),
-                                   ctypes.byref(iters), ctypes.byref(rel))
+        rc = lib().ora_pcg_screened(N, E, _p(glo), _p(dirichlet), _p(G), _po(J), _po(kappa),
+                                    _po(alpha), pc, _p(b), _p(x), float(tol), int(maxit),
+                                    ctypes.byref(iters), ctypes.byref(rel))
     if rc not in (0, 4):
         raise OracleError(f"ora_cg failed with status {rc}")
     return x, iters.value, rel.value, rc

@@ -262,6 +262,62 @@ int ora_ax(int N, int64_t E, const double *G, const double *u, double *w)
 }
 
 /* ------------------------------------------------------------------------- */
+/* NEXT-2.  Diagonal of the local operator, d[q] = (A^e)_qq
+ * = e_q^T A^e e_q, for the Jacobi preconditioner of the PCG at PAPER.md:672-673
+ * ("Besides the preconditioner choice").  Written from the definition of A^e
+ * (eq:semOperator :593-596, reading G4, kappa / alpha as ora_ax_screened):
+ * the reference gradient of the unit vector e_q, q = (i,j,k), at node p = (a,b,c)
+ *     g_r(p) = sum_m D_am e_q[m,b,c] = D_ai  if (b,c) == (j,k), else 0
+ *     g_s(p) = sum_m D_bm e_q[a,m,c] = D_bj  if (a,c) == (i,k), else 0
+ *     g_t(p) = sum_m D_cm e_q[a,b,m] = D_ck  if (a,b) == (i,j), else 0
+ * and (A^e)_qq = sum_p kappa_p g(p)^T G^(p) g(p) + alpha_q w_i w_j w_k J_q.
+ * Nodes p off the three GLL lines through q have g(p) = 0 and are skipped.  */
+int ora_diag_screened(int N, int64_t E, const double *G, const double *J, const double *kappa,
+                      const double *alpha, double *d)
+{
+    if (N < 1 || N > 32 || E < 0 || (E > 0 && (!G || !d))) return ORA_EINVAL;
+    if (E > 0 && alpha && !J) return ORA_EINVAL;
+    int n = N + 1, n3 = n * n * n;
+    double xi[33], wq[33];
+    double *D = (double *)malloc(sizeof(double) * n * n);
+    ora_gll(N, xi, wq);
+    ora_deriv(N, xi, D);
+    for (int64_t e = 0; e < E; ++e) {
+        const double *Ge = G + e * 6 * n3;
+        for (int k = 0; k < n; ++k)
+            for (int j = 0; j < n; ++j)
+                for (int i = 0; i < n; ++i) {
+                    double s = 0.0;
+                    for (int c = 0; c < n; ++c)
+                        for (int b = 0; b < n; ++b)
+                            for (int a = 0; a < n; ++a) {
+                                int onr = (b == j && c == k), ons = (a == i && c == k);
+                                int ont = (a == i && b == j);
+                                if (!onr && !ons && !ont) continue;
+                                double gr = onr ? D[a * n + i] : 0.0;
+                                double gs = ons ? D[b * n + j] : 0.0;
+                                double gt = ont ? D[c * n + k] : 0.0;
+                                int p = a + n * b + n * n * c;
+                                double grr = Ge[0 * n3 + p], grs = Ge[1 * n3 + p];
+                                double grt = Ge[2 * n3 + p], gss = Ge[3 * n3 + p];
+                                double gst = Ge[4 * n3 + p], gtt = Ge[5 * n3 + p];
+                                double fr = grr * gr + grs * gs + grt * gt;
+                                double fs = grs * gr + gss * gs + gst * gt;
+                                double ft = grt * gr + gst * gs + gtt * gt;
+                                double t = gr * fr + gs * fs + gt * ft;
+                                if (kappa) t = kappa[e * n3 + p] * t;
+                                s += t;
+                            }
+                    int q = i + n * j + n * n * k;
+                    if (alpha) s += alpha[e * n3 + q] * (wq[i] * wq[j] * wq[k] * J[e * n3 + q]);
+                    d[e * n3 + q] = s;
+                }
+    }
+    free(D);
+    return ORA_OK;
+}
+
+/* ------------------------------------------------------------------------- */
 /* O5.  Direct-stiffness summation v <- Q Q^T v (global-local numbering,
  * PAPER.md:667, Fischer 1991).  For each global id g, S_g = sum of its local
  * copies in ascending local-index order; S_g is written to every copy.       */
@@ -345,20 +401,36 @@ static void apply_op(int N, int64_t E, const double *G, const ora_coef *cf, cons
     for (int64_t l = 0; l < L; ++l) out[l] = mask[l] * out[l];
 }
 
-/* CG on the screened-Coulomb operator (NEXT-1; same recurrence as O7, the
- * operator is ora_ax_screened's).  ora_cg is the Poisson case. */
-int ora_cg_screened(int N, int64_t E, const int64_t *glo, const uint8_t *dirichlet,
-                    const double *G, const double *J, const double *kappa, const double *alpha,
-                    const double *b, double *x, double tol, int maxit, int *iters,
-                    double *rel_res)
+/* PCG on the screened-Coulomb operator: O7's recurrence with a
+ * preconditioner M^{-1} ("PCG ... Besides the preconditioner
+ * choice"; NEXT-2 of SURVEY.md §8(f)), preconditioned Hestenes-Stiefel:
+ *   r = mask (b - Q Q^T A_L x0); z = M^{-1} r; rho = (r,z)_c; rr = (r,r)_c
+ *   rr0 = rr; k = 0
+ *   while k < maxit and sqrt(rr) > tol sqrt(rr0):            (reading G9, R4)
+ *     beta = (k == 0) ? 0 : rho / rho_old;  p = z + beta p
+ *     w = mask Q Q^T A_L p;  alpha = rho / (w,p)_c
+ *     x += alpha p;  r -= alpha w;  z = M^{-1} r
+ *     rho_old = rho;  rho = (r,z)_c;  rr = (r,r)_c;  k += 1
+ * precond 0: M = I (z = r, rho = rr: exactly O7).
+ * precond 1: Jacobi, M = diag of the assembled masked operator:
+ *   M^{-1}_L = mask_L / (Q Q^T d)_L with d the local diagonal (ora_diag_screened)
+ *   (0 at Dirichlet nodes, where r = 0 anyway).
+ * The stopping rule stays on the residual norm (r,r)_c (reading R4).       */
+int ora_pcg_screened(int N, int64_t E, const int64_t *glo, const uint8_t *dirichlet,
+                     const double *G, const double *J, const double *kappa, const double *alpha,
+                     int precond, const double *b, double *x, double tol, int maxit, int *iters,
+                     double *rel_res)
 {
     if (N < 1 || N > 32 || E < 0 || maxit < 0 || !(tol >= 0.0)) return ORA_EINVAL;
     if (alpha && !J) return ORA_EINVAL;
+    if (precond != 0 && precond != 1) return ORA_EINVAL;
     const ora_coef cf = {J, kappa, alpha};
     int64_t L = E * (N + 1) * (N + 1) * (N + 1);
     double *mask = (double *)malloc(sizeof(double) * (L + 1));
     double *c = (double *)malloc(sizeof(double) * (L + 1));
+    double *minv = (double *)malloc(sizeof(double) * (L + 1));
     double *r = (double *)malloc(sizeof(double) * (L + 1));
+    double *z = (double *)malloc(sizeof(double) * (L + 1));
     double *p = (double *)malloc(sizeof(double) * (L + 1));
     double *w = (double *)malloc(sizeof(double) * (L + 1));
     int64_t *order = sorted_order(L, glo);
@@ -368,39 +440,61 @@ int ora_cg_screened(int N, int64_t E, const int64_t *glo, const uint8_t *dirichl
     }
     dssum_sorted(L, glo, order, c);             /* c = multiplicity m */
     for (int64_t l = 0; l < L; ++l) c[l] = mask[l] / c[l];
+    if (precond == 1) {
+        ora_diag_screened(N, E, G, J, kappa, alpha, minv);   /* local diagonal d */
+        dssum_sorted(L, glo, order, minv);                   /* Q Q^T d */
+        for (int64_t l = 0; l < L; ++l) minv[l] = dirichlet[l] ? 0.0 : 1.0 / minv[l];
+    }
 
     apply_op(N, E, G, &cf, glo, order, mask, x, w);  /* w = mask QQ^T A_L x0 */
     for (int64_t l = 0; l < L; ++l) r[l] = mask[l] * b[l] - w[l];
+    for (int64_t l = 0; l < L; ++l) z[l] = (precond == 1) ? minv[l] * r[l] : r[l];
     for (int64_t l = 0; l < L; ++l) p[l] = 0.0;
-    double rho = dot_c(L, c, r, r), rho0 = rho, rho_old = 0.0;
+    double rr = dot_c(L, c, r, r), rr0 = rr;
+    double rho = dot_c(L, c, r, z), rho_old = 0.0;
     int k = 0;
     int status = ORA_OK;
-    if (rho0 == 0.0) {
+    if (rr0 == 0.0) {
         *iters = 0;
         *rel_res = 0.0;
     } else {
-        while (k < maxit && sqrt(rho) > tol * sqrt(rho0)) {
+        while (k < maxit && sqrt(rr) > tol * sqrt(rr0)) {
             double beta = (k == 0) ? 0.0 : rho / rho_old;
-            for (int64_t l = 0; l < L; ++l) p[l] = r[l] + beta * p[l];
+            for (int64_t l = 0; l < L; ++l) p[l] = z[l] + beta * p[l];
             apply_op(N, E, G, &cf, glo, order, mask, p, w);
-            double alpha = rho / dot_c(L, c, w, p);
-            for (int64_t l = 0; l < L; ++l) x[l] += alpha * p[l];
-            for (int64_t l = 0; l < L; ++l) r[l] -= alpha * w[l];
+            double alpha_k = rho / dot_c(L, c, w, p);
+            for (int64_t l = 0; l < L; ++l) x[l] += alpha_k * p[l];
+            for (int64_t l = 0; l < L; ++l) r[l] -= alpha_k * w[l];
+            for (int64_t l = 0; l < L; ++l) z[l] = (precond == 1) ? minv[l] * r[l] : r[l];
             rho_old = rho;
-            rho = dot_c(L, c, r, r);
+            rho = dot_c(L, c, r, z);
+            rr = dot_c(L, c, r, r);
             k += 1;
         }
         *iters = k;
-        *rel_res = sqrt(rho) / sqrt(rho0);
-        if (tol > 0.0 && sqrt(rho) > tol * sqrt(rho0)) status = ORA_ENOCONV;
+        *rel_res = sqrt(rr) / sqrt(rr0);
+        if (tol > 0.0 && sqrt(rr) > tol * sqrt(rr0)) status = ORA_ENOCONV;
     }
     free(mask);
     free(c);
+    free(minv);
     free(r);
+    free(z);
     free(p);
     free(w);
     free(order);
     return status;
+}
+
+/* CG on the screened-Coulomb operator (NEXT-1): O7, the identity-preconditioned
+ * case of ora_pcg_screened.  ora_cg is the Poisson case. */
+int ora_cg_screened(int N, int64_t E, const int64_t *glo, const uint8_t *dirichlet,
+                    const double *G, const double *J, const double *kappa, const double *alpha,
+                    const double *b, double *x, double tol, int maxit, int *iters,
+                    double *rel_res)
+{
+    return ora_pcg_screened(N, E, glo, dirichlet, G, J, kappa, alpha, 0, b, x, tol, maxit,
+                            iters, rel_res);
 }
 
 int ora_cg(int N, int64_t E, const int64_t *glo, const uint8_t *dirichlet,

@@ -119,3 +119,31 @@ def dense_cg(K, b, tol, maxit):
         rho = r @ r
         k += 1
     return x, k
+
+
+def dense_pcg(K, b, minv, tol, maxit):
+    """Textbook preconditioned CG on a dense SPD matrix with a diagonal
+    preconditioner minv (vector); stopping rule on the residual norm r.r
+    (same as the oracle's reading R4)."""
+    x = np.zeros_like(b)
+    r = b.copy()
+    z = minv * r
+    rho = r @ z
+    rr0 = r @ r
+    rr = rr0
+    p = np.zeros_like(b)
+    k = 0
+    rho_old = 0.0
+    while k < maxit and np.sqrt(rr) > tol * np.sqrt(rr0):
+        beta = 0.0 if k == 0 else rho / rho_old
+        p = z + beta * p
+        q = K @ p
+        alpha = rho / (q @ p)
+        x = x + alpha * p
+        r = r - alpha * q
+        z = minv * r
+        rho_old = rho
+        rho = r @ z
+        rr = r @ r
+        k += 1
+    return x, k
