@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--operator", choices=["poisson", "screened"], default="poisson",
                     help="screened: -div(kappa grad u) + alpha u (NEXT-1) with meshgen.coefficients")
+    ap.add_argument("--precond", choices=["none", "jacobi"], default="none",
+                    help="jacobi: Jacobi-preconditioned CG (NEXT-2, sem_pcg)")
     ap.add_argument("--cpu-its", type=int, default=100,
                     help="oracle CG iterations timed for cpu_baseline (bounded sample)")
     ap.add_argument("--ref-its", type=int, default=3,
@@ -159,8 +161,9 @@ def workload_name(args, world):
     E = args.elems[0] * args.elems[1] * args.elems[2]
     op = ("" if args.operator == "poisson" else
           ", screened Coulomb -div(kappa grad u) + alpha u (meshgen.coefficients)")
+    cg = "CG" if args.precond == "none" else "Jacobi PCG"
     return (f"c3/c5: {E} hex elements ({'x'.join(map(str, args.elems))}) of order N={args.N} "
-            f"per GPU, eps={args.eps} deformed box, full CG to {args.tol:g} from x0=0{op}")
+            f"per GPU, eps={args.eps} deformed box, full {cg} to {args.tol:g} from x0=0{op}")
 
 
 def coefficients(args, m):
@@ -183,7 +186,8 @@ def oracle_sample(args, its_per_call, calls):
     times = []
     for _ in range(calls):
         t0 = time.perf_counter()
-        oracle.cg(args.N, m.glo, m.dirichlet, G, b, tol=0.0, maxit=its_per_call, **co)
+        oracle.cg(args.N, m.glo, m.dirichlet, G, b, tol=0.0, maxit=its_per_call,
+                  precond=args.precond, **co)
         times.append(time.perf_counter() - t0)
     return times, m.nlocal
 
@@ -261,7 +265,7 @@ def main():
     its = None
     for _ in range(max(args.warmup, 1)):
         x.zero_()
-        _, its, rel, ok = ctx.cg(b, x, tol=args.tol, maxit=args.maxit)
+        _, its, rel, ok = ctx.cg(b, x, tol=args.tol, maxit=args.maxit, precond=args.precond)
     assert ok, f"CG did not converge: rel_res={rel}"
 
     # ---- timed region: K full CG solves, inputs resident in HBM ----
@@ -276,7 +280,7 @@ def main():
     iters = []
     for _ in range(args.steps):
         x.zero_()
-        _, it, rel, ok = ctx.cg(b, x, tol=args.tol, maxit=args.maxit)
+        _, it, rel, ok = ctx.cg(b, x, tol=args.tol, maxit=args.maxit, precond=args.precond)
         iters.append(it)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -298,7 +302,7 @@ def main():
     p0.record(stream)
     for _ in range(prof_steps):
         x.zero_()
-        ctx.cg(b, x, tol=args.tol, maxit=args.maxit)
+        ctx.cg(b, x, tol=args.tol, maxit=args.maxit, precond=args.precond)
     p1.record(stream)
     torch.cuda.synchronize()
     prof_ms = p0.elapsed_time(p1)
@@ -335,7 +339,7 @@ def main():
     shares = {k: v[0] / prof_ms for k, v in prof.items() if v[1]}
     # the work vectors were clobbered by the replays; the next solve re-inits
     x.zero_()
-    ctx.cg(b, x, tol=args.tol, maxit=args.maxit)
+    ctx.cg(b, x, tol=args.tol, maxit=args.maxit, precond=args.precond)
 
     # ---- Ax alone on the same mesh (64 B/node), for the Ax GDOF/s metric ----
     u = torch.from_numpy(meshgen.random_field(L, 0)).to(dev)
@@ -370,7 +374,7 @@ def main():
     for _ in range(2):
         b_dev.copy_(b_host, non_blocking=True)
         x.zero_()
-        ctx.cg(b_dev, x, tol=args.tol, maxit=args.maxit)
+        ctx.cg(b_dev, x, tol=args.tol, maxit=args.maxit, precond=args.precond)
         x_host.copy_(x, non_blocking=True)
     barrier()
     torch.cuda.synchronize()
@@ -381,7 +385,7 @@ def main():
     for _ in range(e2e_steps):
         b_dev.copy_(b_host, non_blocking=True)
         x.zero_()
-        _, it2, _, _ = ctx.cg(b_dev, x, tol=args.tol, maxit=args.maxit)
+        _, it2, _, _ = ctx.cg(b_dev, x, tol=args.tol, maxit=args.maxit, precond=args.precond)
         x_host.copy_(x, non_blocking=True)
     h1.record(stream)
     torch.cuda.synchronize()
@@ -397,7 +401,7 @@ def main():
         times, Lc = oracle_sample(args, args.cpu_its, 1)
         cpu = {"value": Lc * args.cpu_its / times[0] / 1e9, "unit": "GDOF/s", "cores": 1,
                "kind": "oracle", "cpu": cpu_info(),
-               "sample": f"plain-C oracle CG, {args.cpu_its} iterations (tol=0) on the same c3 "
+               "sample": f"plain-C oracle {'CG' if args.precond == 'none' else 'Jacobi PCG'}, {args.cpu_its} iterations (tol=0) on the same c3 "
                          f"mesh ({Lc} local DOF), 1 thread, {times[0]:.1f} s; setup untimed"}
 
     if rank == 0:
@@ -412,6 +416,7 @@ def main():
                        "elements_per_gpu": m.nelem, "local_dof_per_gpu": L,
                        "unique_dof_total": ctx.nglobal, "cg_iters": its, "tol": args.tol,
                        "partition": "x".join(map(str, parts)), "operator": args.operator,
+                       "precond": args.precond,
                        "parallelism": f"element partition over {world} GPU(s)",
                        "l2": f"inputs larger than L2: {ws / 2**20:.0f} MiB resident working set "
                              f"> {L2_BYTES / 2**20:.0f} MiB L2, streamed every iteration"},

@@ -150,6 +150,30 @@ int sem_mass(sem_ctx *ctx, const double *f, double *b);
 int sem_cg(sem_ctx *ctx, const double *b, double *x, double tol, int maxit,
            int *iters, double *rel_res);
 
+/* Preconditioners of sem_pcg ("PCG ... Besides the
+ * preconditioner choice"). */
+enum sem_precond {
+    SEM_PC_NONE = 0,    /* identity: exactly sem_cg                                    */
+    SEM_PC_JACOBI = 1   /* M = diag of the assembled masked operator, M^-1 = mask / QQ^T d */
+};
+
+/* Preconditioned CG, same contract as sem_cg (b, x, tol, maxit, iters, rel_res,
+ * collective, synchronises the stream), with the preconditioned
+ * Hestenes-Stiefel recurrence (reading R4):
+ *   z = M^-1 r;  rho = (r, z)_c;  p = z + (rho / rho_old) p;  alpha = rho / (p, A p)_c
+ * while the stopping rule stays on the residual norm sqrt((r,r)_c) <= tol
+ * sqrt((r0,r0)_c), so iteration counts compare directly with sem_cg.  The
+ * Jacobi diagonal is formed on the first SEM_PC_JACOBI call (one extra
+ * diag + DSSUM pass) and kept in the workspace.  SEM_EINVAL for an unknown
+ * precond. */
+int sem_pcg(sem_ctx *ctx, int precond, const double *b, double *x, double tol, int maxit,
+            int *iters, double *rel_res);
+
+/* d = Q Q^T diag(A_L): the diagonal of the assembled (unmasked) operator in
+ * local storage, diag(A^e)_q = sum over the three GLL lines through q
+ * (DESIGN.md "Jacobi").  d: DEVICE [nlocal].  Collective.  Asynchronous. */
+int sem_diag(sem_ctx *ctx, double *d);
+
 /* Size of an ncclUniqueId (128) and a fresh one, for rank 0 to broadcast to
  * the other ranks before sem_setup (HOST buffer of sem_nccl_id_bytes()). */
 int sem_nccl_id_bytes(void);

@@ -15,10 +15,19 @@ cudaError_t launch_ax_cg_tma_mass(const DevMesh &m, const CgVecs &v, int64_t eb,
                                   int pidx0, cudaStream_t s);
 cudaError_t launch_ax_cg_hi_mass(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne,
                                  int pidx0, cudaStream_t s);
+// ax_tma_pc.cu (Jacobi PCG K1, both operators)
+cudaError_t upload_const_D_pc(int N, const double *D_host);
+cudaError_t tma_prepare_pc(int N, bool mass);
+cudaError_t hi_prepare_pc(int N, bool mass);
+cudaError_t launch_ax_cg_tma_pc(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne,
+                                int pidx0, cudaStream_t s);
+cudaError_t launch_ax_cg_hi_pc(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne,
+                               int pidx0, cudaStream_t s);
 
 cudaError_t upload_const_D(int N, const double *D_host) {
     cudaError_t e = upload_D_this_tu(N, D_host);
-    return e == cudaSuccess ? upload_const_D_mass(N, D_host) : e;
+    if (e == cudaSuccess) e = upload_const_D_mass(N, D_host);
+    return e == cudaSuccess ? upload_const_D_pc(N, D_host) : e;
 }
 
 bool tma_supported(int N) { return N >= 1 && N <= kTmaMaxN; }
@@ -45,11 +54,13 @@ int hi_blocks(int N, int64_t E, int nsm, bool cg) {
 }
 
 cudaError_t tma_prepare(int N, bool mass) {
-    return mass ? tma_prepare_mass(N) : tma_prepare_t<false>(N);
+    cudaError_t e = mass ? tma_prepare_mass(N) : tma_prepare_t<false>(N);
+    return e == cudaSuccess ? tma_prepare_pc(N, mass) : e;
 }
 
 cudaError_t hi_prepare(int N, bool mass) {
-    return mass ? hi_prepare_mass(N) : hi_prepare_t<false>(N);
+    cudaError_t e = mass ? hi_prepare_mass(N) : hi_prepare_t<false>(N);
+    return e == cudaSuccess ? hi_prepare_pc(N, mass) : e;
 }
 
 cudaError_t launch_ax_tma(const DevMesh &m, const double *u, double *w, cudaStream_t s) {
@@ -62,12 +73,14 @@ cudaError_t launch_ax_hi(const DevMesh &m, const double *u, double *w, cudaStrea
 
 cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne, int pidx0,
                              cudaStream_t s) {
+    if (v.dinv) return launch_ax_cg_tma_pc(m, v, eb, ne, pidx0, s);
     return m.H ? launch_ax_cg_tma_mass(m, v, eb, ne, pidx0, s)
                : launch_ax_cg_tma_t<false>(m, v, eb, ne, pidx0, s);
 }
 
 cudaError_t launch_ax_cg_hi(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne, int pidx0,
                             cudaStream_t s) {
+    if (v.dinv) return launch_ax_cg_hi_pc(m, v, eb, ne, pidx0, s);
     return m.H ? launch_ax_cg_hi_mass(m, v, eb, ne, pidx0, s)
                : launch_ax_cg_hi_t<false>(m, v, eb, ne, pidx0, s);
 }

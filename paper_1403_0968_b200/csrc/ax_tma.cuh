@@ -165,7 +165,9 @@ struct TmaArgs {
     CgState *st;
 };
 
-template <int N, bool CG, bool MASS>
+// PC: Jacobi PCG scalars (cg_k1_prologue_t); a separate instantiation so the
+// CG kernel's code is unchanged (ax_tma_pc.cu)
+template <int N, bool CG, bool MASS, bool PC = false>
 __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs a) {
     using C = TmaCfg<N>;
     using Lo = TmaLayout<N, CG>;
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
     constexpr int DO = d_off(N);
     extern __shared__ __align__(128) double smem[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + size_t(NG) * 2 * STAGE);  // [NG][2]
-    __shared__ double sred[3 * ((Lo::NT + 31) / 32)];
+    __shared__ double sred[3 * ((Lo::NT + 31) / 32)];   // K1 prologue: up to 4 sums
 
     const int tid = threadIdx.x;
     const int g = tid / GT;                 // group
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
     double beta = 0.0, alpha_prev = 0.0;
     int kit = 0;
     if constexpr (CG) {
-        const CgStep c = cg_k1_prologue<Lo::NT>(a.st, a.red, sred);
+        const CgStep c = cg_k1_prologue_t<Lo::NT, PC>(a.st, a.red, sred);
         if (c.done) {
             // drain the copies already in flight, then leave
             if (leader) {
@@ -432,7 +434,7 @@ struct HiCfg {
     static constexpr size_t SMEM = size_t(NG) * PERG * 8 + size_t(NG) * (2 + R) * 8 + 64;
 };
 
-template <int N, bool CG, bool MASS>
+template <int N, bool CG, bool MASS, bool PC = false>
 __global__ void __launch_bounds__(HiCfg<N, CG>::NT, 1) ax_hi_kernel(TmaArgs a) {
     using C = HiCfg<N, CG>;
     constexpr int n = C::n, n2 = C::n2, n3 = C::n3, GT = C::GT, VL = C::VL, NV = C::NV;
@@ -442,7 +444,7 @@ __global__ void __launch_bounds__(HiCfg<N, CG>::NT, 1) ax_hi_kernel(TmaArgs a) {
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + size_t(NG) * PERG);   // [NG][2 + R]
     constexpr int DS = n | 1;                  // odd row stride: conflict-free lane-indexed rows
     __shared__ double sD[n * DS];
-    __shared__ double sred[3 * ((C::NT + 31) / 32)];
+    __shared__ double sred[4 * ((C::NT + 31) / 32)];
 
     const int tid = threadIdx.x;
     const int g = tid / GT;
@@ -507,7 +509,7 @@ __global__ void __launch_bounds__(HiCfg<N, CG>::NT, 1) ax_hi_kernel(TmaArgs a) {
     double beta = 0.0, alpha_prev = 0.0;
     int kit = 0;
     if constexpr (CG) {
-        const CgStep c = cg_k1_prologue<C::NT>(a.st, a.red, sred);
+        const CgStep c = cg_k1_prologue_t<C::NT, PC>(a.st, a.red, sred);
         if (c.done) {
             if (leader) {       // drain everything in flight
                 for (int64_t gs = 0; gs < R && gs < nsl; ++gs) mbar_wait(gbar + gs, 0);
@@ -653,19 +655,24 @@ static int tma_grid(int64_t E, int nsm) {
     return (int)(need < nsm ? (need < 1 ? 1 : need) : nsm);
 }
 
-template <int N, bool CG, bool MASS>
+template <int N, bool CG, bool MASS, bool PC = false>
 static cudaError_t tma_attr() {
     using Lo = TmaLayout<N, CG>;
     static_assert(Lo::NG >= 1, "stage does not fit in shared memory");
-    return cudaFuncSetAttribute(ax_tma_kernel<N, CG, MASS>,
+    return cudaFuncSetAttribute(ax_tma_kernel<N, CG, MASS, PC>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lo::SMEM);
 }
 
-template <bool MASS>
+// PC = false: the plain and CG kernels; PC = true: the PCG K1 only
+template <bool MASS, bool PC = false>
 static cudaError_t tma_prepare_t(int N) {
     cudaError_t e = cudaSuccess;
-    SEM_TMA_DISPATCH(N, (e = tma_attr<NN, false, MASS>(),
-                         e = (e == cudaSuccess ? tma_attr<NN, true, MASS>() : e)));
+    if constexpr (PC) {
+        SEM_TMA_DISPATCH(N, (e = tma_attr<NN, true, MASS, true>()));
+    } else {
+        SEM_TMA_DISPATCH(N, (e = tma_attr<NN, false, MASS>(),
+                             e = (e == cudaSuccess ? tma_attr<NN, true, MASS>() : e)));
+    }
     return e;
 }
 
@@ -705,18 +712,22 @@ static int hi_grid(int64_t E, int nsm) {
     return (int)(need < nsm ? (need < 1 ? 1 : need) : nsm);
 }
 
-template <int N, bool CG, bool MASS>
+template <int N, bool CG, bool MASS, bool PC = false>
 static cudaError_t hi_attr() {
     static_assert(HiCfg<N, CG>::NG >= 1, "element stage does not fit in shared memory");
-    return cudaFuncSetAttribute(ax_hi_kernel<N, CG, MASS>,
+    return cudaFuncSetAttribute(ax_hi_kernel<N, CG, MASS, PC>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HiCfg<N, CG>::SMEM);
 }
 
-template <bool MASS>
+template <bool MASS, bool PC = false>
 static cudaError_t hi_prepare_t(int N) {
     cudaError_t e = cudaSuccess;
-    SEM_HI_DISPATCH(N, (e = hi_attr<NN, false, MASS>(),
-                        e = (e == cudaSuccess ? hi_attr<NN, true, MASS>() : e)));
+    if constexpr (PC) {
+        SEM_HI_DISPATCH(N, (e = hi_attr<NN, true, MASS, true>()));
+    } else {
+        SEM_HI_DISPATCH(N, (e = hi_attr<NN, false, MASS>(),
+                            e = (e == cudaSuccess ? hi_attr<NN, true, MASS>() : e)));
+    }
     return e;
 }
 
@@ -744,7 +755,7 @@ static TmaArgs cg_args(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne
     TmaArgs a{};
     a.E = ne;
     a.G = m.G + 6 * o;
-    a.r = v.r + o;
+    a.r = k1_src(v) + o;
     a.p = v.p + o;
     a.x = v.xw + o;
     a.w = v.w + o;
@@ -755,22 +766,22 @@ static TmaArgs cg_args(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne
     return a;
 }
 
-template <bool MASS>
+template <bool MASS, bool PC = false>
 static cudaError_t launch_ax_cg_hi_t(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne,
                                      int pidx0, cudaStream_t s) {
     const TmaArgs a = cg_args<MASS>(m, v, eb, ne, pidx0);
     cudaError_t e = cudaSuccess;
-    SEM_HI_DISPATCH(m.N, e = launch_pdl(ax_hi_kernel<NN, true, MASS>, hi_grid<NN, true>(ne, m.nsm),
+    SEM_HI_DISPATCH(m.N, e = launch_pdl(ax_hi_kernel<NN, true, MASS, PC>, hi_grid<NN, true>(ne, m.nsm),
                                         HiCfg<NN, true>::NT, HiCfg<NN, true>::SMEM, s, a));
     return e;
 }
 
-template <bool MASS>
+template <bool MASS, bool PC = false>
 static cudaError_t launch_ax_cg_tma_t(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne,
                                       int pidx0, cudaStream_t s) {
     const TmaArgs a = cg_args<MASS>(m, v, eb, ne, pidx0);
     cudaError_t e = cudaSuccess;
-    SEM_TMA_DISPATCH(m.N, e = launch_pdl(ax_tma_kernel<NN, true, MASS>,
+    SEM_TMA_DISPATCH(m.N, e = launch_pdl(ax_tma_kernel<NN, true, MASS, PC>,
                                          tma_grid<NN, true>(ne, m.nsm), TmaLayout<NN, true>::NT,
                                          TmaLayout<NN, true>::SMEM, s, a));
     return e;

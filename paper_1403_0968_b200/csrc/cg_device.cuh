@@ -9,6 +9,9 @@
 //     rho_k  = (r_k, r_k)_c   partials of K2(k-1)  (K2(-1) = the CG start)
 //     pap_k  = (p_k, A p_k)   partials of K1(k)
 //     alpha_k = rho_k / pap_k,  beta_k = rho_k / rho_{k-1}
+// Jacobi PCG (CgRed::pc, NEXT-2): rho_k = (r_k, z_k)_c from K2's second set of
+// partials drives alpha and beta; rr_k = (r_k, r_k)_c still drives the stopping
+// rule (reading R4).  Without pc rr_k = rho_k.
 // With nranks > 1 a one-block kernel folds the partials into this rank's
 // value, NCCL all-gathers it, and consumers sum the ranks in ascending order.
 #pragma once
@@ -95,6 +98,11 @@ struct CgRed {
     const double *pap_all; // nranks > 1: [4][nranks] all-gathered rank values
     const double *rr_all;
     int nranks;
+    // 1: Jacobi PCG, rho from the (r, z) partials, which sit right after the
+    // (r, r) ones: part3 = part2 + 2 s2 and rz_all = rr_all + kRing nranks
+    // (derived, not stored: the kernels' parameter blocks keep their size --
+    // K1's register allocation is sensitive to it)
+    int pc;
 };
 
 inline CgRed make_red(const DevMesh &m, const CgVecs &v) {
@@ -108,11 +116,13 @@ inline CgRed make_red(const DevMesh &m, const CgVecs &v) {
     R.pap_all = v.pap_all;
     R.rr_all = v.rr_all;
     R.nranks = m.nranks;
+    R.pc = v.dinv != nullptr;
     return R;
 }
 
-// Location of the values whose ordered sum is rho_k / pap_k.
-__device__ __forceinline__ void rho_src(const CgRed &R, int k, const double *&p, int &n) {
+// Location of the values whose ordered sum is rr_k = (r_k, r_k)_c (the
+// stopping norm), rho_k (= rr_k, or (r_k, z_k)_c with pc) and pap_k.
+__device__ __forceinline__ void rr_src(const CgRed &R, int k, const double *&p, int &n) {
     if (R.nranks == 1) {
         p = R.part2 + ((k - 1) & 1) * R.s2;
         n = R.nb2;
@@ -169,12 +179,28 @@ struct CgStep {
     double alpha_prev;    // alpha_{k-1} (0 at k = 0)
 };
 
+// Location of the rho_k sources for a compile-time preconditioner flag.
+template <bool PC>
+__device__ __forceinline__ void rho_src_t(const CgRed &R, int k, const double *&p, int &n) {
+    if constexpr (PC) {
+        if (R.nranks == 1) {
+            p = R.part2 + 2 * R.s2 + ((k - 1) & 1) * R.s2;
+            n = R.nb2;
+        } else {
+            p = R.rr_all + kRing * R.nranks + (k & 3) * R.nranks;
+            n = R.nranks;
+        }
+    } else {
+        rr_src(R, k, p, n);
+    }
+}
+
 // K1 prologue (all threads of the block; contains __syncthreads): k, the
 // stopping decision, beta_k and alpha_{k-1}.  Block 0 records a stop for the
 // host (iters, rel_res, alpha_{it-1} for the final x update, the sticky flag)
-// and, at k = 0, rho_0.
-template <int NT>
-__device__ __forceinline__ CgStep cg_k1_prologue(CgState *st, const CgRed &R, double *red) {
+// and, at k = 0, rr_0.  PC: rho = (r,z) drives alpha / beta, rr = (r,r) the stop.
+template <int NT, bool PC>
+__device__ __forceinline__ CgStep cg_k1_prologue_t(CgState *st, const CgRed &R, double *red) {
     CgStep c{};
     const int done = ld_state(&st->done);
     const int k = ld_state(&st->k1);
@@ -183,27 +209,29 @@ __device__ __forceinline__ CgStep cg_k1_prologue(CgState *st, const CgRed &R, do
         c.done = true;
         return c;
     }
-    const double *src[3];
-    int cnt[3];
-    rho_src(R, k, src[0], cnt[0]);          // rho_k
-    rho_src(R, k - 1, src[1], cnt[1]);      // rho_{k-1}
-    pap_src(R, k - 1, src[2], cnt[2]);      // pap_{k-1}
+    constexpr int NS = PC ? 4 : 3;
+    const double *src[NS];
+    int cnt[NS];
+    rho_src_t<PC>(R, k, src[0], cnt[0]);     // rho_k
+    rho_src_t<PC>(R, k - 1, src[1], cnt[1]); // rho_{k-1}
+    pap_src(R, k - 1, src[2], cnt[2]);       // pap_{k-1}
     if (k == 0) cnt[1] = cnt[2] = 0;
-    double v[3];
-    block_sums<NT, 3>(src, cnt, v, red);
-    const double rho = v[0], rho_m1 = v[1], pap_m1 = v[2];
-    const double rho0 = (k == 0) ? rho : __ldcg(&st->rho0);
+    if constexpr (PC) rr_src(R, k, src[NS - 1], cnt[NS - 1]);   // rr_k (stopping norm)
+    double v[NS];
+    block_sums<NT, NS>(src, cnt, v, red);
+    const double rho = v[0], rho_m1 = v[1], pap_m1 = v[2], rr = v[NS - 1 - (PC ? 0 : 2)];
+    const double rho0 = (k == 0) ? rr : __ldcg(&st->rho0);
     const double alpha_prev = (k == 0) ? 0.0 : rho_m1 / pap_m1;
     c.beta = (k == 0) ? 0.0 : rho / rho_m1;
     c.alpha_prev = alpha_prev;
-    c.done = cg_stop(k, rho, rho0, st->maxit, st->tol);
+    c.done = cg_stop(k, rr, rho0, st->maxit, st->tol);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (k == 0) st->rho0 = rho0;
         st->k2 = k;                      // for K2 of this iteration
         if (c.done) {
             st->iters = k;
-            st->rel_res = (rho0 == 0.0) ? 0.0 : sqrt(rho) / sqrt(rho0);
-            st->converged = (rho0 == 0.0) || !(sqrt(rho) > st->tol * sqrt(rho0));
+            st->rel_res = (rho0 == 0.0) ? 0.0 : sqrt(rr) / sqrt(rho0);
+            st->converged = (rho0 == 0.0) || !(sqrt(rr) > st->tol * sqrt(rho0));
             st->alpha_km1 = alpha_prev;
             __threadfence();
             st->done = 1;
@@ -212,8 +240,22 @@ __device__ __forceinline__ CgStep cg_k1_prologue(CgState *st, const CgRed &R, do
     return c;
 }
 
-// K2 prologue (all threads): k, the same stopping decision, alpha_k.
+// The PCG prologue is kept out of line so the CG kernels' main loops compile
+// exactly as without a preconditioner (K1's register allocation is sensitive).
 template <int NT>
+__device__ __noinline__ CgStep cg_k1_prologue_pc(CgState *st, const CgRed &R, double *red) {
+    return cg_k1_prologue_t<NT, true>(st, R, red);
+}
+
+template <int NT>
+__device__ __forceinline__ CgStep cg_k1_prologue(CgState *st, const CgRed &R, double *red) {
+    if (R.pc) return cg_k1_prologue_pc<NT>(st, R, red);
+    return cg_k1_prologue_t<NT, false>(st, R, red);
+}
+
+// K2 prologue (all threads): k, the same stopping decision, alpha_k.  K2 is
+// instantiated per preconditioner (k2_kernel<N, INIT, PC>).
+template <int NT, bool PC>
 __device__ __forceinline__ CgStep cg_k2_prologue(CgState *st, const CgRed &R, double *red,
                                                  double &alpha) {
     CgStep c{};
@@ -224,14 +266,17 @@ __device__ __forceinline__ CgStep cg_k2_prologue(CgState *st, const CgRed &R, do
         c.done = true;
         return c;
     }
-    const double *src[2];
-    int cnt[2];
-    rho_src(R, k, src[0], cnt[0]);          // rho_k
-    pap_src(R, k, src[1], cnt[1]);          // pap_k
-    double v[2];
-    block_sums<NT, 2>(src, cnt, v, red);
-    const double rho0 = (k == 0) ? v[0] : __ldcg(&st->rho0);
-    c.done = cg_stop(k, v[0], rho0, st->maxit, st->tol);
+    constexpr int NS = PC ? 3 : 2;
+    const double *src[NS];
+    int cnt[NS];
+    rho_src_t<PC>(R, k, src[0], cnt[0]);     // rho_k
+    pap_src(R, k, src[1], cnt[1]);           // pap_k
+    if constexpr (PC) rr_src(R, k, src[2], cnt[2]);   // rr_k (stopping norm)
+    double v[NS];
+    block_sums<NT, NS>(src, cnt, v, red);
+    const double rr = PC ? v[NS - 1] : v[0];
+    const double rho0 = (k == 0) ? rr : __ldcg(&st->rho0);
+    c.done = cg_stop(k, rr, rho0, st->maxit, st->tol);
     alpha = v[0] / v[1];
     if (blockIdx.x == 0 && threadIdx.x == 0 && !c.done) st->k1 = k + 1;   // for K1 of k+1
     return c;

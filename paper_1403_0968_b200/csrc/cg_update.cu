@@ -13,6 +13,8 @@
 // global node is visited once) and one launch + one reduction replaces the
 // gather-scatter pass and the separate r-update pass.  alpha = rho_k / pAp_k
 // with pAp from K1.  INIT = true forms r0 = mask (b - Q Q^T A_L x0) and rho_0.
+// PC = true (Jacobi PCG, NEXT-2): also z = dinv r at every copy (dinv is
+// continuous: read once per group) and the second partial (r, z).
 #include "cg_device.cuh"
 #include "sem_internal.h"
 
@@ -29,6 +31,9 @@ struct K2Args {
     double *r;
     CgRed red;                // where the scalar reductions live
     double *part2;            // this kernel's (r, r) partials, [2][s2]
+    const double *dinv;       // PC: Jacobi inverse diagonal (continuous, 0 on Dirichlet)
+    double *z;                // PC: z = dinv r
+    double *part3;            // PC: (r, z) partials, [2][s2]
     CgState *st;
     int32_t nich;                      // element-interior chunks (first)
     int32_t cchunk[kMaxClasses + 1];   // then: first group chunk of each class
@@ -50,10 +55,10 @@ __device__ __forceinline__ bool k2_owned(const K2Args &a, int g) {
     return !a.own || ((__ldg(a.own + (g >> 5)) >> (g & 31)) & 1u);
 }
 
-template <int M, int U, bool INIT>
-__device__ __forceinline__ double k2_groups(const K2Args &a, const int32_t *__restrict__ ix, int m,
-                                            int cnt, int q0, int qstride, double alpha,
-                                            int gstart) {
+template <int M, int U, bool INIT, bool PC>
+__device__ __forceinline__ void k2_groups(const K2Args &a, const int32_t *__restrict__ ix, int m,
+                                          int cnt, int q0, int qstride, double alpha, int gstart,
+                                          double &part, double &partz) {
     constexpr int MM = M ? M : 8;
     const int mm = M ? M : m;
     int li[U][MM];
@@ -65,14 +70,14 @@ __device__ __forceinline__ double k2_groups(const K2Args &a, const int32_t *__re
 #pragma unroll
         for (int t = 0; t < MM; ++t) li[u][t] = (on[u] && t < mm) ? __ldg(ix + t * cnt + q) : 0;
     }
-    double v[U][MM], r0[U];
+    double v[U][MM], r0[U], dv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
 #pragma unroll
         for (int t = 0; t < MM; ++t) v[u][t] = (on[u] && t < mm) ? a.w[li[u][t]] : 0.0;
         r0[u] = on[u] ? (INIT ? a.b[li[u][0]] : a.r[li[u][0]]) : 0.0;
+        if constexpr (PC) dv[u] = on[u] ? __ldg(a.dinv + li[u][0]) : 0.0;
     }
-    double part = 0.0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         if (!on[u]) continue;
@@ -81,12 +86,19 @@ __device__ __forceinline__ double k2_groups(const K2Args &a, const int32_t *__re
         for (int t = 1; t < MM; ++t)
             if (t < mm) s += v[u][t];                        // ascending local order
         const double rn = INIT ? r0[u] - s : r0[u] - alpha * s;
+        const bool own = k2_owned(a, gstart + q0 + u * qstride);
 #pragma unroll
         for (int t = 0; t < MM; ++t)
             if (t < mm) a.r[li[u][t]] = rn;
-        if (k2_owned(a, gstart + q0 + u * qstride)) part += rn * rn;
+        if (own) part += rn * rn;
+        if constexpr (PC) {
+            const double zn = dv[u] * rn;
+#pragma unroll
+            for (int t = 0; t < MM; ++t)
+                if (t < mm) a.z[li[u][t]] = zn;
+            if (own) partz += rn * zn;
+        }
     }
-    return part;
 }
 
 // Element-interior nodes of one chunk (m = 1, never Dirichlet): local
@@ -107,11 +119,11 @@ __device__ __forceinline__ void k2_interior_idx(int64_t E, int chunk, int (&l)[U
     }
 }
 
-template <int N, bool INIT>
+template <int N, bool INIT, bool PC>
 __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __grid_constant__ K2Args a) {
     constexpr int ni = N - 1;
     constexpr int U = 4;
-    __shared__ double sred[2 * (kK2Threads / 32)];
+    __shared__ double sred[3 * (kK2Threads / 32)];
     if constexpr (!INIT) pdl_trigger();
     if constexpr (!INIT) pdl_wait();
 
@@ -123,7 +135,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
     const int nich = a.nich;
     int ch = blockIdx.x;
     int l[U];
-    double rv[U], wv[U];
+    double rv[U], wv[U], dv[U];
     bool staged = false;
     if constexpr (ni > 0) {
         if (ch < nich) {
@@ -133,6 +145,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
                 if (l[u] >= 0) {
                     rv[u] = INIT ? a.b[l[u]] : a.r[l[u]];
                     wv[u] = __ldcs(a.w + l[u]);
+                    if constexpr (PC) dv[u] = __ldg(a.dinv + l[u]);
                 }
             }
             staged = true;
@@ -142,12 +155,12 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
     double alpha = 0.0;
     int k = -1;               // INIT produces the partials of rho_0 as "iteration -1"
     if constexpr (!INIT) {
-        const CgStep c = cg_k2_prologue<kK2Threads>(a.st, a.red, sred, alpha);
+        const CgStep c = cg_k2_prologue<kK2Threads, PC>(a.st, a.red, sred, alpha);
         if (c.done) return;
         k = c.k;
     }
 
-    double part = 0.0;
+    double part = 0.0, partz = 0.0;
     for (; ch < a.nchunks; ch += gridDim.x) {
         if (ch < nich) {
             if constexpr (ni > 0) {
@@ -158,6 +171,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
                         if (l[u] >= 0) {
                             rv[u] = INIT ? a.b[l[u]] : a.r[l[u]];
                             wv[u] = __ldcs(a.w + l[u]);
+                            if constexpr (PC) dv[u] = __ldg(a.dinv + l[u]);
                         }
                     }
                 }
@@ -168,6 +182,11 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
                         const double rn = INIT ? rv[u] - wv[u] : rv[u] - alpha * wv[u];
                         a.r[l[u]] = rn;
                         part += rn * rn;
+                        if constexpr (PC) {
+                            const double zn = dv[u] * rn;
+                            a.z[l[u]] = zn;
+                            partz += rn * zn;
+                        }
                     }
                 }
             }
@@ -186,15 +205,18 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
             for (int u = 0; u < k2_upb(m); ++u) {
                 const int q = base + u * kK2Threads;
                 if (q < cnt)
-                    for (int t = 0; t < m; ++t) a.r[__ldg(ix + t * cnt + q)] = 0.0;
+                    for (int t = 0; t < m; ++t) {
+                        a.r[__ldg(ix + t * cnt + q)] = 0.0;
+                        if constexpr (PC) a.z[__ldg(ix + t * cnt + q)] = 0.0;
+                    }
             }
             continue;
         }
         switch (m) {
-        case 1: part += k2_groups<1, 4, INIT>(a, ix, m, cnt, base, kK2Threads, alpha, gs0); break;
-        case 2: part += k2_groups<2, 4, INIT>(a, ix, m, cnt, base, kK2Threads, alpha, gs0); break;
-        case 4: part += k2_groups<4, 2, INIT>(a, ix, m, cnt, base, kK2Threads, alpha, gs0); break;
-        case 8: part += k2_groups<8, 1, INIT>(a, ix, m, cnt, base, kK2Threads, alpha, gs0); break;
+        case 1: k2_groups<1, 4, INIT, PC>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
+        case 2: k2_groups<2, 4, INIT, PC>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
+        case 4: k2_groups<4, 2, INIT, PC>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
+        case 8: k2_groups<8, 1, INIT, PC>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
         default: {
             const int q = base;
             if (q < cnt) {
@@ -203,15 +225,30 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
                 const double r0 = INIT ? a.b[__ldg(ix + q)] : a.r[__ldg(ix + q)];
                 const double rn = INIT ? r0 - s : r0 - alpha * s;
                 for (int t = 0; t < m; ++t) a.r[__ldg(ix + t * cnt + q)] = rn;
-                if (k2_owned(a, gs0 + q)) part += rn * rn;
+                const bool own = k2_owned(a, gs0 + q);
+                if (own) part += rn * rn;
+                if constexpr (PC) {
+                    const double zn = __ldg(a.dinv + __ldg(ix + q)) * rn;
+                    for (int t = 0; t < m; ++t) a.z[__ldg(ix + t * cnt + q)] = zn;
+                    if (own) partz += rn * zn;
+                }
             }
         } break;
         }
     }
 
     // one deterministic partial per block; consumers reduce (cg_device.cuh)
-    const double bs = block_sum<kK2Threads>(part, sred);
-    if (threadIdx.x == 0) a.part2[(k & 1) * a.red.s2 + blockIdx.x] = bs;
+    if constexpr (PC) {
+        double v2[2] = {part, partz};
+        block_sum_vec<kK2Threads, 2>(v2, sred);
+        if (threadIdx.x == 0) {
+            a.part2[(k & 1) * a.red.s2 + blockIdx.x] = v2[0];
+            a.part3[(k & 1) * a.red.s2 + blockIdx.x] = v2[1];
+        }
+    } else {
+        const double bs = block_sum<kK2Threads>(part, sred);
+        if (threadIdx.x == 0) a.part2[(k & 1) * a.red.s2 + blockIdx.x] = bs;
+    }
 }
 
 #define SEM_K2_DISPATCH(N_, ...)                                             \
@@ -249,6 +286,9 @@ cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t
     a.r = v.r;
     a.red = make_red(m, v);
     a.part2 = v.part2;
+    a.dinv = v.dinv;
+    a.z = v.z;
+    a.part3 = v.part3;
     a.st = v.st;
     // chunk table: interior chunks first, then the group classes (Dirichlet
     // classes only at INIT)
@@ -265,10 +305,15 @@ cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t
     a.nchunks = a.nich + nch;
     const int nb = k2_blocks(m, init);
     cudaError_t e = cudaSuccess;
-    if (init) {
-        SEM_K2_DISPATCH(m.N, (k2_kernel<NN, true><<<nb, kK2Threads, 0, s>>>(a), e = cudaGetLastError()));
+    const bool pc = v.dinv != nullptr;
+    if (init && pc) {
+        SEM_K2_DISPATCH(m.N, (k2_kernel<NN, true, true><<<nb, kK2Threads, 0, s>>>(a), e = cudaGetLastError()));
+    } else if (init) {
+        SEM_K2_DISPATCH(m.N, (k2_kernel<NN, true, false><<<nb, kK2Threads, 0, s>>>(a), e = cudaGetLastError()));
+    } else if (pc) {
+        SEM_K2_DISPATCH(m.N, e = launch_pdl(k2_kernel<NN, false, true>, nb, kK2Threads, 0, s, a));
     } else {
-        SEM_K2_DISPATCH(m.N, e = launch_pdl(k2_kernel<NN, false>, nb, kK2Threads, 0, s, a));
+        SEM_K2_DISPATCH(m.N, e = launch_pdl(k2_kernel<NN, false, false>, nb, kK2Threads, 0, s, a));
     }
     return e;
 }

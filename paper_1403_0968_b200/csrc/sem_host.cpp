@@ -50,13 +50,16 @@ struct sem_ctx {
     // CUDA graph of kChunk CG iterations (captured on first use)
     bool use_graph = true;
     cudaStream_t cap_stream = nullptr;
-    cudaGraphExec_t graph_exec = nullptr;
-    int64_t graph_kernels = 0;
+    cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};   // by preconditioner (0 none, 1 Jacobi)
+    int64_t graph_kernels[2] = {0, 0};
     cudaGraphExec_t replay_exec = nullptr;   // sem_kernel_replay
     // boundary/interior K1 split (k1_split): the exchange runs on `side`
     // between fork (boundary K1 done) and join (before the pap all-gather)
     cudaStream_t side = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    // Jacobi preconditioner (NEXT-2): mask / Q Q^T diag(A_L), formed on first use
+    double *dinv_buf = nullptr;
+    bool dinv_ready = false;
 };
 
 static constexpr int kChunk = 8;     // CG iterations per graph launch / poll (multiple of 4)
@@ -216,7 +219,7 @@ static void diff_matrix(int N, const double *x, double *D) {
 // ---------------------------------------------------------------------------
 namespace {
 struct Layout {
-    size_t G, BM, H, r, p, w, xw, D, gs_idx, own, partials, rr_all, pap_all, st, total;
+    size_t G, BM, H, r, p, w, xw, z, dinv, D, gs_idx, own, partials, rr_all, pap_all, st, total;
     int64_t nsurf_cap, partial_cap;
 };
 
@@ -242,11 +245,13 @@ Layout make_layout(int N, int64_t E, int nranks, bool mass) {
     Lo.p = take(sizeof(double) * L);
     Lo.w = take(sizeof(double) * L);
     Lo.xw = take(sizeof(double) * L);
+    Lo.z = take(sizeof(double) * L);
+    Lo.dinv = take(sizeof(double) * L);
     Lo.D = take(sizeof(double) * (n * n + n));
     Lo.gs_idx = take(sizeof(int32_t) * Lo.nsurf_cap);
     Lo.own = take(sizeof(uint32_t) * ((Lo.nsurf_cap + 31) / 32 + 1));
-    Lo.partials = take(sizeof(double) * 4 * Lo.partial_cap);   // part1[2][cap], part2[2][cap]
-    Lo.rr_all = take(sizeof(double) * kRing * nranks);
+    Lo.partials = take(sizeof(double) * 6 * Lo.partial_cap);   // part1, part2, part3: [2][cap]
+    Lo.rr_all = take(sizeof(double) * 2 * kRing * nranks);     // rr_all, then rz_all
     Lo.pap_all = take(sizeof(double) * kRing * nranks);
     Lo.st = take(sizeof(CgState));
     Lo.total = o;
@@ -499,8 +504,13 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
     cv.xw = reinterpret_cast<double *>(ws + Lo.xw);
     cv.part1 = reinterpret_cast<double *>(ws + Lo.partials);
     cv.part2 = cv.part1 + 2 * Lo.partial_cap;
+    cv.part3 = cv.part2 + 2 * Lo.partial_cap;
+    cv.z = reinterpret_cast<double *>(ws + Lo.z);
+    cv.dinv = nullptr;
+    ctx->dinv_buf = reinterpret_cast<double *>(ws + Lo.dinv);
     cv.s1 = cv.s2 = (int)Lo.partial_cap;
     cv.rr_all = reinterpret_cast<double *>(ws + Lo.rr_all);
+    cv.rz_all = cv.rr_all + kRing * ctx->nranks;     // cg_device.cuh rho_src_t relies on it
     cv.pap_all = reinterpret_cast<double *>(ws + Lo.pap_all);
     cv.st = reinterpret_cast<CgState *>(ws + Lo.st);
     {
@@ -563,6 +573,7 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
                                cudaMemcpyHostToDevice, s));
         CU(cudaMemsetAsync(cv.st, 0, sizeof(CgState), s));
         CU(cudaMemsetAsync(cv.rr_all, 0, sizeof(double) * kRing * ctx->nranks, s));
+        CU(cudaMemsetAsync(cv.rz_all, 0, sizeof(double) * kRing * ctx->nranks, s));
         CU(cudaMemsetAsync(cv.pap_all, 0, sizeof(double) * kRing * ctx->nranks, s));
         // xyz -> device (temporarily in r|p|w, exactly 3L doubles), then G^, B
         double *xyz_d = cv.r;
@@ -654,8 +665,10 @@ extern "C" int sem_exchange_plan(const sem_mesh *mesh, int N, int64_t *counts, i
 
 extern "C" void sem_free(sem_ctx *ctx) {
     if (!ctx) return;
-    if (ctx->graph_exec || ctx->replay_exec) cudaStreamSynchronize(ctx->stream);
-    if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+    if (ctx->graph_exec[0] || ctx->graph_exec[1] || ctx->replay_exec)
+        cudaStreamSynchronize(ctx->stream);
+    for (auto &g : ctx->graph_exec)
+        if (g) cudaGraphExecDestroy(g);
     if (ctx->replay_exec) cudaGraphExecDestroy(ctx->replay_exec);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->side) cudaStreamDestroy(ctx->side);
@@ -755,10 +768,13 @@ static int allgather_scalar(sem_ctx *ctx, double *slot_base, cudaStream_t s) {
 // Algorithmic bytes of one K2 launch: w copies read + r copies written at
 // surface nodes, r read once per non-Dirichlet group, and r read/write + w
 // read at element-interior nodes.
+// Jacobi PCG adds z written at every copy and dinv read once per group.
 static double k2_bytes(const sem_ctx *ctx) {
     const int64_t ni = ctx->N - 1;
     const double nint = double(ctx->E) * ni * ni * ni;
-    return 16.0 * ctx->dm.nsurf + 8.0 * (ctx->dm.ngroups - ctx->dm.ndir) + 24.0 * nint;
+    const double pc = ctx->cv.dinv ? 1.0 : 0.0;
+    return (16.0 + 8.0 * pc) * ctx->dm.nsurf + (8.0 + 8.0 * pc) * (ctx->dm.ngroups - ctx->dm.ndir) +
+           (24.0 + 16.0 * pc) * nint;
 }
 
 // One CG iteration: K1 (x/p update + Ax + (w,p) -> pap slot), [all-gather of
@@ -802,6 +818,10 @@ static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
     if (P > 1) {
         LAUNCH(launch_cg_red_rr(ctx->dm, v, s));
         if ((rc = allgather_scalar(ctx, v.rr_all + ((k + 1) & 3) * P, s))) return rc;
+        if (v.dinv) {
+            LAUNCH(launch_cg_red_rz(ctx->dm, v, s));
+            if ((rc = allgather_scalar(ctx, v.rz_all + ((k + 1) & 3) * P, s))) return rc;
+        }
     }
     return SEM_OK;
 }
@@ -816,22 +836,62 @@ static int build_cg_graph(sem_ctx *ctx) {
     for (int q = 0; q < kChunk && rc == SEM_OK; ++q) rc = enqueue_iteration(ctx, q, ctx->cap_stream);
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &g);
-    ctx->graph_kernels = ctx->launches - l0;
+    ctx->graph_kernels[ctx->cv.dinv ? 1 : 0] = ctx->launches - l0;
     ctx->launches = l0;
     if (rc) {
         if (g) cudaGraphDestroy(g);
         return rc;
     }
     CU(e);
-    e = cudaGraphInstantiate(&ctx->graph_exec, g, 0);
+    e = cudaGraphInstantiate(&ctx->graph_exec[ctx->cv.dinv ? 1 : 0], g, 0);
     cudaGraphDestroy(g);
     CU(e);
     return SEM_OK;
 }
 
+// d = Q Q^T diag(A_L) (local storage, unmasked), the assembled diagonal.
+static int diag_impl(sem_ctx *ctx, double *d, cudaStream_t s) {
+    LAUNCH(launch_diag(ctx->dm, d, s));
+    return dssum_impl(ctx, d, 0, -1, s);
+}
+
+extern "C" int sem_diag(sem_ctx *ctx, double *d) {
+    CHECK_CTX();
+    if (!d || !aligned8(d)) return fail(ctx, SEM_EINVAL, "sem_diag: bad pointer");
+    return diag_impl(ctx, d, ctx->stream);
+}
+
+// Jacobi preconditioner dinv = mask / (Q Q^T diag A_L), once per context.
+static int prepare_jacobi(sem_ctx *ctx, cudaStream_t s) {
+    if (ctx->dinv_ready) return SEM_OK;
+    double *d = ctx->cv.z;            // scratch: z is rewritten by the next K2 start
+    int rc = diag_impl(ctx, d, s);
+    if (rc) return rc;
+    LAUNCH(launch_recip(ctx->dm, d, ctx->dinv_buf, s));
+    if (ctx->dm.ndir > 0) LAUNCH(launch_mask(ctx->dm, ctx->dinv_buf, s));
+    ctx->dinv_ready = true;
+    return SEM_OK;
+}
+
+static int cg_impl(sem_ctx *ctx, int precond, const double *b, double *x, double tol, int maxit,
+                   int *iters, double *rel_res);
+
 extern "C" int sem_cg(sem_ctx *ctx, const double *b, double *x, double tol, int maxit,
                       int *iters, double *rel_res) {
     CHECK_CTX();
+    return cg_impl(ctx, SEM_PC_NONE, b, x, tol, maxit, iters, rel_res);
+}
+
+extern "C" int sem_pcg(sem_ctx *ctx, int precond, const double *b, double *x, double tol,
+                       int maxit, int *iters, double *rel_res) {
+    CHECK_CTX();
+    if (precond != SEM_PC_NONE && precond != SEM_PC_JACOBI)
+        return fail(ctx, SEM_EINVAL, "sem_pcg: precond must be SEM_PC_NONE or SEM_PC_JACOBI");
+    return cg_impl(ctx, precond, b, x, tol, maxit, iters, rel_res);
+}
+
+static int cg_impl(sem_ctx *ctx, int precond, const double *b, double *x, double tol, int maxit,
+                   int *iters, double *rel_res) {
     if (!b || !x || !aligned8(b) || !aligned8(x)) return fail(ctx, SEM_EINVAL, "sem_cg: bad pointer");
     if (!(tol >= 0.0) || maxit < 0) return fail(ctx, SEM_EINVAL, "sem_cg: tol >= 0 and maxit >= 0 required");
     cudaStream_t s = ctx->stream;
@@ -840,6 +900,8 @@ extern "C" int sem_cg(sem_ctx *ctx, const double *b, double *x, double tol, int 
     v.x = x;
     const int P = ctx->nranks;
     int rc;
+    if (precond == SEM_PC_JACOBI && (rc = prepare_jacobi(ctx, s))) return rc;
+    v.dinv = (precond == SEM_PC_JACOBI) ? ctx->dinv_buf : nullptr;
     // tol / maxit into the device state (the init kernel resets the rest)
     {
         CgState h{};
@@ -856,6 +918,10 @@ extern "C" int sem_cg(sem_ctx *ctx, const double *b, double *x, double tol, int 
     if (P > 1) {
         LAUNCH(launch_cg_red_rr(ctx->dm, v, s));
         if ((rc = allgather_scalar(ctx, v.rr_all + 0 * P, s))) return rc;
+        if (v.dinv) {
+            LAUNCH(launch_cg_red_rz(ctx->dm, v, s));
+            if ((rc = allgather_scalar(ctx, v.rz_all + 0 * P, s))) return rc;
+        }
     }
 
     // Iterations in chunks of kChunk (a multiple of 4: the all-gather slot of
@@ -864,12 +930,13 @@ extern "C" int sem_cg(sem_ctx *ctx, const double *b, double *x, double tol, int 
     // more chunks once it is set (later kernels of a chunk are no-ops).  Each
     // chunk is one CUDA-graph launch unless profiling (per-launch events).
     const bool graph = !ctx->prof && ctx->use_graph;
-    if (graph && !ctx->graph_exec && (rc = build_cg_graph(ctx))) return rc;
+    cudaGraphExec_t &gexec = ctx->graph_exec[v.dinv ? 1 : 0];
+    if (graph && !gexec && (rc = build_cg_graph(ctx))) return rc;
     int k = 0, c = 0;
     while (true) {
         if (graph) {
-            CU(cudaGraphLaunch(ctx->graph_exec, s));
-            ctx->launches += ctx->graph_kernels;
+            CU(cudaGraphLaunch(gexec, s));
+            ctx->launches += ctx->graph_kernels[v.dinv ? 1 : 0];
             k += kChunk;
         } else {
             for (int q = 0; q < kChunk; ++q, ++k)

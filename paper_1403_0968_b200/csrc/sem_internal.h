@@ -13,7 +13,7 @@ constexpr int kTmaMaxN = 10;     // TMA-pipelined Ax kernel for N <= 10
 
 // Device-resident CG state (one per context, in the workspace).
 struct CgState {
-    double rho0;                // (r0, r0)_c, written by K1 at k = 0
+    double rho0;                // (r0, r0)_c, written by K1 at k = 0 (the stopping norm)
     double tol;
     int32_t maxit;
     int32_t done;               // sticky: 1 once the stopping rule fired
@@ -73,7 +73,16 @@ struct CgVecs {
     double *rr_all;             // [kRing][nranks] rank values of (r,r)_c (nranks > 1)
     double *pap_all;            // [kRing][nranks] rank values of (p,Ap) (nranks > 1)
     CgState *st;
+    // Jacobi PCG (NEXT-2; nullptr dinv = identity preconditioner, plain CG):
+    // z = dinv .* r written by K2 next to r, read by K1 in place of r
+    const double *dinv;         // [L] mask / (Q Q^T diag A_L), continuous
+    double *z;                  // [L]
+    double *part3;              // [2][s2] per-block partials of (r, z) (K2) = part2 + 2 s2
+    double *rz_all;             // [kRing][nranks] rank values of (r,z)_c = rr_all + kRing nranks
 };
+
+// the vector K1 forms p from: p = z + beta p (PCG) or p = r + beta p (CG)
+inline const double *k1_src(const CgVecs &v) { return v.dinv ? v.z : v.r; }
 
 constexpr int kGsThreads = 256;
 constexpr int kMaxPartials = 1024;     // per-block partial slots of K1 / K2 (<= 4 CTAs/SM)
@@ -111,6 +120,12 @@ cudaError_t launch_cg_finish(const DevMesh &m, const CgVecs &v, cudaStream_t s);
 // pap_all / rr_all before the NCCL all-gather
 cudaError_t launch_cg_red_pap(const DevMesh &m, const CgVecs &v, cudaStream_t s);
 cudaError_t launch_cg_red_rr(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+cudaError_t launch_cg_red_rz(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+// Jacobi preconditioner (NEXT-2): d = diag(A_L) per local node (unassembled;
+// kappa-folded G^ + the mass term H); then, after Q Q^T d, dinv = 1 / d
+// (the caller masks it)
+cudaError_t launch_diag(const DevMesh &m, double *d, cudaStream_t s);
+cudaError_t launch_recip(const DevMesh &m, const double *d, double *dinv, cudaStream_t s);
 
 // ax_tma.cu
 bool tma_supported(int N);

@@ -95,6 +95,49 @@ __global__ void geom_kernel(int n, int64_t E, const double *__restrict__ D,
 }
 
 // --------------------------------------------------------------------------
+// NEXT-2 (Jacobi PCG): the diagonal of the local operator.
+// A^e = D_r^T G_rr D_r + ... (6 factor products, G^ symmetric), so for node
+// q = (i,j,k) the unit vector's reference gradient is nonzero only on the
+// three GLL lines through q, which gives
+//   d_q = sum_m D_mi^2 G_rr(m,j,k) + sum_m D_mj^2 G_ss(i,m,k) + sum_m D_mk^2 G_tt(i,j,m)
+//       + 2 D_ii D_jj G_rs(q) + 2 D_ii D_kk G_rt(q) + 2 D_jj D_kk G_st(q) + H(q)
+// (kappa is folded into G^, H = alpha w J).  Setup-only; one thread per node.
+// --------------------------------------------------------------------------
+__global__ void diag_kernel(int n, int64_t E, const double *__restrict__ D,
+                            const double *__restrict__ G, const double *__restrict__ H,
+                            double *__restrict__ d, bool slice_major) {
+    const int n2 = n * n, n3 = n2 * n;
+    const int64_t L = E * n3;
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L;
+         l += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = l / n3;
+        const int q = (int)(l - e * n3);
+        const int i = q % n, j = (q / n) % n, k = q / n2;
+        const double *Ge = G + e * 6 * n3;
+        // factor f at node (a,b,c) of this element, in either G^ layout
+        auto g = [&](int f, int a, int b, int c) {
+            return slice_major ? Ge[(int64_t)c * 6 * n2 + f * n2 + a + n * b]
+                               : Ge[f * n3 + a + n * b + n2 * c];
+        };
+        double s = 0.0;
+        for (int m = 0; m < n; ++m) {
+            const double dr = D[m * n + i], ds = D[m * n + j], dt = D[m * n + k];
+            s += dr * dr * g(0, m, j, k) + ds * ds * g(3, i, m, k) + dt * dt * g(5, i, j, m);
+        }
+        const double di = D[i * n + i], dj = D[j * n + j], dk = D[k * n + k];
+        s += 2.0 * (di * dj * g(1, i, j, k) + di * dk * g(2, i, j, k) + dj * dk * g(4, i, j, k));
+        if (H) s += H[l];
+        d[l] = s;
+    }
+}
+
+__global__ void recip_kernel(int64_t L, const double *__restrict__ d, double *__restrict__ dinv) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L;
+         l += (int64_t)gridDim.x * blockDim.x)
+        dinv[l] = 1.0 / d[l];
+}
+
+// --------------------------------------------------------------------------
 // a3-a5: local stiffness apply.  Block = EPB elements x (n x n) threads; thread
 // (i,j) owns the k-column of its element in registers:
 //   u_r, u_s from the k-slice in shared memory, u_t from the register column,
@@ -135,7 +178,7 @@ ax_kernel(int64_t E, const double *__restrict__ Dg, const double *__restrict__ G
     __shared__ double su[EPB][n3];
     __shared__ double sfr[EPB][n2];
     __shared__ double sfs[EPB][n2];
-    __shared__ double sred[3 * ((NT + 31) / 32)];
+    __shared__ double sred[4 * ((NT + 31) / 32)];
 
     double beta = 0.0, alpha_prev = 0.0;
     int kit = 0;
@@ -483,7 +526,7 @@ cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
     if (m.use_hi) return launch_ax_cg_hi(m, v, 0, m.E, 0, s);
     if (m.use_tma) return launch_ax_cg_tma(m, v, 0, m.E, 0, s);
     if (m.H) return cudaErrorInvalidValue;
-    AxCgArgs a{v.r, v.p, v.xw, make_red(m, v), v.part1, v.st};
+    AxCgArgs a{k1_src(v), v.p, v.xw, make_red(m, v), v.part1, v.st};
     cudaError_t e = cudaSuccess;
     SEM_DISPATCH_N(m.N, (e = launch_pdl(ax_kernel<NN, true>, ax_grid(m.N, m.E, m.nsm), AxCfg<NN>::NT,
                                         0, s, m.E, m.D, m.G, (const double *)nullptr, v.w, a)));
@@ -541,6 +584,22 @@ cudaError_t launch_cg_red_pap(const DevMesh &m, const CgVecs &v, cudaStream_t s)
 cudaError_t launch_cg_red_rr(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
     cg_red_kernel<<<1, kRedThreads, 0, s>>>(v.part2, v.s2, v.nb2, v.rr_all, v.st, 1, m.rank,
                                              m.nranks);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cg_red_rz(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
+    cg_red_kernel<<<1, kRedThreads, 0, s>>>(v.part3, v.s2, v.nb2, v.rz_all, v.st, 1, m.rank,
+                                             m.nranks);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_diag(const DevMesh &m, double *d, cudaStream_t s) {
+    diag_kernel<<<grid_for(m.L, 256), 256, 0, s>>>(m.n, m.E, m.D, m.G, m.H, d, m.use_hi);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_recip(const DevMesh &m, const double *d, double *dinv, cudaStream_t s) {
+    recip_kernel<<<grid_for(m.L, 256), 256, 0, s>>>(m.L, d, dinv);
     return cudaGetLastError();
 }
 

@@ -43,7 +43,11 @@ class SemMesh(ctypes.Structure):
 EXPORTS = ["sem_version", "sem_gll", "sem_workspace_bytes", "sem_setup", "sem_sizes",
            "sem_ax", "sem_dssum", "sem_mask", "sem_mass", "sem_cg", "sem_launch_count",
            "sem_free", "sem_strerror", "sem_last_error", "sem_nccl_id_bytes",
-           "sem_nccl_get_unique_id", "sem_profile", "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan"]
+           "sem_nccl_get_unique_id", "sem_profile", "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan",
+           "sem_pcg", "sem_diag"]
+
+# preconditioners of sem_pcg (include/sem.h enum sem_precond)
+PRECOND = {"none": 0, "jacobi": 1}
 
 _lib = None
 
@@ -77,6 +81,9 @@ def lib():
     L.sem_mass.argtypes = [P, P, P]
     L.sem_cg.argtypes = [P, P, P, ctypes.c_double, ctypes.c_int,
                          ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
+    L.sem_pcg.argtypes = [P, ctypes.c_int, P, P, ctypes.c_double, ctypes.c_int,
+                          ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
+    L.sem_diag.argtypes = [P, P]
     L.sem_launch_count.argtypes = [P]
     L.sem_launch_count.restype = i64
     L.sem_free.argtypes = [P]
@@ -95,7 +102,7 @@ def lib():
                                     ctypes.POINTER(i64), ctypes.POINTER(i64)]
     for f in ("sem_gll", "sem_workspace_bytes", "sem_setup", "sem_sizes", "sem_ax", "sem_dssum",
               "sem_mask", "sem_mass", "sem_cg", "sem_nccl_get_unique_id", "sem_profile",
-              "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan"):
+              "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan", "sem_pcg", "sem_diag"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
@@ -213,19 +220,34 @@ class Context:
                self._ctx)
         return b
 
-    def cg(self, b, x=None, tol: float = 1e-8, maxit: int = 1000, raise_noconv: bool = False):
-        """Returns (x, iters, rel_res, converged)."""
+    def cg(self, b, x=None, tol: float = 1e-8, maxit: int = 1000, raise_noconv: bool = False,
+           precond: str = "none"):
+        """Returns (x, iters, rel_res, converged).  precond="jacobi": sem_pcg
+        with the Jacobi preconditioner (NEXT-2)."""
         import torch
         if x is None:
             x = torch.zeros_like(b)
         it = ctypes.c_int(0)
         rr = ctypes.c_double(0.0)
-        rc = lib().sem_cg(self._ctx, _dptr(b, self.nlocal, "b"), _dptr(x, self.nlocal, "x"),
-                          float(tol), int(maxit), ctypes.byref(it), ctypes.byref(rr))
+        if precond == "none":
+            rc = lib().sem_cg(self._ctx, _dptr(b, self.nlocal, "b"), _dptr(x, self.nlocal, "x"),
+                              float(tol), int(maxit), ctypes.byref(it), ctypes.byref(rr))
+        else:
+            rc = lib().sem_pcg(self._ctx, PRECOND[precond], _dptr(b, self.nlocal, "b"),
+                               _dptr(x, self.nlocal, "x"), float(tol), int(maxit),
+                               ctypes.byref(it), ctypes.byref(rr))
         if rc == SEM_ENOCONV and not raise_noconv:
             return x, it.value, rr.value, False
         _check(rc, self._ctx)
         return x, it.value, rr.value, True
+
+    def diag(self, d=None):
+        """d = Q Q^T diag(A_L): assembled operator diagonal in local storage."""
+        import torch
+        if d is None:
+            d = torch.empty(self.nlocal, dtype=torch.float64, device=f"cuda:{self.device}")
+        _check(lib().sem_diag(self._ctx, _dptr(d, self.nlocal, "d")), self._ctx)
+        return d
 
     def rhs(self, f):
         """b = mask Q Q^T (B_L f): assembled, masked right-hand side."""

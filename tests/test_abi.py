@@ -155,6 +155,8 @@ def test_null_context_calls(L):
     assert L.sem_ax(None, None, None) == sem.SEM_ESTATE
     assert L.sem_dssum(None, None) == sem.SEM_ESTATE
     assert L.sem_cg(None, None, None, 1e-8, 10, None, None) == sem.SEM_ESTATE
+    assert L.sem_pcg(None, 1, None, None, 1e-8, 10, None, None) == sem.SEM_ESTATE
+    assert L.sem_diag(None, None) == sem.SEM_ESTATE
     assert L.sem_launch_count(None) == -1
     L.sem_free(None)
     for c in range(6):
