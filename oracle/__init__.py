@@ -17,18 +17,20 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sem_oracle.c")
+_SRC_FD = os.path.join(_HERE, "fd_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 # Plain build: -O2, no -ffast-math, no FMA contraction (FP64 rounding order is
 # exactly the order written in the C source).
 GCC_CMD = ["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", "-ffp-contract=off",
-           "-fno-fast-math", _SRC, "-o", _LIB, "-lm"]
+           "-fno-fast-math", _SRC, _SRC_FD, "-o", _LIB, "-lm"]
 
 _lib = None
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
+            os.path.getmtime(_SRC), os.path.getmtime(_SRC_FD)):
         subprocess.check_call(GCC_CMD)
     return _LIB
 
@@ -51,12 +53,14 @@ def lib():
         L.ora_ax_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P, P]
         L.ora_cg_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P, P, P, P,
                                       ctypes.c_double, ctypes.c_int, P, P]
+        L.ora_fd_weights.argtypes = [ctypes.c_int, ctypes.c_double, P]
+        L.ora_fd_step.argtypes = [i64, i64, ctypes.c_int, P, ctypes.c_double, P, P, P]
         L.ora_diag_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P]
         L.ora_pcg_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P, P, ctypes.c_int, P, P,
                                        ctypes.c_double, ctypes.c_int, P, P]
         for f in (L.ora_gll, L.ora_deriv, L.ora_geom, L.ora_ax, L.ora_dssum,
                   L.ora_multiplicity, L.ora_cg, L.ora_ax_screened, L.ora_cg_screened,
-                  L.ora_diag_screened, L.ora_pcg_screened):
+                  L.ora_diag_screened, L.ora_pcg_screened, L.ora_fd_weights, L.ora_fd_step):
             f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -209,3 +213,26 @@ def mass_rhs(N: int, glo, dirichlet, J, f):
     bl = (J * w3[None, :]).reshape(-1) * np.asarray(f).reshape(-1)
     b = dssum(glo, bl)
     return b * (1.0 - np.asarray(dirichlet, dtype=np.float64).reshape(-1))
+
+
+# --- NEXT-4: the finite-difference wave-equation example ---
+def fd_weights(r: int, dx: float) -> np.ndarray:
+    """omega_{-r..r}: central second-derivative weights of order 2r / dx^2
+    (reading R6; the paper gives none)."""
+    w = np.zeros(2 * r + 1)
+    _check(lib().ora_fd_weights(int(r), float(dx), _p(w)), "ora_fd_weights")
+    return w
+
+
+def fd_step(u1: np.ndarray, u2: np.ndarray, weights: np.ndarray, dt: float) -> np.ndarray:
+    """u3 of lst:fdCode on the periodic h x w grid of u1."""
+    u1 = np.ascontiguousarray(u1, dtype=np.float64)
+    u2 = np.ascontiguousarray(u2, dtype=np.float64)
+    weights = np.ascontiguousarray(weights, dtype=np.float64)
+    h, w = u1.shape
+    assert u2.shape == u1.shape and weights.size % 2 == 1
+    r = weights.size // 2
+    u3 = np.zeros_like(u1)
+    _check(lib().ora_fd_step(w, h, r, _p(weights), float(dt), _p(u1), _p(u2), _p(u3)),
+           "ora_fd_step")
+    return u3
