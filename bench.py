@@ -51,6 +51,11 @@ def parse():
                     help="screened: -div(kappa grad u) + alpha u (NEXT-1) with meshgen.coefficients")
     ap.add_argument("--precond", choices=["none", "jacobi"], default="none",
                     help="jacobi: Jacobi-preconditioned CG (NEXT-2, sem_pcg)")
+    ap.add_argument("--workload", choices=["sem", "fd"], default="sem",
+                    help="fd: the finite-difference wave step of lst:fdCode (NEXT-4), "
+                         "MNodes/s over stencil sizes 3..15")
+    ap.add_argument("--fd-size", type=int, default=8192, help="fd grid is size x size")
+    ap.add_argument("--fd-radii", type=int, nargs="+", default=[1, 2, 3, 4, 5, 6, 7])
     ap.add_argument("--cpu-its", type=int, default=100,
                     help="oracle CG iterations timed for cpu_baseline (bounded sample)")
     ap.add_argument("--ref-its", type=int, default=3,
@@ -214,6 +219,102 @@ def run_reference(args, rank, world):
     print(json.dumps(out), flush=True)
 
 
+FD_METRIC = "FD wave step MNodes/s vs stencil size (lst:fdCode), % of HBM roofline"
+
+
+def run_fd(args, rank, world):
+    """NEXT-4: fd2d_run over `steps` time steps of a size x size periodic grid
+    per GPU (weak scaling: independent replicas, the stencil does not shard
+    across this API), each stencil radius in --fd-radii; CUDA events on the
+    launching stream, L2 flushed by the working set (3 x 512 MiB > L2)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1403_0968_b200 import fd
+
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = args.fd_size
+    rng = np.random.default_rng(1 + rank)
+    u1 = torch.from_numpy(rng.uniform(-1, 1, (n, n))).to(dev)
+    u2 = torch.from_numpy(rng.uniform(-1, 1, (n, n))).to(dev)
+    u3 = torch.empty_like(u1)
+    stream = torch.cuda.current_stream()
+    peak, peak_src = peaks()
+    sweep = {}
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    for r in args.fd_radii:
+        om = fd.weights(r, 2.0 / n)
+        dt = 0.2 * 2.0 / n
+        fd.run(u1, u2, u3, om, dt, max(args.warmup, 3))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fd.run(u1, u2, u3, om, dt, args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        nodes = float(n) * n * args.steps * world
+        sweep[2 * r + 1] = {"mnodes_s": nodes / (ms * 1e-3) / 1e6, "us_per_step": 1e3 * ms / args.steps,
+                            "achieved_gbs": 24.0 * n * n / (ms / args.steps * 1e-3) / 1e9}
+        # input data was rotated: refresh so every radius starts from finite values
+        u1.uniform_(-1, 1)
+        u2.uniform_(-1, 1)
+    clocks = sampler.stop()
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        import oracle
+        m = 2048
+        a, b = rng.uniform(-1, 1, (m, m)), rng.uniform(-1, 1, (m, m))
+        r = args.fd_radii[-1]
+        om = oracle.fd_weights(r, 2.0 / m)
+        t0 = time.perf_counter()
+        reps = 3
+        for _ in range(reps):
+            oracle.fd_step(a, b, om, 0.1 / m)
+        tc = (time.perf_counter() - t0) / reps
+        cpu = {"value": m * m / tc / 1e6, "unit": "MNodes/s", "cores": 1, "kind": "oracle",
+               "cpu": cpu_info(),
+               "sample": f"plain-C oracle ora_fd_step, {m}x{m} grid, stencil size {2 * r + 1}, "
+                         f"{reps} steps, 1 thread, {tc * reps:.1f} s"}
+    if rank == 0:
+        rmax = 2 * args.fd_radii[-1] + 1
+        head = sweep[rmax]
+        out = {"metric": FD_METRIC, "value": head["mnodes_s"], "unit": "MNodes/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": head["us_per_step"] / 1e3, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic (seeded U(-1,1) fields)",
+               "config": {"workload": f"fd2d (lst:fdCode) {n}x{n} periodic grid per GPU, stencil "
+                                      f"size {rmax} (headline) and the sweep 3..15",
+                          "grid": [n, n], "stencil_size": rmax,
+                          "l2": "inputs larger than L2: 3 x 512 MiB fields"},
+               "sweep": {str(k): v for k, v in sweep.items()},
+               "roofline": {"bound": "hbm", "kernel": f"fd2d_kernel<{args.fd_radii[-1]}>",
+                            "achieved": head["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                            "frac": head["achieved_gbs"] / peak, "traffic": None,
+                            "peak_source": peak_src,
+                            "bytes_per_node": "24 (u1, u2 read; u3 written)",
+                            "timing": "CUDA events around fd2d_run(steps) on the launching stream"},
+               "gpu_launches": args.steps * len(args.fd_radii),
+               "cpu_baseline": cpu, "clocks": clocks}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -221,6 +322,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.workload == "fd":
+        run_fd(args, rank, world)
         return
     import numpy as np
     import torch

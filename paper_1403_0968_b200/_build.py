@@ -11,7 +11,7 @@ CSRC = os.path.join(PKG, "csrc")
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libsem.so")
 SOURCES = ["sem_kernels.cu", "ax_tma.cu", "ax_tma_mass.cu", "ax_tma_pc.cu", "cg_update.cu", "sem_host.cpp",
-           "sem_comm.cu"]
+           "sem_comm.cu", "fd2d.cu"]
 HEADERS = ["sem_internal.h", "sem_comm.h", "cg_device.cuh", "ax_tma.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -32,6 +32,7 @@ def needs_build() -> bool:
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "sem.h"))
+    deps.append(os.path.join(ROOT, "include", "fd.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps)
 

@@ -249,22 +249,25 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
         for (int v = 0; v < NV; ++v) bulk_g2s(sb + v * VL, vsrc[v] + vr.a0, vb, gbar + s, pol_v);
     };
 
+    // ---- the scalar loads of this iteration go out first (small, L2-resident:
+    // ahead of the bulk copies in the memory queues), then the geometric
+    // factors and the vectors produced by the previous kernels; the scalars
+    // are reduced while all those copies are in flight ----
+    K1Pre<PC> pre;
+    if constexpr (CG) {
+        pdl_wait();
+        cg_k1_load<Lo::NT, PC>(a.st, a.red, pre);
+    }
     if (leader) {
         if (u0 < nunits) issue_G(u0, 0);
         if (u0 + TG < nunits) issue_G(u0 + TG, 1);
-    }
-
-    // ---- the vectors (produced by the previous kernels) follow; the scalars
-    // of this iteration are reduced while all those copies are in flight ----
-    if constexpr (CG) pdl_wait();
-    if (leader) {
         if (u0 < nunits) issue_V(u0, 0);
         if (u0 + TG < nunits) issue_V(u0 + TG, 1);
     }
     double beta = 0.0, alpha_prev = 0.0;
     int kit = 0;
     if constexpr (CG) {
-        const CgStep c = cg_k1_prologue_t<Lo::NT, PC>(a.st, a.red, sred);
+        const CgStep c = cg_k1_finish<Lo::NT, PC>(a.st, sred, pre);
         if (c.done) {
             // drain the copies already in flight, then leave
             if (leader) {
@@ -499,17 +502,21 @@ __global__ void __launch_bounds__(HiCfg<N, CG>::NT, 1) ax_hi_kernel(TmaArgs a) {
         mbar_arrive(vbar + s);
         for (int v = 0; v < NV; ++v) bulk_g2s(sb + v * VL, vsrc[v] + vr.a0, vb, vbar + s, pol_v);
     };
-    if (leader)
-        for (int64_t gs = 0; gs < R && gs < nsl; ++gs) issue_slice(gs);   // static data first
-    if constexpr (CG) pdl_wait();
+    // scalar loads first (see ax_tma_kernel), then G^ slices and vectors
+    K1Pre<PC> pre;
+    if constexpr (CG) {
+        pdl_wait();
+        cg_k1_load<C::NT, PC>(a.st, a.red, pre);
+    }
     if (leader) {
+        for (int64_t gs = 0; gs < R && gs < nsl; ++gs) issue_slice(gs);
         if (nel > 0) issue_vec(e0, 0);
         if (nel > 1) issue_vec(e0 + TG, 1);
     }
     double beta = 0.0, alpha_prev = 0.0;
     int kit = 0;
     if constexpr (CG) {
-        const CgStep c = cg_k1_prologue_t<C::NT, PC>(a.st, a.red, sred);
+        const CgStep c = cg_k1_finish<C::NT, PC>(a.st, sred, pre);
         if (c.done) {
             if (leader) {       // drain everything in flight
                 for (int64_t gs = 0; gs < R && gs < nsl; ++gs) mbar_wait(gbar + gs, 0);

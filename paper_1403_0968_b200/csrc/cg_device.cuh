@@ -195,31 +195,96 @@ __device__ __forceinline__ void rho_src_t(const CgRed &R, int k, const double *&
     }
 }
 
-// K1 prologue (all threads of the block; contains __syncthreads): k, the
-// stopping decision, beta_k and alpha_{k-1}.  Block 0 records a stop for the
-// host (iters, rel_res, alpha_{it-1} for the final x update, the sticky flag)
-// and, at k = 0, rr_0.  PC: rho = (r,z) drives alpha / beta, rr = (r,r) the stop.
+// One thread's share of an ordered partial sum (the per-thread part of
+// block_sums: PER strided values, then the tail).
+template <int NT>
+__device__ __forceinline__ double thread_sum(const double *src, int cnt) {
+    constexpr int PER = 8;
+    double v[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const int t = threadIdx.x + u * NT;
+        v[u] = (t < cnt) ? __ldcg(src + t) : 0.0;
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) s += v[u];
+    for (int t = threadIdx.x + PER * NT; t < cnt; t += NT) s += __ldcg(src + t);
+    return s;
+}
+
+// The scalars' sources of iteration k.  One rank: the partial slots are
+// selected by the parity of k, which is itself read from the state, so both
+// parities are summed speculatively in the SAME round trip as the state
+// loads (the slot of the wrong parity may be written concurrently by this
+// very kernel's blocks; its sum is discarded) -- one memory round trip
+// instead of two.  Several ranks: the all-gathered rank values, after k.
+// K1 prologue (all threads of the block): k, the stopping decision, beta_k
+// and alpha_{k-1}.  Block 0 records a stop for the host (iters, rel_res,
+// alpha_{it-1} for the final x update, the sticky flag) and, at k = 0, rr_0.
+// PC: rho = (r,z) drives alpha / beta, rr = (r,r) the stop.  Only K1 takes the
+// stopping decision (K2 follows the sticky flag).  Split in two so a kernel can
+// issue the scalar loads BEFORE its bulk copies (they would otherwise queue
+// behind them: ncu r01g put 25% of K1's stall samples in the prologue):
+//   cg_k1_load    state + partial loads, per-thread partial sums (no barrier)
+//   cg_k1_finish  block reduction (__syncthreads), decisions, state writes
+template <bool PC>
+struct K1Pre {
+    static constexpr int NS = PC ? 4 : 3;
+    int done, k;
+    double v[NS];
+};
+
 template <int NT, bool PC>
-__device__ __forceinline__ CgStep cg_k1_prologue_t(CgState *st, const CgRed &R, double *red) {
+__device__ __forceinline__ void cg_k1_load(CgState *st, const CgRed &R, K1Pre<PC> &P) {
+    constexpr int NS = K1Pre<PC>::NS;
+    if (R.nranks == 1) {
+        // rho sources: part2 ((r,r)) or part3 ((r,z)); pap: part1
+        const double *prho = PC ? R.part2 + 2 * R.s2 : R.part2;
+        P.done = ld_state(&st->done);
+        P.k = ld_state(&st->k1);
+        const double r0 = thread_sum<NT>(prho, R.nb2), r1 = thread_sum<NT>(prho + R.s2, R.nb2);
+        const double q0 = thread_sum<NT>(R.part1, R.nb1), q1 = thread_sum<NT>(R.part1 + R.s1, R.nb1);
+        double rr0 = 0.0, rr1 = 0.0;
+        if constexpr (PC) {
+            rr0 = thread_sum<NT>(R.part2, R.nb2);
+            rr1 = thread_sum<NT>(R.part2 + R.s2, R.nb2);
+        }
+        const int k = P.k;
+        const bool odd = (k - 1) & 1;           // parity of the slots of rho_k, pap_{k-1}
+        P.v[0] = odd ? r1 : r0;                   // rho_k
+        P.v[1] = (k == 0) ? 0.0 : (odd ? r0 : r1);   // rho_{k-1}
+        P.v[2] = (k == 0) ? 0.0 : (odd ? q1 : q0);   // pap_{k-1}
+        if constexpr (PC) P.v[NS - 1] = odd ? rr1 : rr0;   // rr_k (stopping norm)
+    } else {
+        P.done = ld_state(&st->done);
+        P.k = ld_state(&st->k1);
+        const int k = P.k;
+        const double *src[NS];
+        int cnt[NS];
+        rho_src_t<PC>(R, k, src[0], cnt[0]);     // rho_k
+        rho_src_t<PC>(R, k - 1, src[1], cnt[1]); // rho_{k-1}
+        pap_src(R, k - 1, src[2], cnt[2]);       // pap_{k-1}
+        if (k == 0) cnt[1] = cnt[2] = 0;
+        if constexpr (PC) rr_src(R, k, src[NS - 1], cnt[NS - 1]);   // rr_k (stopping norm)
+#pragma unroll
+        for (int q = 0; q < NS; ++q) P.v[q] = thread_sum<NT>(src[q], cnt[q]);
+    }
+}
+
+template <int NT, bool PC>
+__device__ __forceinline__ CgStep cg_k1_finish(CgState *st, double *red, K1Pre<PC> &P) {
+    constexpr int NS = K1Pre<PC>::NS;
     CgStep c{};
-    const int done = ld_state(&st->done);
-    const int k = ld_state(&st->k1);
+    const int k = P.k;
     c.k = k;
-    if (done) {
+    if (P.done) {
         c.done = true;
         return c;
     }
-    constexpr int NS = PC ? 4 : 3;
-    const double *src[NS];
-    int cnt[NS];
-    rho_src_t<PC>(R, k, src[0], cnt[0]);     // rho_k
-    rho_src_t<PC>(R, k - 1, src[1], cnt[1]); // rho_{k-1}
-    pap_src(R, k - 1, src[2], cnt[2]);       // pap_{k-1}
-    if (k == 0) cnt[1] = cnt[2] = 0;
-    if constexpr (PC) rr_src(R, k, src[NS - 1], cnt[NS - 1]);   // rr_k (stopping norm)
-    double v[NS];
-    block_sums<NT, NS>(src, cnt, v, red);
-    const double rho = v[0], rho_m1 = v[1], pap_m1 = v[2], rr = v[NS - 1 - (PC ? 0 : 2)];
+    block_sum_vec<NT, NS>(P.v, red);
+    const double rho = P.v[0], rho_m1 = P.v[1], pap_m1 = P.v[2];
+    const double rr = P.v[NS - 1 - (PC ? 0 : 2)];
     const double rho0 = (k == 0) ? rr : __ldcg(&st->rho0);
     const double alpha_prev = (k == 0) ? 0.0 : rho_m1 / pap_m1;
     c.beta = (k == 0) ? 0.0 : rho / rho_m1;
@@ -240,6 +305,13 @@ __device__ __forceinline__ CgStep cg_k1_prologue_t(CgState *st, const CgRed &R, 
     return c;
 }
 
+template <int NT, bool PC>
+__device__ __forceinline__ CgStep cg_k1_prologue_t(CgState *st, const CgRed &R, double *red) {
+    K1Pre<PC> P;
+    cg_k1_load<NT, PC>(st, R, P);
+    return cg_k1_finish<NT, PC>(st, red, P);
+}
+
 // The PCG prologue is kept out of line so the CG kernels' main loops compile
 // exactly as without a preconditioner (K1's register allocation is sensitive).
 template <int NT>
@@ -253,32 +325,42 @@ __device__ __forceinline__ CgStep cg_k1_prologue(CgState *st, const CgRed &R, do
     return cg_k1_prologue_t<NT, false>(st, R, red);
 }
 
-// K2 prologue (all threads): k, the same stopping decision, alpha_k.  K2 is
-// instantiated per preconditioner (k2_kernel<N, INIT, PC>).
+// K2 prologue (all threads): k and alpha_k = rho_k / pap_k.  The stopping
+// decision of iteration k was taken by K1(k) (sticky flag): K2 only follows
+// it, so the two kernels can never disagree.  K2 is instantiated per
+// preconditioner (k2_kernel<N, INIT, PC>).
 template <int NT, bool PC>
 __device__ __forceinline__ CgStep cg_k2_prologue(CgState *st, const CgRed &R, double *red,
                                                  double &alpha) {
     CgStep c{};
-    const int done = ld_state(&st->done);
-    const int k = ld_state(&st->k2);
+    double v[2];
+    int done, k;
+    if (R.nranks == 1) {
+        const double *prho = PC ? R.part2 + 2 * R.s2 : R.part2;
+        done = ld_state(&st->done);
+        k = ld_state(&st->k2);
+        const double r0 = thread_sum<NT>(prho, R.nb2), r1 = thread_sum<NT>(prho + R.s2, R.nb2);
+        const double q0 = thread_sum<NT>(R.part1, R.nb1), q1 = thread_sum<NT>(R.part1 + R.s1, R.nb1);
+        v[0] = ((k - 1) & 1) ? r1 : r0;          // rho_k
+        v[1] = (k & 1) ? q1 : q0;                // pap_k
+    } else {
+        done = ld_state(&st->done);
+        k = ld_state(&st->k2);
+        const double *src[2];
+        int cnt[2];
+        rho_src_t<PC>(R, k, src[0], cnt[0]);     // rho_k
+        pap_src(R, k, src[1], cnt[1]);           // pap_k
+        v[0] = thread_sum<NT>(src[0], cnt[0]);
+        v[1] = thread_sum<NT>(src[1], cnt[1]);
+    }
     c.k = k;
     if (done) {
         c.done = true;
         return c;
     }
-    constexpr int NS = PC ? 3 : 2;
-    const double *src[NS];
-    int cnt[NS];
-    rho_src_t<PC>(R, k, src[0], cnt[0]);     // rho_k
-    pap_src(R, k, src[1], cnt[1]);           // pap_k
-    if constexpr (PC) rr_src(R, k, src[2], cnt[2]);   // rr_k (stopping norm)
-    double v[NS];
-    block_sums<NT, NS>(src, cnt, v, red);
-    const double rr = PC ? v[NS - 1] : v[0];
-    const double rho0 = (k == 0) ? rr : __ldcg(&st->rho0);
-    c.done = cg_stop(k, rr, rho0, st->maxit, st->tol);
+    block_sum_vec<NT, 2>(v, red);
     alpha = v[0] / v[1];
-    if (blockIdx.x == 0 && threadIdx.x == 0 && !c.done) st->k1 = k + 1;   // for K1 of k+1
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->k1 = k + 1;   // for K1 of k+1
     return c;
 }
 

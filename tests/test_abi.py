@@ -20,7 +20,7 @@ def declared_functions():
             continue
         src = open(os.path.join(ROOT, "include", fn)).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-        for mm in re.finditer(r"^[A-Za-z_][\w\s\*]*?\b(sem_\w+)\s*\(", src, flags=re.M):
+        for mm in re.finditer(r"^[A-Za-z_][\w\s\*]*?\b((?:sem|fd|fd2d)_\w+)\s*\(", src, flags=re.M):
             names.add(mm.group(1))
     return names
 
@@ -37,6 +37,7 @@ def test_exports_every_declared_symbol(L):
     assert {"sem_setup", "sem_ax", "sem_dssum", "sem_cg", "sem_mask", "sem_free"} <= names
     for nm in sorted(names):
         assert hasattr(L, nm), f"libsem.so does not export {nm}"
+    assert {"fd_weights", "fd2d_step", "fd2d_run"} <= names
     assert set(sem.EXPORTS) >= names
     assert b"sm_100a" in L.sem_version()
 
@@ -177,3 +178,24 @@ def test_no_cpu_fallback_without_gpu(L):
     m = meshgen.box_mesh(N, xi, elems=(1, 1, 1))
     with pytest.raises(Exception):
         sem.Context(m, N, device=0)
+
+
+def test_fd_host_calls(L, oracle):
+    """fd.h host side: the library's own weights (Fornberg) agree with the
+    oracle's closed form; bad arguments are rejected before any GPU work."""
+    from paper_1403_0968_b200 import fd
+    for r in range(1, 8):
+        for dx in (1.0, 0.003):
+            np.testing.assert_allclose(fd.weights(r, dx), oracle.fd_weights(r, dx), rtol=1e-12,
+                                       atol=1e-13 / dx ** 2)
+    om = (ctypes.c_double * 3)(1.0, -2.0, 1.0)
+    p = ctypes.c_void_p(256)
+    assert L.fd2d_step(p, ctypes.c_void_p(512), ctypes.c_void_p(768), 16, 16, 0, om, 0.1,
+                       None) == sem.SEM_EINVAL          # r = 0
+    assert L.fd2d_step(p, ctypes.c_void_p(512), ctypes.c_void_p(768), 2, 16, 1, om, 0.1,
+                       None) == sem.SEM_EINVAL          # w < 2r+1
+    assert L.fd2d_step(p, p, ctypes.c_void_p(768), 16, 16, 1, om, 0.1,
+                       None) == sem.SEM_EINVAL          # aliasing
+    assert L.fd2d_step(ctypes.c_void_p(264), ctypes.c_void_p(512), ctypes.c_void_p(768), 16, 16,
+                       1, om, 0.1, None) == sem.SEM_EINVAL   # misaligned
+    assert L.fd_weights(0, 1.0, om) == sem.SEM_EINVAL

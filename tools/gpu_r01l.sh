@@ -1,0 +1,18 @@
+# round 1 (l): FD paired copies + symmetric weights; K1 scalar loads before bulk copies
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke_r01l.log 2>&1; tail -1 gpurun_out/smoke_r01l.log
+timeout 900 python -m pytest tests/test_gpu_fd.py -x -q > gpurun_out/pytest_fd_r01l.log 2>&1; tail -3 gpurun_out/pytest_fd_r01l.log
+timeout 600 python bench.py --workload fd --steps 20 > gpurun_out/bench_fd_r01l.json 2> gpurun_out/bench_fd_r01l.err; tail -2 gpurun_out/bench_fd_r01l.err
+python -c "
+import json; d=json.loads(open('gpurun_out/bench_fd_r01l.json').read().strip().splitlines()[-1])
+print(d['value'], d['roofline']['frac'], {k:(round(v['mnodes_s']),round(v['achieved_gbs'])) for k,v in d['sweep'].items()})"
+for i in 1 2; do
+timeout 300 python bench.py --steps 10 --no-cpu-baseline > gpurun_out/bench_r01l_$i.json 2> gpurun_out/bench_r01l.err
+python -c "
+import json; d=json.loads(open('gpurun_out/bench_r01l_$i.json').read().strip().splitlines()[-1]); r=d['roofline']
+print(d['value'], r['avg_launch_us'], r['iteration']['us'], r['step_share'])"
+done
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_r01l.log 2>&1; tail -2 gpurun_out/pytest_gpu_r01l.log
+ncu --set full --clock-control none --import-source on -k regex:fd2d_kernel -s 3 -c 1 -o gpurun_out/prof_fd_r01l python bench.py --workload fd --steps 3 --warmup 3 --fd-radii 7 --no-cpu-baseline > gpurun_out/ncu_fd.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:ax_tma_kernel -s 10 -c 1 -o gpurun_out/prof_k1_r01l python bench.py --steps 1 --warmup 1 --no-cpu-baseline --ax-reps 5 > gpurun_out/ncu_k1l.log 2>&1
+ls gpurun_out/*r01l*.ncu-rep
