@@ -195,7 +195,8 @@ int sem_profile(sem_ctx *ctx, int enable);
 
 /* Benchmark helper (one rank): enqueue, as ONE CUDA graph on the context
  * stream, `reps` back-to-back launches of one kernel of the CG iteration on the
- * context's internal work vectors (which = 1: K1, 2: K2, 0: the Ax kernel),
+ * context's internal work vectors (which = 1: K1, 2: K2, 0: the Ax kernel,
+ * 3: the Ax kernel followed by the sem_dssum gather-scatter, config c2),
  * from a mid-solve state, so the caller can time the kernel with CUDA events
  * around the call.  The caller's vectors are untouched; the internal CG state
  * is left undefined until the next sem_cg.  Asynchronous. */

@@ -53,6 +53,8 @@ def lib():
         L.ora_ax_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P, P]
         L.ora_cg_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P, P, P, P,
                                       ctypes.c_double, ctypes.c_int, P, P]
+        L.ora_cg_cgs.argtypes = [ctypes.c_int, i64, P, P, P, P, P, ctypes.c_double, ctypes.c_int,
+                                 P, P]
         L.ora_fd_weights.argtypes = [ctypes.c_int, ctypes.c_double, P]
         L.ora_fd_step.argtypes = [i64, i64, ctypes.c_int, P, ctypes.c_double, P, P, P]
         L.ora_diag_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P]
@@ -60,7 +62,7 @@ def lib():
                                        ctypes.c_double, ctypes.c_int, P, P]
         for f in (L.ora_gll, L.ora_deriv, L.ora_geom, L.ora_ax, L.ora_dssum,
                   L.ora_multiplicity, L.ora_cg, L.ora_ax_screened, L.ora_cg_screened,
-                  L.ora_diag_screened, L.ora_pcg_screened, L.ora_fd_weights, L.ora_fd_step):
+                  L.ora_diag_screened, L.ora_pcg_screened, L.ora_fd_weights, L.ora_fd_step, L.ora_cg_cgs):
             f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -200,6 +202,25 @@ def cg(N: int, glo, dirichlet, G, b, x0=None, tol=1e-8, maxit=1000, J=None, kapp
                                     ctypes.byref(iters), ctypes.byref(rel))
     if rc not in (0, 4):
         raise OracleError(f"ora_cg failed with status {rc}")
+    return x, iters.value, rel.value, rc
+
+
+def cg_single_reduction(N: int, glo, dirichlet, G, b, x0=None, tol=1e-8, maxit=1000):
+    """NEXT-3: Chronopoulos-Gear single-reduction CG (reading R7), Poisson
+    operator, identity preconditioner.  Returns (x, iters, rel_res, status)."""
+    n3 = (N + 1) ** 3
+    glo = np.ascontiguousarray(glo, dtype=np.int64).reshape(-1)
+    dirichlet = np.ascontiguousarray(dirichlet, dtype=np.uint8).reshape(-1)
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
+    E = glo.size // n3
+    x = np.zeros(E * n3) if x0 is None else np.array(x0, dtype=np.float64).reshape(-1).copy()
+    iters = ctypes.c_int(0)
+    rel = ctypes.c_double(0.0)
+    rc = lib().ora_cg_cgs(N, E, _p(glo), _p(dirichlet), _p(G), _p(b), _p(x), float(tol), int(maxit),
+                          ctypes.byref(iters), ctypes.byref(rel))
+    if rc not in (0, 4):
+        raise OracleError(f"ora_cg_cgs failed with status {rc}")
     return x, iters.value, rel.value, rc
 
 

@@ -486,6 +486,93 @@ int ora_pcg_screened(int N, int64_t E, const int64_t *glo, const uint8_t *dirich
     return status;
 }
 
+/* NEXT-3: the single-reduction CG of Chronopoulos and Gear
+ * (1989), a latency-hiding variant of the PCG of PAPER.md:672-673 (reading R7):
+ * the operator is applied to the residual, A p is carried by the recurrence
+ * s = w + beta s, and both inner products of an iteration, gamma = (r,u)_c and
+ * delta = (w,u)_c, come from the same vectors (one reduction point):
+ *   r = mask (b - Q Q^T A_L x0); u = r; w = mask Q Q^T A_L u
+ *   gamma = (r,u)_c; delta = (w,u)_c; rr0 = (r,r)_c; k = 0
+ *   while k < maxit and sqrt((r,r)_c) > tol sqrt(rr0):           (G9)
+ *     if k == 0: beta = 0; alpha = gamma / delta
+ *     else:      beta = gamma / gamma_old; alpha = gamma / (delta - beta gamma / alpha_old)
+ *     p = u + beta p;  s = w + beta s;  x += alpha p;  r -= alpha s
+ *     u = r;  w = mask Q Q^T A_L u
+ *     gamma_old = gamma; alpha_old = alpha; gamma = (r,u)_c; delta = (w,u)_c; k += 1
+ * (identity preconditioner: u = r, gamma = (r,r)_c).  Returns as ora_cg.      */
+int ora_cg_cgs(int N, int64_t E, const int64_t *glo, const uint8_t *dirichlet, const double *G,
+               const double *b, double *x, double tol, int maxit, int *iters, double *rel_res)
+{
+    if (N < 1 || N > 32 || E < 0 || maxit < 0 || !(tol >= 0.0)) return ORA_EINVAL;
+    const ora_coef cf = {NULL, NULL, NULL};
+    int64_t L = E * (N + 1) * (N + 1) * (N + 1);
+    double *mask = (double *)malloc(sizeof(double) * (L + 1));
+    double *c = (double *)malloc(sizeof(double) * (L + 1));
+    double *r = (double *)malloc(sizeof(double) * (L + 1));
+    double *u = (double *)malloc(sizeof(double) * (L + 1));
+    double *w = (double *)malloc(sizeof(double) * (L + 1));
+    double *p = (double *)malloc(sizeof(double) * (L + 1));
+    double *sv = (double *)malloc(sizeof(double) * (L + 1));
+    int64_t *order = sorted_order(L, glo);
+    for (int64_t l = 0; l < L; ++l) {
+        mask[l] = dirichlet[l] ? 0.0 : 1.0;
+        c[l] = 1.0;
+    }
+    dssum_sorted(L, glo, order, c);
+    for (int64_t l = 0; l < L; ++l) c[l] = mask[l] / c[l];
+
+    apply_op(N, E, G, &cf, glo, order, mask, x, w);   /* w = mask QQ^T A_L x0 */
+    for (int64_t l = 0; l < L; ++l) r[l] = mask[l] * b[l] - w[l];
+    for (int64_t l = 0; l < L; ++l) u[l] = r[l];
+    apply_op(N, E, G, &cf, glo, order, mask, u, w);   /* w = mask QQ^T A_L u */
+    for (int64_t l = 0; l < L; ++l) p[l] = 0.0;
+    for (int64_t l = 0; l < L; ++l) sv[l] = 0.0;
+    double gamma = dot_c(L, c, r, u), delta = dot_c(L, c, w, u);
+    double rr = dot_c(L, c, r, r), rr0 = rr;
+    double gamma_old = 0.0, alpha_old = 0.0;
+    int k = 0;
+    int status = ORA_OK;
+    if (rr0 == 0.0) {
+        *iters = 0;
+        *rel_res = 0.0;
+    } else {
+        while (k < maxit && sqrt(rr) > tol * sqrt(rr0)) {
+            double beta, alpha;
+            if (k == 0) {
+                beta = 0.0;
+                alpha = gamma / delta;
+            } else {
+                beta = gamma / gamma_old;
+                alpha = gamma / (delta - beta * gamma / alpha_old);
+            }
+            for (int64_t l = 0; l < L; ++l) p[l] = u[l] + beta * p[l];
+            for (int64_t l = 0; l < L; ++l) sv[l] = w[l] + beta * sv[l];
+            for (int64_t l = 0; l < L; ++l) x[l] += alpha * p[l];
+            for (int64_t l = 0; l < L; ++l) r[l] -= alpha * sv[l];
+            for (int64_t l = 0; l < L; ++l) u[l] = r[l];
+            apply_op(N, E, G, &cf, glo, order, mask, u, w);
+            gamma_old = gamma;
+            alpha_old = alpha;
+            gamma = dot_c(L, c, r, u);
+            delta = dot_c(L, c, w, u);
+            rr = dot_c(L, c, r, r);
+            k += 1;
+        }
+        *iters = k;
+        *rel_res = sqrt(rr) / sqrt(rr0);
+        if (tol > 0.0 && sqrt(rr) > tol * sqrt(rr0)) status = ORA_ENOCONV;
+    }
+    free(mask);
+    free(c);
+    free(r);
+    free(u);
+    free(w);
+    free(p);
+    free(sv);
+    free(order);
+    return status;
+}
+
 /* CG on the screened-Coulomb operator (NEXT-1): O7, the identity-preconditioned
  * case of ora_pcg_screened.  ora_cg is the Poisson case. */
 int ora_cg_screened(int N, int64_t E, const int64_t *glo, const uint8_t *dirichlet,

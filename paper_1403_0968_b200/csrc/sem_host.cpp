@@ -974,8 +974,9 @@ static int cg_impl(sem_ctx *ctx, int precond, const double *b, double *x, double
 // ---------------------------------------------------------------------------
 extern "C" int sem_kernel_replay(sem_ctx *ctx, int which, int reps) {
     CHECK_CTX();
-    if (reps < 1 || (which != 1 && which != 2 && which != 0))
-        return fail(ctx, SEM_EINVAL, "sem_kernel_replay: which in {0,1,2}, reps >= 1");
+    if (reps < 1 || which < 0 || which > 3)
+        return fail(ctx, SEM_EINVAL, "sem_kernel_replay: which in {0,1,2,3}, reps >= 1");
+    if (which == 3 && ctx->nranks != 1) return fail(ctx, SEM_EINVAL, "sem_kernel_replay: single rank only");
     if (ctx->nranks != 1) return fail(ctx, SEM_EINVAL, "sem_kernel_replay: single rank only");
     cudaStream_t s = ctx->stream;
     CgVecs &v = ctx->cv;
@@ -998,6 +999,10 @@ extern "C" int sem_kernel_replay(sem_ctx *ctx, int which, int reps) {
     for (int q = 0; q < reps && e == cudaSuccess; ++q) {
         if (which == 1) e = launch_ax_cg(ctx->dm, v, ctx->cap_stream);
         else if (which == 2) e = launch_k2(ctx->dm, v, false, ctx->cap_stream);
+        else if (which == 3) {     // sem_ax then sem_dssum (config c2)
+            e = launch_ax(ctx->dm, v.r, v.w, ctx->cap_stream);
+            if (e == cudaSuccess) e = launch_gs(ctx->dm, v.w, 0, nullptr, ctx->cap_stream);
+        }
         else e = launch_ax(ctx->dm, v.r, v.w, ctx->cap_stream);
     }
     cudaGraph_t g = nullptr;
@@ -1015,7 +1020,7 @@ extern "C" int sem_kernel_replay(sem_ctx *ctx, int which, int reps) {
     cudaGraphDestroy(g);
     CU(e);
     CU(cudaGraphLaunch(ctx->replay_exec, s));
-    ctx->launches += reps;
+    ctx->launches += (which == 3 ? 2 : 1) * int64_t(reps);
     return SEM_OK;
 }
 

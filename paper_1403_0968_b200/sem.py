@@ -271,7 +271,7 @@ class Context:
             out[nm] = (ms.value, n.value, by.value)
         return out
 
-    KERNELS = {"ax": 0, "k1": 1, "k2": 2}
+    KERNELS = {"ax": 0, "k1": 1, "k2": 2, "ax+dssum": 3}
 
     def kernel_replay(self, which: str, reps: int):
         """Enqueue `reps` back-to-back launches of one CG kernel as one graph on

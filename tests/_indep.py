@@ -147,3 +147,35 @@ def dense_pcg(K, b, minv, tol, maxit):
         rr = r @ r
         k += 1
     return x, k
+
+
+def dense_cg_single_reduction(K, b, tol, maxit):
+    """Textbook Chronopoulos-Gear CG on a dense SPD matrix (same stopping
+    rule on r.r as the oracle's reading G9)."""
+    x = np.zeros_like(b)
+    r = b.copy()
+    u = r.copy()
+    w = K @ u
+    gamma, delta = r @ u, w @ u
+    rr0 = r @ r
+    rr = rr0
+    p = np.zeros_like(b)
+    s = np.zeros_like(b)
+    k = 0
+    gamma_old = alpha_old = 0.0
+    while k < maxit and np.sqrt(rr) > tol * np.sqrt(rr0):
+        if k == 0:
+            beta, alpha = 0.0, gamma / delta
+        else:
+            beta = gamma / gamma_old
+            alpha = gamma / (delta - beta * gamma / alpha_old)
+        p = u + beta * p
+        s = w + beta * s
+        x = x + alpha * p
+        r = r - alpha * s
+        u = r.copy()
+        w = K @ u
+        gamma_old, alpha_old = gamma, alpha
+        gamma, delta, rr = r @ u, w @ u, r @ r
+        k += 1
+    return x, k
