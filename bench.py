@@ -51,6 +51,8 @@ def parse():
                     help="screened: -div(kappa grad u) + alpha u (NEXT-1) with meshgen.coefficients")
     ap.add_argument("--precond", choices=["none", "jacobi"], default="none",
                     help="jacobi: Jacobi-preconditioned CG (NEXT-2, sem_pcg)")
+    ap.add_argument("--cg-variant", choices=["standard", "single_reduction"], default="standard",
+                    help="single_reduction: Chronopoulos-Gear CG (NEXT-3, sem_cg_sr)")
     ap.add_argument("--workload", choices=["sem", "fd"], default="sem",
                     help="fd: the finite-difference wave step of lst:fdCode (NEXT-4), "
                          "MNodes/s over stencil sizes 3..15")
@@ -167,6 +169,8 @@ def workload_name(args, world):
     op = ("" if args.operator == "poisson" else
           ", screened Coulomb -div(kappa grad u) + alpha u (meshgen.coefficients)")
     cg = "CG" if args.precond == "none" else "Jacobi PCG"
+    if args.cg_variant != "standard":
+        cg = "single-reduction (Chronopoulos-Gear) CG"
     return (f"c3/c5: {E} hex elements ({'x'.join(map(str, args.elems))}) of order N={args.N} "
             f"per GPU, eps={args.eps} deformed box, full {cg} to {args.tol:g} from x0=0{op}")
 
@@ -191,8 +195,11 @@ def oracle_sample(args, its_per_call, calls):
     times = []
     for _ in range(calls):
         t0 = time.perf_counter()
-        oracle.cg(args.N, m.glo, m.dirichlet, G, b, tol=0.0, maxit=its_per_call,
-                  precond=args.precond, **co)
+        if args.cg_variant == "single_reduction":
+            oracle.cg_single_reduction(args.N, m.glo, m.dirichlet, G, b, tol=0.0, maxit=its_per_call)
+        else:
+            oracle.cg(args.N, m.glo, m.dirichlet, G, b, tol=0.0, maxit=its_per_call,
+                      precond=args.precond, **co)
         times.append(time.perf_counter() - t0)
     return times, m.nlocal
 
@@ -369,7 +376,8 @@ def main():
     its = None
     for _ in range(max(args.warmup, 1)):
         x.zero_()
-        _, its, rel, ok = ctx.cg(b, x, tol=args.tol, maxit=args.maxit, precond=args.precond)
+        _, its, rel, ok = ctx.cg(b, x, tol=args.tol, maxit=args.maxit, precond=args.precond,
+                        variant=args.cg_variant)
     assert ok, f"CG did not converge: rel_res={rel}"
 
     # ---- timed region: K full CG solves, inputs resident in HBM ----
@@ -384,7 +392,8 @@ def main():
     iters = []
     for _ in range(args.steps):
         x.zero_()
-        _, it, rel, ok = ctx.cg(b, x, tol=args.tol, maxit=args.maxit, precond=args.precond)
+        _, it, rel, ok = ctx.cg(b, x, tol=args.tol, maxit=args.maxit, precond=args.precond,
+                        variant=args.cg_variant)
         iters.append(it)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -406,7 +415,8 @@ def main():
     p0.record(stream)
     for _ in range(prof_steps):
         x.zero_()
-        ctx.cg(b, x, tol=args.tol, maxit=args.maxit, precond=args.precond)
+        ctx.cg(b, x, tol=args.tol, maxit=args.maxit, precond=args.precond,
+                        variant=args.cg_variant)
     p1.record(stream)
     torch.cuda.synchronize()
     prof_ms = p0.elapsed_time(p1)
@@ -441,9 +451,20 @@ def main():
     traffic = ncu_traffic((f"ax_tma_kernel<{args.N}, true, false>", f"ax_tma_kernel<{args.N}, 1>")) \
         if alpha is None else None
     shares = {k: v[0] / prof_ms for k, v in prof.items() if v[1]}
+    # every CG kernel inside the solve (per-launch CUDA events, profiled pass):
+    # K2 reads the w K1 just wrote from L2, unlike its back-to-back replay
+    in_solve = {}
+    for name in ("k1", "k2"):
+        ms_, n_, by_ = prof[name]
+        if n_:
+            us_ = 1e3 * ms_ / n_
+            in_solve[name] = {"avg_launch_us": us_, "bytes_per_launch": by_ / n_,
+                              "achieved_gbs": by_ / n_ / (us_ * 1e-6) / 1e9,
+                              "frac": by_ / n_ / (us_ * 1e-6) / 1e9 / peak}
     # the work vectors were clobbered by the replays; the next solve re-inits
     x.zero_()
-    ctx.cg(b, x, tol=args.tol, maxit=args.maxit, precond=args.precond)
+    ctx.cg(b, x, tol=args.tol, maxit=args.maxit, precond=args.precond,
+                        variant=args.cg_variant)
 
     # ---- Ax alone on the same mesh (64 B/node), for the Ax GDOF/s metric ----
     u = torch.from_numpy(meshgen.random_field(L, 0)).to(dev)
@@ -478,7 +499,8 @@ def main():
     for _ in range(2):
         b_dev.copy_(b_host, non_blocking=True)
         x.zero_()
-        ctx.cg(b_dev, x, tol=args.tol, maxit=args.maxit, precond=args.precond)
+        ctx.cg(b_dev, x, tol=args.tol, maxit=args.maxit, precond=args.precond,
+                        variant=args.cg_variant)
         x_host.copy_(x, non_blocking=True)
     barrier()
     torch.cuda.synchronize()
@@ -489,7 +511,8 @@ def main():
     for _ in range(e2e_steps):
         b_dev.copy_(b_host, non_blocking=True)
         x.zero_()
-        _, it2, _, _ = ctx.cg(b_dev, x, tol=args.tol, maxit=args.maxit, precond=args.precond)
+        _, it2, _, _ = ctx.cg(b_dev, x, tol=args.tol, maxit=args.maxit, precond=args.precond,
+                        variant=args.cg_variant)
         x_host.copy_(x, non_blocking=True)
     h1.record(stream)
     torch.cuda.synchronize()
@@ -520,7 +543,7 @@ def main():
                        "elements_per_gpu": m.nelem, "local_dof_per_gpu": L,
                        "unique_dof_total": ctx.nglobal, "cg_iters": its, "tol": args.tol,
                        "partition": "x".join(map(str, parts)), "operator": args.operator,
-                       "precond": args.precond,
+                       "precond": args.precond, "cg_variant": args.cg_variant,
                        "parallelism": f"element partition over {world} GPU(s)",
                        "l2": f"inputs larger than L2: {ws / 2**20:.0f} MiB resident working set "
                              f"> {L2_BYTES / 2**20:.0f} MiB L2, streamed every iteration"},
@@ -535,6 +558,7 @@ def main():
                          "avg_launch_us": k1_in_solve_us,
                          "launches": k1_n,
                          "kernels_replayed": kern,
+                         "kernels_in_solve": in_solve,
                          "step_share": shares,
                          "iteration": {"us": 1e3 * ms / args.steps / its,
                                        "algorithmic_bytes": bpn_k1 * L + (k2_bytes or 0.0),
@@ -544,7 +568,8 @@ def main():
                                    f"stream over {prof_steps} solves of the same workload run right "
                                    "after the timed region (also step_share); kernels_replayed: "
                                    "CUDA events around a graph of 50 back-to-back launches "
-                                   "(sem_kernel_replay, no CG neighbours in L2)"},
+                                   "(sem_kernel_replay, no CG neighbours in L2); kernels_in_solve: "
+                                   "the per-launch events of the profiled solves"},
             "gpu_launches": gpu_launches,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -169,6 +169,18 @@ enum sem_precond {
 int sem_pcg(sem_ctx *ctx, int precond, const double *b, double *x, double tol, int maxit,
             int *iters, double *rel_res);
 
+/* Single-reduction CG (reading R7): the
+ * Chronopoulos-Gear recurrence of the same CG (identity preconditioner,
+ * Poisson operator): A is applied to the residual, A p is carried by
+ * s = w + beta s, and both inner products of an iteration, (r,r)_c and
+ * (r, A r)_c, are reduced at ONE point (one all-gather per iteration with
+ * nranks > 1 instead of two).  Same contract as sem_cg (b, x, tol, maxit,
+ * iters, rel_res, stopping rule, collective, synchronises).  x may hold a
+ * discontinuous x0: the solution is x0 + the accumulated increment at every
+ * copy.  SEM_EINVAL with a screened (alpha) operator or the simple Ax kernel. */
+int sem_cg_sr(sem_ctx *ctx, const double *b, double *x, double tol, int maxit, int *iters,
+              double *rel_res);
+
 /* d = Q Q^T diag(A_L): the diagonal of the assembled (unmasked) operator in
  * local storage, diag(A^e)_q = sum over the three GLL lines through q
  * (DESIGN.md "Jacobi").  d: DEVICE [nlocal].  Collective.  Asynchronous. */

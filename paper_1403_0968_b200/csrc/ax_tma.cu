@@ -27,7 +27,8 @@ cudaError_t launch_ax_cg_hi_pc(const DevMesh &m, const CgVecs &v, int64_t eb, in
 cudaError_t upload_const_D(int N, const double *D_host) {
     cudaError_t e = upload_D_this_tu(N, D_host);
     if (e == cudaSuccess) e = upload_const_D_mass(N, D_host);
-    return e == cudaSuccess ? upload_const_D_pc(N, D_host) : e;
+    if (e == cudaSuccess) e = upload_const_D_pc(N, D_host);
+    return e == cudaSuccess ? upload_const_D_sr(N, D_host) : e;
 }
 
 bool tma_supported(int N) { return N >= 1 && N <= kTmaMaxN; }

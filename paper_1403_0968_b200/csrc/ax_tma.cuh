@@ -166,8 +166,12 @@ struct TmaArgs {
 };
 
 // PC: Jacobi PCG scalars (cg_k1_prologue_t); a separate instantiation so the
-// CG kernel's code is unchanged (ax_tma_pc.cu)
-template <int N, bool CG, bool MASS, bool PC = false>
+// CG kernel's code is unchanged (ax_tma_pc.cu).
+// DOT (with CG = false): KA of the single-reduction CG (NEXT-3, ax_tma_sr.cu):
+// the plain apply w = A_L u plus per-CTA partials of (u, A_L u) = (u, w)_c for
+// continuous masked u; no scalars needed (only the iteration parity k1, and
+// the sticky stop flag to skip iterations after the stop).
+template <int N, bool CG, bool MASS, bool PC = false, bool DOT = false>
 __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs a) {
     using C = TmaCfg<N>;
     using Lo = TmaLayout<N, CG>;
@@ -258,14 +262,28 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
         pdl_wait();
         cg_k1_load<Lo::NT, PC>(a.st, a.red, pre);
     }
+    int dot_done = 0, kit = 0;
+    if constexpr (DOT) {
+        dot_done = ld_state(&a.st->done);
+        kit = ld_state(&a.st->k1);
+    }
     if (leader) {
         if (u0 < nunits) issue_G(u0, 0);
         if (u0 + TG < nunits) issue_G(u0 + TG, 1);
         if (u0 < nunits) issue_V(u0, 0);
         if (u0 + TG < nunits) issue_V(u0 + TG, 1);
     }
+    if constexpr (DOT) {
+        if (dot_done) {
+            if (leader) {
+                if (u0 < nunits) mbar_wait(gbar + 0, 0);
+                if (u0 + TG < nunits) mbar_wait(gbar + 1, 0);
+            }
+            return;
+        }
+        if (blockIdx.x == 0 && tid == 0) a.st->k2 = kit;   // for KB of this iteration
+    }
     double beta = 0.0, alpha_prev = 0.0;
-    int kit = 0;
     if constexpr (CG) {
         const CgStep c = cg_k1_finish<Lo::NT, PC>(a.st, sred, pre);
         if (c.done) {
@@ -388,7 +406,7 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
             if constexpr (MASS) wv = fma(hc[k], col[k], wv);
             if (on) {
                 a.w[gbase + k * n2] = wv;
-                if constexpr (CG) pap = fma(wv, col[k], pap);
+                if constexpr (CG || DOT) pap = fma(wv, col[k], pap);
             }
         }
         fence_proxy_async();     // generic smem writes before the next async refill
@@ -399,7 +417,7 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
         }
     }
 
-    if constexpr (CG) {
+    if constexpr (CG || DOT) {
         // (p, mask Q Q^T A_L p)_c = sum_e p_e^T A_e p_e because p is continuous
         // and zero on the Dirichlet boundary: every local node counts, no
         // weights, no assembly.  One deterministic partial per CTA; the
@@ -437,7 +455,7 @@ struct HiCfg {
     static constexpr size_t SMEM = size_t(NG) * PERG * 8 + size_t(NG) * (2 + R) * 8 + 64;
 };
 
-template <int N, bool CG, bool MASS, bool PC = false>
+template <int N, bool CG, bool MASS, bool PC = false, bool DOT = false>
 __global__ void __launch_bounds__(HiCfg<N, CG>::NT, 1) ax_hi_kernel(TmaArgs a) {
     using C = HiCfg<N, CG>;
     constexpr int n = C::n, n2 = C::n2, n3 = C::n3, GT = C::GT, VL = C::VL, NV = C::NV;
@@ -508,13 +526,28 @@ __global__ void __launch_bounds__(HiCfg<N, CG>::NT, 1) ax_hi_kernel(TmaArgs a) {
         pdl_wait();
         cg_k1_load<C::NT, PC>(a.st, a.red, pre);
     }
+    int dot_done = 0, kit = 0;
+    if constexpr (DOT) {
+        dot_done = ld_state(&a.st->done);
+        kit = ld_state(&a.st->k1);
+    }
     if (leader) {
         for (int64_t gs = 0; gs < R && gs < nsl; ++gs) issue_slice(gs);
         if (nel > 0) issue_vec(e0, 0);
         if (nel > 1) issue_vec(e0 + TG, 1);
     }
+    if constexpr (DOT) {
+        if (dot_done) {
+            if (leader) {
+                for (int64_t gs = 0; gs < R && gs < nsl; ++gs) mbar_wait(gbar + gs, 0);
+                if (nel > 0) mbar_wait(vbar + 0, 0);
+                if (nel > 1) mbar_wait(vbar + 1, 0);
+            }
+            return;
+        }
+        if (blockIdx.x == 0 && tid == 0) a.st->k2 = kit;
+    }
     double beta = 0.0, alpha_prev = 0.0;
-    int kit = 0;
     if constexpr (CG) {
         const CgStep c = cg_k1_finish<C::NT, PC>(a.st, sred, pre);
         if (c.done) {
@@ -623,14 +656,14 @@ __global__ void __launch_bounds__(HiCfg<N, CG>::NT, 1) ax_hi_kernel(TmaArgs a) {
             for (int k = 0; k < n; ++k) {
                 if constexpr (MASS) rw[k] = fma(hc[k], col[k], rw[k]);
                 a.w[gb + k * n2] = rw[k];
-                if constexpr (CG) pap = fma(rw[k], col[k], pap);
+                if constexpr (CG || DOT) pap = fma(rw[k], col[k], pap);
             }
         }
         fence_proxy_async();
         group_bar(1 + g, GT);    // stage s and both f slices consumed
         if (leader && t + 2 < nel) issue_vec(e + 2 * TG, s);
     }
-    if constexpr (CG) {
+    if constexpr (CG || DOT) {
         const double bs = block_sum<C::NT>(pap, sred);
         if (tid == 0) a.part1[(kit & 1) * a.red.s1 + blockIdx.x] = bs;
     }
@@ -749,6 +782,51 @@ static cudaError_t launch_ax_hi_t(const DevMesh &m, const double *u, double *w, 
     SEM_HI_DISPATCH(m.N, (ax_hi_kernel<NN, false, MASS><<<hi_grid<NN, false>(m.E, m.nsm),
                                                           HiCfg<NN, false>::NT,
                                                           HiCfg<NN, false>::SMEM, s>>>(a)));
+    return cudaGetLastError();
+}
+
+// KA of the single-reduction CG: w = A_L r plus (r, w) partials (DOT)
+static TmaArgs sr_args(const DevMesh &m, const CgVecs &v) {
+    TmaArgs a{};
+    a.E = m.E;
+    a.G = m.G;
+    a.u = v.r;
+    a.w = v.w;
+    a.red = make_red(m, v);
+    a.part1 = v.part1;
+    a.st = v.st;
+    return a;
+}
+
+static cudaError_t tma_prepare_dot(int N) {
+    cudaError_t e = cudaSuccess;
+    SEM_TMA_DISPATCH(N, (e = cudaFuncSetAttribute(ax_tma_kernel<NN, false, false, false, true>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)TmaLayout<NN, false>::SMEM)));
+    return e;
+}
+
+static cudaError_t launch_ax_dot_tma_t(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
+    const TmaArgs a = sr_args(m, v);
+    SEM_TMA_DISPATCH(m.N, (ax_tma_kernel<NN, false, false, false, true>
+                           <<<tma_grid<NN, false>(m.E, m.nsm), TmaLayout<NN, false>::NT,
+                              TmaLayout<NN, false>::SMEM, s>>>(a)));
+    return cudaGetLastError();
+}
+
+static cudaError_t hi_prepare_dot(int N) {
+    cudaError_t e = cudaSuccess;
+    SEM_HI_DISPATCH(N, (e = cudaFuncSetAttribute(ax_hi_kernel<NN, false, false, false, true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)HiCfg<NN, false>::SMEM)));
+    return e;
+}
+
+static cudaError_t launch_ax_dot_hi_t(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
+    const TmaArgs a = sr_args(m, v);
+    SEM_HI_DISPATCH(m.N, (ax_hi_kernel<NN, false, false, false, true>
+                          <<<hi_grid<NN, false>(m.E, m.nsm), HiCfg<NN, false>::NT,
+                             HiCfg<NN, false>::SMEM, s>>>(a)));
     return cudaGetLastError();
 }
 

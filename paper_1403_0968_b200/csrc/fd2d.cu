@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/fd.h"
@@ -61,9 +62,20 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// compile-time loop: f(std::integral_constant<int, i>) for i = 0 .. M-1
+template <int I, int M, typename F>
+__device__ __forceinline__ void static_for_impl(F &&f) {
+    if constexpr (I < M) {
+        f(std::integral_constant<int, I>{});
+        static_for_impl<I + 1, M>(f);
+    }
+}
+template <int M, typename F>
+__device__ __forceinline__ void static_for(F &&f) { static_for_impl<0, M>(f); }
+
 // Grid: x = tiles of kTW columns, y = strips of `ty` rows.
 template <int R, bool SYM>
-__global__ void __launch_bounds__(kNT) fd2d_kernel(const double *__restrict__ u1,
+__global__ void __launch_bounds__(kNT, 3) fd2d_kernel(const double *__restrict__ u1,
                                                     const double *__restrict__ u2,
                                                     double *__restrict__ u3, int64_t w, int64_t h,
                                                     int ty, double dt2) {
@@ -118,24 +130,24 @@ __global__ void __launch_bounds__(kNT) fd2d_kernel(const double *__restrict__ u1
     for (int s = 0; s < kP; ++s) issue(s);
 
     const int c0 = 2 * tid;                       // this thread's columns c0, c0+1
-    double q0[2 * R + 1], q1[2 * R + 1];          // u1 rows center-R .. center+R
+    // register queues of the column values of rows s-2R .. s: row s lives in
+    // slot s mod NQ; the row loop is unrolled by NQ so every slot index is a
+    // compile-time constant (a rotating queue, no register moves)
+    constexpr int NQ = 2 * R + 1;
+    double q0[NQ], q1[NQ];
 #pragma unroll
-    for (int k = 0; k < 2 * R + 1; ++k) q0[k] = q1[k] = 0.0;
+    for (int k = 0; k < NQ; ++k) q0[k] = q1[k] = 0.0;
 
-    for (int s = 0; s < nl; ++s) {
+    auto step = [&](const int s, auto uc) {
+        constexpr int u = decltype(uc)::value;        // s mod NQ
         cp_async_wait<kP - 1>();
         __syncthreads();          // row s landed for all; step s-1's reads are done
         issue(s + kP);            // refills the slot of row s+kP-NB = s-R-1 (no longer read)
         const int slot = s % NB;
-#pragma unroll
-        for (int k = 0; k < 2 * R; ++k) {
-            q0[k] = q0[k + 1];
-            q1[k] = q1[k + 1];
-        }
         const double2 nv = *reinterpret_cast<const double2 *>(s1 + slot * RW + LP + c0);
-        q0[2 * R] = nv.x;                               // own columns of the new row
-        q1[2 * R] = nv.y;
-        if (s < 2 * R) continue;
+        q0[u] = nv.x;                                   // own columns of the new row
+        q1[u] = nv.y;
+        if (s < 2 * R) return;
         // center row s - R: x-neighbours from its smem row, u2 from the slot of row s
         const int64_t j = j0 + s - 2 * R;
         // window of the center row: xw[XO + R + k] = u1(c0 + k), 16-byte pairs
@@ -148,31 +160,34 @@ __global__ void __launch_bounds__(kNT) fd2d_kernel(const double *__restrict__ u1
             xw[2 * t + 1] = pv.y;
         }
         const double *xv = xw + XO;                     // xv[R + k] = u1(c0 + k)
+        // y[R + k] = u1 of row (center + k) = slot (u - R + k) mod NQ
+        auto Y0 = [&](int k) -> double { return q0[(u - R + k + 2 * NQ) % NQ]; };
+        auto Y1 = [&](int k) -> double { return q1[(u - R + k + 2 * NQ) % NQ]; };
         const double2 v2 = *reinterpret_cast<const double2 *>(s2 + slot * kTW + c0);
         double o0, o1;
         if constexpr (SYM) {
-            double lap0 = c_omega[R] * (q0[R] + q0[R]);
-            double lap1 = c_omega[R] * (q1[R] + q1[R]);
+            double lap0 = c_omega[R] * (Y0(0) + Y0(0));
+            double lap1 = c_omega[R] * (Y1(0) + Y1(0));
 #pragma unroll
             for (int k = 1; k <= R; ++k) {
                 const double om = c_omega[R + k];
-                lap0 = fma(om, (xv[R - k] + xv[R + k]) + (q0[R - k] + q0[R + k]), lap0);
-                lap1 = fma(om, (xv[R - k + 1] + xv[R + k + 1]) + (q1[R - k] + q1[R + k]), lap1);
+                lap0 = fma(om, (xv[R - k] + xv[R + k]) + (Y0(-k) + Y0(k)), lap0);
+                lap1 = fma(om, (xv[R - k + 1] + xv[R + k + 1]) + (Y1(-k) + Y1(k)), lap1);
             }
-            o0 = fma(-dt2, lap0, fma(-2.0, q0[R], v2.x));
-            o1 = fma(-dt2, lap1, fma(-2.0, q1[R], v2.y));
+            o0 = fma(-dt2, lap0, fma(-2.0, Y0(0), v2.x));
+            o1 = fma(-dt2, lap1, fma(-2.0, Y1(0), v2.y));
         } else {
             double lap0 = 0.0, lap1 = 0.0;
 #pragma unroll
             for (int k = -R; k <= R; ++k) {
                 const double om = c_omega[R + k];
                 // lap += weight[r+k]*u1[j*w + nX] + weight[r+k]*u1[nY*w + i]
-                lap0 = __dadd_rn(lap0, __dadd_rn(__dmul_rn(om, xv[R + k]), __dmul_rn(om, q0[R + k])));
-                lap1 = __dadd_rn(lap1, __dadd_rn(__dmul_rn(om, xv[R + k + 1]), __dmul_rn(om, q1[R + k])));
+                lap0 = __dadd_rn(lap0, __dadd_rn(__dmul_rn(om, xv[R + k]), __dmul_rn(om, Y0(k))));
+                lap1 = __dadd_rn(lap1, __dadd_rn(__dmul_rn(om, xv[R + k + 1]), __dmul_rn(om, Y1(k))));
             }
             // u3[id] = (-2*r_u1 + r_u2 - dt*dt*lap)
-            o0 = __dsub_rn(__dadd_rn(__dmul_rn(-2.0, q0[R]), v2.x), __dmul_rn(dt2, lap0));
-            o1 = __dsub_rn(__dadd_rn(__dmul_rn(-2.0, q1[R]), v2.y), __dmul_rn(dt2, lap1));
+            o0 = __dsub_rn(__dadd_rn(__dmul_rn(-2.0, Y0(0)), v2.x), __dmul_rn(dt2, lap0));
+            o1 = __dsub_rn(__dadd_rn(__dmul_rn(-2.0, Y1(0)), v2.y), __dmul_rn(dt2, lap1));
         }
         const int64_t x = i0 + c0;
         double *out = u3 + j * w + x;
@@ -186,6 +201,12 @@ __global__ void __launch_bounds__(kNT) fd2d_kernel(const double *__restrict__ u1
         } else if (x < w) {
             __stcs(out, o0);
         }
+    };
+    for (int s0 = 0; s0 < nl; s0 += NQ) {
+        static_for<NQ>([&](auto uc) {
+            const int s = s0 + decltype(uc)::value;
+            if (s < nl) step(s, uc);
+        });
     }
     cp_async_wait<0>();
 }

@@ -258,6 +258,15 @@ int comm_allgather_scalar(Comm *cp, double *slot_base, cudaStream_t s, std::stri
     return SEM_OK;
 }
 
+int comm_allgather(Comm *cp, double *slot_base, int count, cudaStream_t s, std::string &err) {
+    if (!cp) {
+        err = "no communicator";
+        return SEM_ESTATE;
+    }
+    NC(ncclAllGather(slot_base + size_t(cp->rank) * count, slot_base, count, ncclDouble, cp->nccl, s));
+    return SEM_OK;
+}
+
 void comm_free(Comm *c) {
     if (!c) return;
     if (c->nccl) ncclCommDestroy(c->nccl);

@@ -51,6 +51,8 @@ int comm_exchange(Comm *c, const DevMesh &m, double *w, cudaStream_t s, int64_t 
                   std::string &err);
 // In-place all-gather of one double per rank at slot_base[0..nranks).
 int comm_allgather_scalar(Comm *c, double *slot_base, cudaStream_t s, std::string &err);
+// `count` doubles per rank, rank-major at slot_base (in place)
+int comm_allgather(Comm *c, double *slot_base, int count, cudaStream_t s, std::string &err);
 void comm_free(Comm *c);
 
 }  // namespace sem

@@ -50,8 +50,9 @@ struct sem_ctx {
     // CUDA graph of kChunk CG iterations (captured on first use)
     bool use_graph = true;
     cudaStream_t cap_stream = nullptr;
-    cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};   // by preconditioner (0 none, 1 Jacobi)
-    int64_t graph_kernels[2] = {0, 0};
+    cudaGraphExec_t graph_exec[3] = {nullptr, nullptr, nullptr};   // CG, Jacobi PCG, single-reduction CG
+    int64_t graph_kernels[3] = {0, 0, 0};
+    int method = 0;                  // solver being run / captured: 0 CG, 1 Jacobi PCG, 2 single-reduction
     cudaGraphExec_t replay_exec = nullptr;   // sem_kernel_replay
     // boundary/interior K1 split (k1_split): the exchange runs on `side`
     // between fork (boundary K1 done) and join (before the pap all-gather)
@@ -564,6 +565,7 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         CU(upload_const_D(N, Dh.data()));
         if (dm.use_tma) CU(tma_prepare(N, dm.H != nullptr));
         if (dm.use_hi) CU(hi_prepare(N, dm.H != nullptr));
+        if ((dm.use_tma || dm.use_hi) && !dm.H) CU(sr_prepare(dm));
         CU(cudaEventCreateWithFlags(&ctx->ev[0], cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&ctx->ev[1], cudaEventDisableTiming));
         CU(cudaMemcpyAsync((void *)dm.D, Dh.data(), sizeof(double) * Dh.size(),
@@ -665,7 +667,7 @@ extern "C" int sem_exchange_plan(const sem_mesh *mesh, int N, int64_t *counts, i
 
 extern "C" void sem_free(sem_ctx *ctx) {
     if (!ctx) return;
-    if (ctx->graph_exec[0] || ctx->graph_exec[1] || ctx->replay_exec)
+    if (ctx->graph_exec[0] || ctx->graph_exec[1] || ctx->graph_exec[2] || ctx->replay_exec)
         cudaStreamSynchronize(ctx->stream);
     for (auto &g : ctx->graph_exec)
         if (g) cudaGraphExecDestroy(g);
@@ -826,24 +828,51 @@ static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
     return SEM_OK;
 }
 
-// Capture kChunk iterations once per context into a CUDA graph (on a private
-// non-blocking stream; the graph is launched into the caller's stream).
+// Single-reduction CG (NEXT-3): KA (w = A_L r, (r,w) partials), [exchange of
+// w, fold + ONE all-gather of the (gamma, delta) pair], KB (DSSUM + the
+// recurrences + (r,r) partials; the only scalar reduction of the iteration).
+static double kb_bytes(const sem_ctx *ctx) {
+    const int64_t ni = ctx->N - 1;
+    const double nint = double(ctx->E) * ni * ni * ni;
+    return 16.0 * ctx->dm.nsurf + 56.0 * (ctx->dm.ngroups - ctx->dm.ndir) + 72.0 * nint;
+}
+
+static int enqueue_iteration_sr(sem_ctx *ctx, int k, cudaStream_t s) {
+    CgVecs &v = ctx->cv;
+    const int P = ctx->nranks;
+    int rc;
+    LAUNCHP(kProfAxCg, 64.0 * ctx->L, k, launch_ax_dot(ctx->dm, v, s));
+    if (P > 1) {
+        if ((rc = exchange_impl(ctx, v.w, s))) return rc;
+        LAUNCH(launch_sr_fold(ctx->dm, v, s));
+        std::string cerr;
+        rc = comm_allgather(ctx->comm, v.rr_all + (k & 3) * 2 * P, 2, s, cerr);
+        if (rc) return fail(ctx, rc, "%s", cerr.c_str());
+    }
+    LAUNCHP(kProfK2, kb_bytes(ctx), k, launch_kb_sr(ctx->dm, v, s));
+    return SEM_OK;
+}
+
+// Capture kChunk iterations once per context and method into a CUDA graph (on
+// a private non-blocking stream; the graph is launched into the caller's stream).
 static int build_cg_graph(sem_ctx *ctx) {
     if (!ctx->cap_stream) CU(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
     const int64_t l0 = ctx->launches;
     CU(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
     int rc = SEM_OK;
-    for (int q = 0; q < kChunk && rc == SEM_OK; ++q) rc = enqueue_iteration(ctx, q, ctx->cap_stream);
+    for (int q = 0; q < kChunk && rc == SEM_OK; ++q)
+        rc = ctx->method == 2 ? enqueue_iteration_sr(ctx, q, ctx->cap_stream)
+                              : enqueue_iteration(ctx, q, ctx->cap_stream);
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &g);
-    ctx->graph_kernels[ctx->cv.dinv ? 1 : 0] = ctx->launches - l0;
+    ctx->graph_kernels[ctx->method] = ctx->launches - l0;
     ctx->launches = l0;
     if (rc) {
         if (g) cudaGraphDestroy(g);
         return rc;
     }
     CU(e);
-    e = cudaGraphInstantiate(&ctx->graph_exec[ctx->cv.dinv ? 1 : 0], g, 0);
+    e = cudaGraphInstantiate(&ctx->graph_exec[ctx->method], g, 0);
     cudaGraphDestroy(g);
     CU(e);
     return SEM_OK;
@@ -890,6 +919,92 @@ extern "C" int sem_pcg(sem_ctx *ctx, int precond, const double *b, double *x, do
     return cg_impl(ctx, precond, b, x, tol, maxit, iters, rel_res);
 }
 
+static int cg_sr_impl(sem_ctx *ctx, const double *b, double *x, double tol, int maxit,
+                      int *iters, double *rel_res);
+
+extern "C" int sem_cg_sr(sem_ctx *ctx, const double *b, double *x, double tol, int maxit,
+                         int *iters, double *rel_res) {
+    CHECK_CTX();
+    return cg_sr_impl(ctx, b, x, tol, maxit, iters, rel_res);
+}
+
+// Poll the device state one chunk behind (see cg_impl) until the sticky stop
+// flag is set; returns with the stream's work for the last chunk enqueued.
+static int run_chunks(sem_ctx *ctx, int maxit, bool graph, cudaGraphExec_t gexec, cudaStream_t s) {
+    CgVecs &v = ctx->cv;
+    int rc;
+    int k = 0, c = 0;
+    while (true) {
+        if (graph) {
+            CU(cudaGraphLaunch(gexec, s));
+            ctx->launches += ctx->graph_kernels[ctx->method];
+            k += kChunk;
+        } else {
+            for (int q = 0; q < kChunk; ++q, ++k) {
+                rc = ctx->method == 2 ? enqueue_iteration_sr(ctx, k, s) : enqueue_iteration(ctx, k, s);
+                if (rc) return rc;
+            }
+        }
+        CU(cudaMemcpyAsync(&ctx->host_state[c & 1], v.st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
+        CU(cudaEventRecord(ctx->ev[c & 1], s));
+        if (c > 0) {
+            CU(cudaEventSynchronize(ctx->ev[(c - 1) & 1]));
+            if (ctx->host_state[(c - 1) & 1].done) break;
+        }
+        if (k > maxit + 3 * kChunk) {  // the device must have stopped by now
+            CU(cudaEventSynchronize(ctx->ev[c & 1]));
+            break;
+        }
+        ++c;
+    }
+    return SEM_OK;
+}
+
+static int cg_sr_impl(sem_ctx *ctx, const double *b, double *x, double tol, int maxit,
+                      int *iters, double *rel_res) {
+    if (!b || !x || !aligned8(b) || !aligned8(x)) return fail(ctx, SEM_EINVAL, "sem_cg_sr: bad pointer");
+    if (!(tol >= 0.0) || maxit < 0) return fail(ctx, SEM_EINVAL, "sem_cg_sr: tol >= 0 and maxit >= 0 required");
+    if (!ctx->dm.use_tma && !ctx->dm.use_hi)
+        return fail(ctx, SEM_EINVAL, "sem_cg_sr: needs the TMA / high-order Ax kernels (not SEM_AX_KERNEL=simple)");
+    if (ctx->dm.H) return fail(ctx, SEM_EINVAL, "sem_cg_sr: Poisson operator only (no alpha mass term)");
+    cudaStream_t s = ctx->stream;
+    CgVecs &v = ctx->cv;
+    v.b = b;
+    v.x = x;
+    v.dinv = nullptr;
+    ctx->method = 2;
+    int rc;
+    {
+        CgState h{};
+        h.tol = tol;
+        h.maxit = maxit;
+        CU(cudaMemcpyAsync(&v.st->tol, &h.tol, sizeof(double), cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(&v.st->maxit, &h.maxit, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    }
+    // r = mask (b - Q Q^T A_L x0) and (r,r) partials (K2's start); p = s = x increment = 0
+    LAUNCH(launch_ax(ctx->dm, x, v.w, s));
+    if ((rc = exchange_impl(ctx, v.w, s))) return rc;
+    LAUNCH(launch_sr_init(ctx->dm, v, s));
+    LAUNCH(launch_k2(ctx->dm, v, true, s));
+    const bool graph = !ctx->prof && ctx->use_graph;
+    cudaGraphExec_t &gexec = ctx->graph_exec[2];
+    if (graph && !gexec && (rc = build_cg_graph(ctx))) return rc;
+    if ((rc = run_chunks(ctx, maxit, graph, gexec, s))) return rc;
+    LAUNCH(launch_sr_finish(ctx->dm, v, s));
+    CU(cudaMemcpyAsync(&ctx->host_state[0], v.st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    const CgState &hs = ctx->host_state[0];
+    if (!hs.done) return fail(ctx, SEM_ECUDA, "sem_cg_sr: device did not reach a stopping decision");
+    if (ctx->prof) prof_fold(ctx, hs.iters);
+    if (iters) *iters = hs.iters;
+    if (rel_res) *rel_res = hs.rel_res;
+    if (!hs.converged && tol > 0.0) {
+        fail(ctx, SEM_ENOCONV, "sem_cg_sr: maxit=%d reached, rel_res=%.3e > tol=%.3e", maxit, hs.rel_res, tol);
+        return SEM_ENOCONV;
+    }
+    return SEM_OK;
+}
+
 static int cg_impl(sem_ctx *ctx, int precond, const double *b, double *x, double tol, int maxit,
                    int *iters, double *rel_res) {
     if (!b || !x || !aligned8(b) || !aligned8(x)) return fail(ctx, SEM_EINVAL, "sem_cg: bad pointer");
@@ -902,6 +1017,7 @@ static int cg_impl(sem_ctx *ctx, int precond, const double *b, double *x, double
     int rc;
     if (precond == SEM_PC_JACOBI && (rc = prepare_jacobi(ctx, s))) return rc;
     v.dinv = (precond == SEM_PC_JACOBI) ? ctx->dinv_buf : nullptr;
+    ctx->method = (precond == SEM_PC_JACOBI) ? 1 : 0;
     // tol / maxit into the device state (the init kernel resets the rest)
     {
         CgState h{};
@@ -930,13 +1046,13 @@ static int cg_impl(sem_ctx *ctx, int precond, const double *b, double *x, double
     // more chunks once it is set (later kernels of a chunk are no-ops).  Each
     // chunk is one CUDA-graph launch unless profiling (per-launch events).
     const bool graph = !ctx->prof && ctx->use_graph;
-    cudaGraphExec_t &gexec = ctx->graph_exec[v.dinv ? 1 : 0];
+    cudaGraphExec_t &gexec = ctx->graph_exec[ctx->method];
     if (graph && !gexec && (rc = build_cg_graph(ctx))) return rc;
     int k = 0, c = 0;
     while (true) {
         if (graph) {
             CU(cudaGraphLaunch(gexec, s));
-            ctx->launches += ctx->graph_kernels[v.dinv ? 1 : 0];
+            ctx->launches += ctx->graph_kernels[ctx->method];
             k += kChunk;
         } else {
             for (int q = 0; q < kChunk; ++q, ++k)

@@ -23,6 +23,9 @@ struct CgState {
     double alpha_km1;           // alpha_{it-1} at the stop, for the final x update
     int32_t k1;                 // iteration of the next K1 (written by K2 / the CG start)
     int32_t k2;                 // iteration of the next K2 (written by K1)
+    // single-reduction CG (NEXT-3): gamma_k, alpha_k of iteration k in slot k & 1
+    double gamma_hist[2];
+    double alpha_hist[2];
 };
 
 // Gather-scatter groups are stored by class (Dirichlet flag, multiplicity m):
@@ -121,6 +124,19 @@ cudaError_t launch_cg_finish(const DevMesh &m, const CgVecs &v, cudaStream_t s);
 cudaError_t launch_cg_red_pap(const DevMesh &m, const CgVecs &v, cudaStream_t s);
 cudaError_t launch_cg_red_rr(const DevMesh &m, const CgVecs &v, cudaStream_t s);
 cudaError_t launch_cg_red_rz(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+// single-reduction (Chronopoulos-Gear) CG, NEXT-3 (cg_update.cu, ax_tma_sr.cu).
+// Global storage: p, s and the x increment live once per global node of the
+// rank -- surface group g at slot g, element-interior node t at ngroups + t --
+// in the workspace vectors p, z and xw.  sr_all: [kRing][nranks][2] rank
+// values of (gamma, delta) (the rr_all region).
+cudaError_t upload_const_D_sr(int N, const double *D_host);
+cudaError_t sr_prepare(const DevMesh &m);
+cudaError_t launch_ax_dot(const DevMesh &m, const CgVecs &v, cudaStream_t s);   // KA
+int ka_blocks(const DevMesh &m);                  // KA's grid = its partial count
+cudaError_t launch_kb_sr(const DevMesh &m, const CgVecs &v, cudaStream_t s);    // KB
+cudaError_t launch_sr_init(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+cudaError_t launch_sr_finish(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+cudaError_t launch_sr_fold(const DevMesh &m, const CgVecs &v, cudaStream_t s);  // nranks > 1
 // Jacobi preconditioner (NEXT-2): d = diag(A_L) per local node (unassembled;
 // kappa-folded G^ + the mass term H); then, after Q Q^T d, dinv = 1 / d
 // (the caller masks it)

@@ -44,7 +44,7 @@ EXPORTS = ["sem_version", "sem_gll", "sem_workspace_bytes", "sem_setup", "sem_si
            "sem_ax", "sem_dssum", "sem_mask", "sem_mass", "sem_cg", "sem_launch_count",
            "sem_free", "sem_strerror", "sem_last_error", "sem_nccl_id_bytes",
            "sem_nccl_get_unique_id", "sem_profile", "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan",
-           "sem_pcg", "sem_diag", "fd_weights", "fd2d_step", "fd2d_run"]
+           "sem_pcg", "sem_diag", "sem_cg_sr", "fd_weights", "fd2d_step", "fd2d_run"]
 
 # preconditioners of sem_pcg (include/sem.h enum sem_precond)
 PRECOND = {"none": 0, "jacobi": 1}
@@ -84,6 +84,8 @@ def lib():
     L.sem_pcg.argtypes = [P, ctypes.c_int, P, P, ctypes.c_double, ctypes.c_int,
                           ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
     L.sem_diag.argtypes = [P, P]
+    L.sem_cg_sr.argtypes = [P, P, P, ctypes.c_double, ctypes.c_int,
+                            ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
     L.sem_launch_count.argtypes = [P]
     L.sem_launch_count.restype = i64
     L.sem_free.argtypes = [P]
@@ -102,7 +104,7 @@ def lib():
                                     ctypes.POINTER(i64), ctypes.POINTER(i64)]
     for f in ("sem_gll", "sem_workspace_bytes", "sem_setup", "sem_sizes", "sem_ax", "sem_dssum",
               "sem_mask", "sem_mass", "sem_cg", "sem_nccl_get_unique_id", "sem_profile",
-              "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan", "sem_pcg", "sem_diag"):
+              "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan", "sem_pcg", "sem_diag", "sem_cg_sr"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
@@ -221,15 +223,23 @@ class Context:
         return b
 
     def cg(self, b, x=None, tol: float = 1e-8, maxit: int = 1000, raise_noconv: bool = False,
-           precond: str = "none"):
+           precond: str = "none", variant: str = "standard"):
         """Returns (x, iters, rel_res, converged).  precond="jacobi": sem_pcg
-        with the Jacobi preconditioner (NEXT-2)."""
+        with the Jacobi preconditioner (NEXT-2).  variant="single_reduction":
+        sem_cg_sr, the Chronopoulos-Gear recurrence (NEXT-3)."""
         import torch
         if x is None:
             x = torch.zeros_like(b)
         it = ctypes.c_int(0)
         rr = ctypes.c_double(0.0)
-        if precond == "none":
+        if variant == "single_reduction":
+            if precond != "none":
+                raise ValueError("the single-reduction variant has no preconditioner")
+            rc = lib().sem_cg_sr(self._ctx, _dptr(b, self.nlocal, "b"), _dptr(x, self.nlocal, "x"),
+                                 float(tol), int(maxit), ctypes.byref(it), ctypes.byref(rr))
+        elif variant != "standard":
+            raise ValueError(f"unknown CG variant {variant!r}")
+        elif precond == "none":
             rc = lib().sem_cg(self._ctx, _dptr(b, self.nlocal, "b"), _dptr(x, self.nlocal, "x"),
                               float(tol), int(maxit), ctypes.byref(it), ctypes.byref(rr))
         else:
