@@ -218,7 +218,17 @@ static int fd_fail(int code, const char *msg) {
     return code;
 }
 
-constexpr int kStrip = 64;   // rows per CTA strip
+// rows per CTA strip (the 2r halo rows are re-read per strip); SEM_FD_STRIP
+// overrides it for experiments
+// (measured on 8192^2: 32 rows best up to r = 4, 64 above -- tools/gpu_r01q.sh)
+static int strip_rows(int r) {
+    static const int v = [] {
+        const char *e = getenv("SEM_FD_STRIP");
+        const int x = e ? atoi(e) : 0;
+        return x >= 8 ? x : 0;
+    }();
+    return v ? v : (r <= 4 ? 32 : 64);
+}
 
 template <int R, bool SYM>
 static cudaError_t launch_rs(const double *u1, const double *u2, double *u3, int64_t w, int64_t h,
@@ -231,8 +241,9 @@ static cudaError_t launch_rs(const double *u1, const double *u2, double *u3, int
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    dim3 grid((unsigned)((w + kTW - 1) / kTW), (unsigned)((h + kStrip - 1) / kStrip));
-    fd2d_kernel<R, SYM><<<grid, kNT, C::SMEM, s>>>(u1, u2, u3, w, h, kStrip, dt2);
+    const int ty = strip_rows(R);
+    dim3 grid((unsigned)((w + kTW - 1) / kTW), (unsigned)((h + ty - 1) / ty));
+    fd2d_kernel<R, SYM><<<grid, kNT, C::SMEM, s>>>(u1, u2, u3, w, h, ty, dt2);
     return cudaGetLastError();
 }
 

@@ -172,3 +172,43 @@ def coefficients(mesh: Mesh, kappa_amp: float = 0.5, alpha0: float = 1.0):
                                * np.cos(2 * np.pi * z / Lz))
     alpha = alpha0 * (1.0 + 0.5 * np.cos(np.pi * x / Lx) * np.cos(np.pi * y / Ly))
     return np.ascontiguousarray(kappa.reshape(-1)), np.ascontiguousarray(alpha.reshape(-1))
+
+
+def relabel(mesh: Mesh, seed: int, rotate: bool = True, id_stride: int = 3) -> Mesh:
+    """The same discretisation presented differently (robustness inputs; no
+    method arithmetic): elements in a random order, each element's local
+    nodes turned by a random quarter rotation about its k axis,
+    (i, j, k) <- (N - j, i, k) applied 0-3 times (orientation preserving, so
+    J stays > 0), and the global ids replaced by a random injective relabelling
+    with gaps (id -> id_stride * perm(id) + 7, a non-compact id range).
+    Returns a new Mesh (nboundary = 0)."""
+    rng = np.random.default_rng(seed)
+    n = mesh.N + 1
+    n3 = n ** 3
+    E = mesh.nelem
+    order = rng.permutation(E)
+    k, j, i = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    i, j, k = i.reshape(-1), j.reshape(-1), k.reshape(-1)
+    rots = [np.arange(n3)]
+    ii, jj = i.copy(), j.copy()
+    for _ in range(3):
+        ii, jj = mesh.N - jj, ii                  # new node (i,j,k) takes old (N-j, i, k)
+        rots.append(ii + n * jj + n * n * k)
+    which = rng.integers(0, 4 if rotate else 1, size=E)
+    xyz = np.empty_like(mesh.xyz)
+    glo = np.empty_like(mesh.glo)
+    dirichlet = np.empty_like(mesh.dirichlet)
+    for new_e, old_e in enumerate(order):
+        src = rots[which[new_e]]
+        xyz[new_e] = mesh.xyz[old_e][:, src]
+        glo[new_e] = mesh.glo[old_e][src]
+        dirichlet[new_e] = mesh.dirichlet[old_e][src]
+    ids = np.unique(mesh.glo)
+    perm = rng.permutation(ids.size)
+    remap = np.empty(int(ids.max()) + 1, dtype=np.int64)
+    remap[ids] = id_stride * perm.astype(np.int64) + 7
+    glo = remap[glo]
+    eidx = None if mesh.eidx is None else mesh.eidx[order]
+    return Mesh(N=mesh.N, xyz=np.ascontiguousarray(xyz), glo=np.ascontiguousarray(glo),
+                dirichlet=np.ascontiguousarray(dirichlet), elems=mesh.elems, lengths=mesh.lengths,
+                parts=mesh.parts, rank=mesh.rank, eidx=eidx, nboundary=0)

@@ -261,3 +261,26 @@ def test_c3_cg_full_size(dev, c3):
     # both solutions approximate the manufactured u* equally well
     us, _ = meshgen.manufactured(m)
     assert abs(np.abs(x.cpu().numpy() - us).max() - np.abs(xr - us).max()) <= 1e-10
+
+
+# --- the same discretisation presented differently (meshgen.relabel): random
+# element order, quarter-turned elements, non-compact global ids ---
+@pytest.mark.parametrize("N,elems", [(3, (4, 3, 3)), (7, (4, 4, 3)), (12, (2, 2, 2))])
+def test_relabelled_mesh_parity(dev, impl, N, elems):
+    from paper_1403_0968_b200 import sem
+    xi, _ = oracle.gll(N)
+    m = meshgen.relabel(meshgen.box_mesh(N, xi, elems=elems, eps=0.05), seed=N)
+    G, J = oracle.geom(N, m.xyz)
+    ctx = sem.Context(m, N, device=0)
+    u = meshgen.random_field(m.nlocal, 1)
+    w = ctx.ax(T(u, dev))
+    wr = oracle.ax(N, G, u)
+    assert relerr(w.cpu().numpy(), wr) <= 1e-12
+    ctx.dssum(w)
+    assert relerr(w.cpu().numpy(), oracle.dssum(m.glo, wr)) <= 1e-12
+    _, f = meshgen.manufactured(m)
+    b = oracle.mass_rhs(N, m.glo, m.dirichlet, J, f)
+    x, its, rel, ok = ctx.cg(T(b, dev), tol=1e-8, maxit=3000)
+    xr, its_r, rel_r, st = oracle.cg(N, m.glo, m.dirichlet, G, b, tol=1e-8, maxit=3000)
+    assert ok and st == 0 and its == its_r, (its, its_r)
+    assert relerr(x.cpu().numpy(), xr) <= 1e-10
