@@ -2,6 +2,7 @@
 // and the exported launchers; operators with a mass term (DevMesh::H) are
 // forwarded to ax_tma_mass.cu.
 #include "ax_tma.cuh"
+#include "ax_dmma.cuh"
 
 namespace sem {
 
@@ -32,6 +33,22 @@ cudaError_t upload_const_D(int N, const double *D_host) {
 }
 
 bool tma_supported(int N) { return N >= 1 && N <= kTmaMaxN; }
+bool dmma_supported(int N) { return N == 7; }
+
+template <bool CG>
+static int dmma_grid(int64_t E, int nsm) {
+    const int64_t need = (E + TmaLayout<7, CG>::NG - 1) / TmaLayout<7, CG>::NG;
+    return (int)(need < nsm ? (need < 1 ? 1 : need) : nsm);
+}
+
+static cudaError_t dmma_prepare() {
+    cudaError_t e = cudaFuncSetAttribute(ax_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)TmaLayout<7, false>::SMEM);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(ax_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)TmaLayout<7, true>::SMEM);
+    return e;
+}
 bool hi_supported(int N) { return N >= 6 && N <= 15; }
 
 int tma_blocks(int N, int64_t E, int nsm, bool cg) {
@@ -56,6 +73,7 @@ int hi_blocks(int N, int64_t E, int nsm, bool cg) {
 
 cudaError_t tma_prepare(int N, bool mass) {
     cudaError_t e = mass ? tma_prepare_mass(N) : tma_prepare_t<false>(N);
+    if (e == cudaSuccess && dmma_supported(N)) e = dmma_prepare();
     return e == cudaSuccess ? tma_prepare_pc(N, mass) : e;
 }
 
@@ -65,6 +83,16 @@ cudaError_t hi_prepare(int N, bool mass) {
 }
 
 cudaError_t launch_ax_tma(const DevMesh &m, const double *u, double *w, cudaStream_t s) {
+    if (m.use_dmma && !m.H) {
+        TmaArgs a{};
+        a.E = m.E;
+        a.G = m.G;
+        a.u = u;
+        a.w = w;
+        ax_dmma_kernel<false><<<dmma_grid<false>(m.E, m.nsm), TmaLayout<7, false>::NT,
+                                TmaLayout<7, false>::SMEM, s>>>(a);
+        return cudaGetLastError();
+    }
     return m.H ? launch_ax_tma_mass(m, u, w, s) : launch_ax_tma_t<false>(m, u, w, s);
 }
 
@@ -75,6 +103,11 @@ cudaError_t launch_ax_hi(const DevMesh &m, const double *u, double *w, cudaStrea
 cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne, int pidx0,
                              cudaStream_t s) {
     if (v.dinv) return launch_ax_cg_tma_pc(m, v, eb, ne, pidx0, s);
+    if (m.use_dmma && !m.H) {
+        const TmaArgs a = cg_args<false>(m, v, eb, ne, pidx0);
+        return launch_pdl(ax_dmma_kernel<true>, dmma_grid<true>(ne, m.nsm), TmaLayout<7, true>::NT,
+                          TmaLayout<7, true>::SMEM, s, a);
+    }
     return m.H ? launch_ax_cg_tma_mass(m, v, eb, ne, pidx0, s)
                : launch_ax_cg_tma_t<false>(m, v, eb, ne, pidx0, s);
 }

@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(TmaLayout<N, CG>::NT, 1) ax_tma_kernel(TmaArgs
     }
     double beta = 0.0, alpha_prev = 0.0;
     if constexpr (CG) {
-        const CgStep c = cg_k1_finish<Lo::NT, PC>(a.st, sred, pre);
+        const CgStep c = cg_k1_finish<Lo::NT, PC>(a.st, a.red, sred, pre);
         if (c.done) {
             // drain the copies already in flight, then leave
             if (leader) {
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(HiCfg<N, CG>::NT, 1) ax_hi_kernel(TmaArgs a) {
     }
     double beta = 0.0, alpha_prev = 0.0;
     if constexpr (CG) {
-        const CgStep c = cg_k1_finish<C::NT, PC>(a.st, sred, pre);
+        const CgStep c = cg_k1_finish<C::NT, PC>(a.st, a.red, sred, pre);
         if (c.done) {
             if (leader) {       // drain everything in flight
                 for (int64_t gs = 0; gs < R && gs < nsl; ++gs) mbar_wait(gbar + gs, 0);

@@ -230,35 +230,57 @@ __device__ __forceinline__ double thread_sum(const double *src, int cnt) {
 //   cg_k1_finish  block reduction (__syncthreads), decisions, state writes
 template <bool PC>
 struct K1Pre {
-    static constexpr int NS = PC ? 4 : 3;
-    int done, k;
+    static constexpr int NS = PC ? 4 : 3;     // sums: rho_k, rho_{k-1}, pap_{k-1} [, rr_k]
+    static constexpr int NL = PC ? 6 : 4;     // loaded partial sets (both parities)
+    static constexpr int PER = 4;             // loads in flight per thread and set
+    int done, k, maxit, multi;
+    double tol, rho0;
+    double raw[NL][PER];
     double v[NS];
 };
 
+// first PER strided values of one partial set (issued, not consumed)
+template <int NT, int PER>
+__device__ __forceinline__ void thread_load(const double *src, int cnt, double (&v)[PER]) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const int t = threadIdx.x + u * NT;
+        v[u] = (t < cnt) ? __ldcg(src + t) : 0.0;
+    }
+}
+template <int NT, int PER>
+__device__ __forceinline__ double thread_finish(const double *src, int cnt, const double (&v)[PER]) {
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) s += v[u];
+    for (int t = threadIdx.x + PER * NT; t < cnt; t += NT) s += __ldcg(src + t);
+    return s;
+}
+
+// Issue every load of the prologue (state words, partials of both parities)
+// without consuming any, so a kernel can put its bulk copies behind them and
+// only then wait (cg_k1_finish).
 template <int NT, bool PC>
 __device__ __forceinline__ void cg_k1_load(CgState *st, const CgRed &R, K1Pre<PC> &P) {
-    constexpr int NS = K1Pre<PC>::NS;
-    if (R.nranks == 1) {
+    constexpr int NS = K1Pre<PC>::NS, PER = K1Pre<PC>::PER;
+    P.done = ld_state(&st->done);
+    P.k = ld_state(&st->k1);
+    P.maxit = st->maxit;
+    P.tol = st->tol;
+    P.rho0 = __ldcg(&st->rho0);
+    P.multi = R.nranks > 1;
+    if (!P.multi) {
         // rho sources: part2 ((r,r)) or part3 ((r,z)); pap: part1
         const double *prho = PC ? R.part2 + 2 * R.s2 : R.part2;
-        P.done = ld_state(&st->done);
-        P.k = ld_state(&st->k1);
-        const double r0 = thread_sum<NT>(prho, R.nb2), r1 = thread_sum<NT>(prho + R.s2, R.nb2);
-        const double q0 = thread_sum<NT>(R.part1, R.nb1), q1 = thread_sum<NT>(R.part1 + R.s1, R.nb1);
-        double rr0 = 0.0, rr1 = 0.0;
+        thread_load<NT, PER>(prho, R.nb2, P.raw[0]);
+        thread_load<NT, PER>(prho + R.s2, R.nb2, P.raw[1]);
+        thread_load<NT, PER>(R.part1, R.nb1, P.raw[2]);
+        thread_load<NT, PER>(R.part1 + R.s1, R.nb1, P.raw[3]);
         if constexpr (PC) {
-            rr0 = thread_sum<NT>(R.part2, R.nb2);
-            rr1 = thread_sum<NT>(R.part2 + R.s2, R.nb2);
+            thread_load<NT, PER>(R.part2, R.nb2, P.raw[4]);
+            thread_load<NT, PER>(R.part2 + R.s2, R.nb2, P.raw[5]);
         }
-        const int k = P.k;
-        const bool odd = (k - 1) & 1;           // parity of the slots of rho_k, pap_{k-1}
-        P.v[0] = odd ? r1 : r0;                   // rho_k
-        P.v[1] = (k == 0) ? 0.0 : (odd ? r0 : r1);   // rho_{k-1}
-        P.v[2] = (k == 0) ? 0.0 : (odd ? q1 : q0);   // pap_{k-1}
-        if constexpr (PC) P.v[NS - 1] = odd ? rr1 : rr0;   // rr_k (stopping norm)
     } else {
-        P.done = ld_state(&st->done);
-        P.k = ld_state(&st->k1);
         const int k = P.k;
         const double *src[NS];
         int cnt[NS];
@@ -273,8 +295,9 @@ __device__ __forceinline__ void cg_k1_load(CgState *st, const CgRed &R, K1Pre<PC
 }
 
 template <int NT, bool PC>
-__device__ __forceinline__ CgStep cg_k1_finish(CgState *st, double *red, K1Pre<PC> &P) {
-    constexpr int NS = K1Pre<PC>::NS;
+__device__ __forceinline__ CgStep cg_k1_finish(CgState *st, const CgRed &R, double *red,
+                                               K1Pre<PC> &P) {
+    constexpr int NS = K1Pre<PC>::NS, PER = K1Pre<PC>::PER;
     CgStep c{};
     const int k = P.k;
     c.k = k;
@@ -282,21 +305,37 @@ __device__ __forceinline__ CgStep cg_k1_finish(CgState *st, double *red, K1Pre<P
         c.done = true;
         return c;
     }
+    if (!P.multi) {
+        const double *prho = PC ? R.part2 + 2 * R.s2 : R.part2;
+        const double r0 = thread_finish<NT, PER>(prho, R.nb2, P.raw[0]);
+        const double r1 = thread_finish<NT, PER>(prho + R.s2, R.nb2, P.raw[1]);
+        const double q0 = thread_finish<NT, PER>(R.part1, R.nb1, P.raw[2]);
+        const double q1 = thread_finish<NT, PER>(R.part1 + R.s1, R.nb1, P.raw[3]);
+        const bool odd = (k - 1) & 1;           // parity of the slots of rho_k, pap_{k-1}
+        P.v[0] = odd ? r1 : r0;                   // rho_k
+        P.v[1] = (k == 0) ? 0.0 : (odd ? r0 : r1);   // rho_{k-1}
+        P.v[2] = (k == 0) ? 0.0 : (odd ? q1 : q0);   // pap_{k-1}
+        if constexpr (PC) {
+            const double rr0 = thread_finish<NT, PER>(R.part2, R.nb2, P.raw[4]);
+            const double rr1 = thread_finish<NT, PER>(R.part2 + R.s2, R.nb2, P.raw[5]);
+            P.v[NS - 1] = odd ? rr1 : rr0;        // rr_k (stopping norm)
+        }
+    }
     block_sum_vec<NT, NS>(P.v, red);
     const double rho = P.v[0], rho_m1 = P.v[1], pap_m1 = P.v[2];
     const double rr = P.v[NS - 1 - (PC ? 0 : 2)];
-    const double rho0 = (k == 0) ? rr : __ldcg(&st->rho0);
+    const double rho0 = (k == 0) ? rr : P.rho0;
     const double alpha_prev = (k == 0) ? 0.0 : rho_m1 / pap_m1;
     c.beta = (k == 0) ? 0.0 : rho / rho_m1;
     c.alpha_prev = alpha_prev;
-    c.done = cg_stop(k, rr, rho0, st->maxit, st->tol);
+    c.done = cg_stop(k, rr, rho0, P.maxit, P.tol);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (k == 0) st->rho0 = rho0;
         st->k2 = k;                      // for K2 of this iteration
         if (c.done) {
             st->iters = k;
             st->rel_res = (rho0 == 0.0) ? 0.0 : sqrt(rr) / sqrt(rho0);
-            st->converged = (rho0 == 0.0) || !(sqrt(rr) > st->tol * sqrt(rho0));
+            st->converged = (rho0 == 0.0) || !(sqrt(rr) > P.tol * sqrt(rho0));
             st->alpha_km1 = alpha_prev;
             __threadfence();
             st->done = 1;
@@ -309,7 +348,7 @@ template <int NT, bool PC>
 __device__ __forceinline__ CgStep cg_k1_prologue_t(CgState *st, const CgRed &R, double *red) {
     K1Pre<PC> P;
     cg_k1_load<NT, PC>(st, R, P);
-    return cg_k1_finish<NT, PC>(st, red, P);
+    return cg_k1_finish<NT, PC>(st, R, red, P);
 }
 
 // The PCG prologue is kept out of line so the CG kernels' main loops compile
@@ -328,38 +367,60 @@ __device__ __forceinline__ CgStep cg_k1_prologue(CgState *st, const CgRed &R, do
 // K2 prologue (all threads): k and alpha_k = rho_k / pap_k.  The stopping
 // decision of iteration k was taken by K1(k) (sticky flag): K2 only follows
 // it, so the two kernels can never disagree.  K2 is instantiated per
-// preconditioner (k2_kernel<N, INIT, PC>).
-template <int NT, bool PC>
-__device__ __forceinline__ CgStep cg_k2_prologue(CgState *st, const CgRed &R, double *red,
-                                                 double &alpha) {
-    CgStep c{};
+// preconditioner (k2_kernel<N, INIT, PC>).  Split like K1's: cg_k2_load
+// issues every load (both parities), cg_k2_finish consumes them.
+struct K2Pre {
+    static constexpr int PER = 4;
+    int done, k, multi;
+    double raw[4][PER];
     double v[2];
-    int done, k;
-    if (R.nranks == 1) {
+};
+
+template <int NT, bool PC>
+__device__ __forceinline__ void cg_k2_load(CgState *st, const CgRed &R, K2Pre &P) {
+    constexpr int PER = K2Pre::PER;
+    P.done = ld_state(&st->done);
+    P.k = ld_state(&st->k2);
+    P.multi = R.nranks > 1;
+    if (!P.multi) {
         const double *prho = PC ? R.part2 + 2 * R.s2 : R.part2;
-        done = ld_state(&st->done);
-        k = ld_state(&st->k2);
-        const double r0 = thread_sum<NT>(prho, R.nb2), r1 = thread_sum<NT>(prho + R.s2, R.nb2);
-        const double q0 = thread_sum<NT>(R.part1, R.nb1), q1 = thread_sum<NT>(R.part1 + R.s1, R.nb1);
-        v[0] = ((k - 1) & 1) ? r1 : r0;          // rho_k
-        v[1] = (k & 1) ? q1 : q0;                // pap_k
+        thread_load<NT, PER>(prho, R.nb2, P.raw[0]);
+        thread_load<NT, PER>(prho + R.s2, R.nb2, P.raw[1]);
+        thread_load<NT, PER>(R.part1, R.nb1, P.raw[2]);
+        thread_load<NT, PER>(R.part1 + R.s1, R.nb1, P.raw[3]);
     } else {
-        done = ld_state(&st->done);
-        k = ld_state(&st->k2);
+        const int k = P.k;
         const double *src[2];
         int cnt[2];
         rho_src_t<PC>(R, k, src[0], cnt[0]);     // rho_k
         pap_src(R, k, src[1], cnt[1]);           // pap_k
-        v[0] = thread_sum<NT>(src[0], cnt[0]);
-        v[1] = thread_sum<NT>(src[1], cnt[1]);
+        P.v[0] = thread_sum<NT>(src[0], cnt[0]);
+        P.v[1] = thread_sum<NT>(src[1], cnt[1]);
     }
+}
+
+template <int NT, bool PC>
+__device__ __forceinline__ CgStep cg_k2_finish(CgState *st, const CgRed &R, double *red, K2Pre &P,
+                                               double &alpha) {
+    constexpr int PER = K2Pre::PER;
+    CgStep c{};
+    const int k = P.k;
     c.k = k;
-    if (done) {
+    if (P.done) {
         c.done = true;
         return c;
     }
-    block_sum_vec<NT, 2>(v, red);
-    alpha = v[0] / v[1];
+    if (!P.multi) {
+        const double *prho = PC ? R.part2 + 2 * R.s2 : R.part2;
+        const double r0 = thread_finish<NT, PER>(prho, R.nb2, P.raw[0]);
+        const double r1 = thread_finish<NT, PER>(prho + R.s2, R.nb2, P.raw[1]);
+        const double q0 = thread_finish<NT, PER>(R.part1, R.nb1, P.raw[2]);
+        const double q1 = thread_finish<NT, PER>(R.part1 + R.s1, R.nb1, P.raw[3]);
+        P.v[0] = ((k - 1) & 1) ? r1 : r0;        // rho_k
+        P.v[1] = (k & 1) ? q1 : q0;              // pap_k
+    }
+    block_sum_vec<NT, 2>(P.v, red);
+    alpha = P.v[0] / P.v[1];
     if (blockIdx.x == 0 && threadIdx.x == 0) st->k1 = k + 1;   // for K1 of k+1
     return c;
 }

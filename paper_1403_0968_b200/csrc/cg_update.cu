@@ -131,12 +131,16 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
     // [nich + cchunk[c], nich + cchunk[c+1]) the groups of class c
     // (kK2Threads * U_m each).  A block walks chunks blockIdx.x, +gridDim.x, ...
     // Its first chunk is interior whenever there are enough of them, and its
-    // loads are issued BEFORE the scalar prologue so they overlap it.
+    // loads are issued right after the scalar prologue's loads, before the
+    // prologue consumes them.
     const int nich = a.nich;
     int ch = blockIdx.x;
     int l[U];
     double rv[U], wv[U], dv[U];
     bool staged = false;
+    // the scalar loads go out first (L2-resident, ahead of the staged chunk)
+    K2Pre pre;
+    if constexpr (!INIT) cg_k2_load<kK2Threads, PC>(a.st, a.red, pre);
     if constexpr (ni > 0) {
         if (ch < nich) {
             k2_interior_idx<N, U>(a.E, ch, l);
@@ -155,7 +159,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
     double alpha = 0.0;
     int k = -1;               // INIT produces the partials of rho_0 as "iteration -1"
     if constexpr (!INIT) {
-        const CgStep c = cg_k2_prologue<kK2Threads, PC>(a.st, a.red, sred, alpha);
+        const CgStep c = cg_k2_finish<kK2Threads, PC>(a.st, a.red, sred, pre, alpha);
         if (c.done) return;
         k = c.k;
     }

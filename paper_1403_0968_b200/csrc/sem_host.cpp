@@ -532,6 +532,15 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         const bool force_hi = impl && strcmp(impl, "hi") == 0;
         dm.use_hi = !force_simple && !force_tma && hi_supported(N) && (force_hi || N >= hi_min);
         dm.use_tma = !force_simple && !dm.use_hi && tma_supported(N);
+        // DMMA contractions for N = 7 (default; SEM_AX_KERNEL=tma|hi|simple
+        // select the CUDA-core kernels); the TMA family serves every variant it
+        // does not cover (mass term, preconditioner, single reduction)
+        const bool force_dmma = impl && strcmp(impl, "dmma") == 0;
+        dm.use_dmma = dmma_supported(N) && (force_dmma || (!impl || !*impl));
+        if (dm.use_dmma) {
+            dm.use_hi = false;
+            dm.use_tma = true;
+        }
         if (dm.H && !dm.use_tma && !dm.use_hi) {   // only TMA / hi carry the mass term
             dm.use_hi = hi_supported(N) && N >= hi_min;
             dm.use_tma = !dm.use_hi && tma_supported(N);

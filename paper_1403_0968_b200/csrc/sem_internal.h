@@ -63,6 +63,7 @@ struct DevMesh {
     int nsm;                    // SM count of the device (persistent grids)
     bool use_tma;               // TMA element-staged Ax kernels (N <= kTmaMaxN)
     bool use_hi;                // TMA vector + register-streamed G^ kernels (high N)
+    bool use_dmma;              // N = 7: r/s contractions on the FP64 tensor cores (ax_dmma.cuh)
 };
 
 struct CgVecs {
@@ -145,6 +146,7 @@ cudaError_t launch_recip(const DevMesh &m, const double *d, double *dinv, cudaSt
 
 // ax_tma.cu
 bool tma_supported(int N);
+bool dmma_supported(int N);
 int tma_blocks(int N, int64_t E, int nsm, bool cg);
 cudaError_t tma_prepare(int N, bool mass);
 cudaError_t upload_const_D(int N, const double *D_host);

@@ -28,11 +28,13 @@ def relerr(a, b):
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
-@pytest.fixture(params=["tma", "hi", "simple", "tma-nograph", "tma-split", "hi-split"])
+@pytest.fixture(params=["tma", "hi", "simple", "tma-nograph", "tma-split", "hi-split", "dmma",
+                        "dmma-split"])
 def impl(request, monkeypatch):
     """All Ax kernel families -- element-staged TMA (N <= 10), vector-staged TMA
     with register-streamed G^ ("hi", N >= 6; lower N fall back to TMA), the
-    simple one-block-per-element kernel (all N) -- and the CG driver with and
+    simple one-block-per-element kernel (all N), the N = 7 DMMA kernel ("dmma";
+    other N fall back to the defaults) -- and the CG driver with and
     without CUDA-graph chunks.  "-split": K1 as two element-range launches
     (the multi-rank boundary/interior schedule, here without an exchange)."""
     monkeypatch.setenv("SEM_AX_KERNEL", request.param.split("-")[0])
