@@ -448,8 +448,13 @@ def main():
     k1_ms, k1_n, k1_bytes = prof["k1"]
     achieved = (k1_bytes / k1_n) / (k1_ms / k1_n * 1e-3) / 1e9 if k1_n else None
     k1_in_solve_us = 1e3 * k1_ms / k1_n if k1_n else None
-    traffic = ncu_traffic((f"ax_tma_kernel<{args.N}, true, false>", f"ax_tma_kernel<{args.N}, 1>")) \
-        if alpha is None else None
+    dmma = args.N == 7 and not os.environ.get("SEM_AX_KERNEL")
+    k1_name = ("K1: ax_dmma_kernel<CG=true> (N=7: r/s contractions on the FP64 tensor cores; "
+               "x/p update + Ax + (p,Ap) partials)" if dmma else
+               "K1: ax_tma_kernel<N,CG=true> (x/p update + Ax + (p,Ap) partials)")
+    traffic = ncu_traffic(("ax_dmma_kernel<1, 0, 0, 0>",) if dmma else
+                          (f"ax_tma_kernel<{args.N}, true, false>", f"ax_tma_kernel<{args.N}, 1>")) \
+        if alpha is None and args.precond == "none" and args.cg_variant == "standard" else None
     shares = {k: v[0] / prof_ms for k, v in prof.items() if v[1]}
     # every CG kernel inside the solve (per-launch CUDA events, profiled pass):
     # K2 reads the w K1 just wrote from L2, unlike its back-to-back replay
@@ -549,7 +554,7 @@ def main():
                              f"> {L2_BYTES / 2**20:.0f} MiB L2, streamed every iteration"},
             "ax": ax,
             "roofline": {"bound": "hbm",
-                         "kernel": "K1: ax_tma_kernel<N,CG=true> (x/p update + Ax + (p,Ap) partials)",
+                         "kernel": k1_name,
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
                          "peak_source": peak_src,

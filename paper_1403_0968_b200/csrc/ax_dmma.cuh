@@ -30,7 +30,10 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-template <bool CG, bool PC = false, bool DOT = false>
+// MASS: + h u with h = alpha w J (screened Coulomb, the h pointer in the field
+// the variant does not use, as ax_tma_kernel); PC: Jacobi PCG scalars; DOT:
+// KA of the single-reduction CG (plain apply + (u, w) partials).
+template <bool CG, bool MASS = false, bool PC = false, bool DOT = false>
 __global__ void __launch_bounds__(TmaLayout<7, CG>::NT, 1) ax_dmma_kernel(TmaArgs a) {
     constexpr int N = 7;
     using C = TmaCfg<N>;
@@ -256,9 +259,14 @@ __global__ void __launch_bounds__(TmaLayout<7, CG>::NT, 1) ax_dmma_kernel(TmaArg
             w0 += t0;
             w1 += t1;
             const int q = k * n2 + lq;
+            const double2 pv = *reinterpret_cast<const double2 *>(su + q);
+            if constexpr (MASS) {
+                const double2 hv = __ldg(reinterpret_cast<const double2 *>((CG ? a.u : a.r) + e * n3 + q));
+                w0 = fma(hv.x, pv.x, w0);
+                w1 = fma(hv.y, pv.y, w1);
+            }
             *reinterpret_cast<double2 *>(a.w + e * n3 + q) = make_double2(w0, w1);
             if constexpr (CG || DOT) {
-                const double2 pv = *reinterpret_cast<const double2 *>(su + q);
                 pap = fma(w0, pv.x, pap);
                 pap = fma(w1, pv.y, pap);
             }
@@ -274,6 +282,35 @@ __global__ void __launch_bounds__(TmaLayout<7, CG>::NT, 1) ax_dmma_kernel(TmaArg
         const double bs = block_sum<Lo::NT>(pap, sred);
         if (tid == 0) a.part1[(kit & 1) * a.red.s1 + blockIdx.x] = bs;
     }
+}
+
+// ---- launchers (instantiated by the translation unit of each variant) ----
+template <bool CG>
+static int dmma_grid(int64_t E, int nsm) {
+    const int64_t need = (E + TmaLayout<7, CG>::NG - 1) / TmaLayout<7, CG>::NG;
+    return (int)(need < nsm ? (need < 1 ? 1 : need) : nsm);
+}
+
+template <bool CG, bool MASS, bool PC, bool DOT>
+static cudaError_t dmma_attr() {
+    return cudaFuncSetAttribute(ax_dmma_kernel<CG, MASS, PC, DOT>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)TmaLayout<7, CG>::SMEM);
+}
+
+// plain apply (MASS: h in a.r)
+template <bool MASS, bool DOT = false>
+static cudaError_t launch_dmma_plain(const TmaArgs &a, int nsm, cudaStream_t s) {
+    ax_dmma_kernel<false, MASS, false, DOT>
+        <<<dmma_grid<false>(a.E, nsm), TmaLayout<7, false>::NT, TmaLayout<7, false>::SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
+// K1 over the element range of a (cg_args)
+template <bool MASS, bool PC>
+static cudaError_t launch_dmma_cg(const TmaArgs &a, int nsm, cudaStream_t s) {
+    return launch_pdl(ax_dmma_kernel<true, MASS, PC, false>, dmma_grid<true>(a.E, nsm),
+                      TmaLayout<7, true>::NT, TmaLayout<7, true>::SMEM, s, a);
 }
 
 }  // namespace sem

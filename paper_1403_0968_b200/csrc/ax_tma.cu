@@ -34,22 +34,12 @@ cudaError_t upload_const_D(int N, const double *D_host) {
 
 bool tma_supported(int N) { return N >= 1 && N <= kTmaMaxN; }
 bool dmma_supported(int N) { return N == 7; }
-
-template <bool CG>
-static int dmma_grid(int64_t E, int nsm) {
-    const int64_t need = (E + TmaLayout<7, CG>::NG - 1) / TmaLayout<7, CG>::NG;
-    return (int)(need < nsm ? (need < 1 ? 1 : need) : nsm);
-}
+bool hi_supported(int N) { return N >= 6 && N <= 15; }
 
 static cudaError_t dmma_prepare() {
-    cudaError_t e = cudaFuncSetAttribute(ax_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)TmaLayout<7, false>::SMEM);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(ax_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)TmaLayout<7, true>::SMEM);
-    return e;
+    cudaError_t e = dmma_attr<false, false, false, false>();
+    return e == cudaSuccess ? dmma_attr<true, false, false, false>() : e;
 }
-bool hi_supported(int N) { return N >= 6 && N <= 15; }
 
 int tma_blocks(int N, int64_t E, int nsm, bool cg) {
     int nb = 0;
@@ -89,9 +79,7 @@ cudaError_t launch_ax_tma(const DevMesh &m, const double *u, double *w, cudaStre
         a.G = m.G;
         a.u = u;
         a.w = w;
-        ax_dmma_kernel<false><<<dmma_grid<false>(m.E, m.nsm), TmaLayout<7, false>::NT,
-                                TmaLayout<7, false>::SMEM, s>>>(a);
-        return cudaGetLastError();
+        return launch_dmma_plain<false>(a, m.nsm, s);
     }
     return m.H ? launch_ax_tma_mass(m, u, w, s) : launch_ax_tma_t<false>(m, u, w, s);
 }
@@ -104,9 +92,7 @@ cudaError_t launch_ax_cg_tma(const DevMesh &m, const CgVecs &v, int64_t eb, int6
                              cudaStream_t s) {
     if (v.dinv) return launch_ax_cg_tma_pc(m, v, eb, ne, pidx0, s);
     if (m.use_dmma && !m.H) {
-        const TmaArgs a = cg_args<false>(m, v, eb, ne, pidx0);
-        return launch_pdl(ax_dmma_kernel<true>, dmma_grid<true>(ne, m.nsm), TmaLayout<7, true>::NT,
-                          TmaLayout<7, true>::SMEM, s, a);
+        return launch_dmma_cg<false, false>(cg_args<false>(m, v, eb, ne, pidx0), m.nsm, s);
     }
     return m.H ? launch_ax_cg_tma_mass(m, v, eb, ne, pidx0, s)
                : launch_ax_cg_tma_t<false>(m, v, eb, ne, pidx0, s);

@@ -5,13 +5,17 @@
 // translation unit (and its own __constant__ copy of D) so the CG kernels keep
 // their code and the variants compile in parallel.
 #include "ax_tma.cuh"
+#include "ax_dmma.cuh"
 
 namespace sem {
 
 cudaError_t upload_const_D_pc(int N, const double *D_host) { return upload_D_this_tu(N, D_host); }
 
 cudaError_t tma_prepare_pc(int N, bool mass) {
-    return mass ? tma_prepare_t<true, true>(N) : tma_prepare_t<false, true>(N);
+    cudaError_t e = mass ? tma_prepare_t<true, true>(N) : tma_prepare_t<false, true>(N);
+    if (e == cudaSuccess && N == 7)
+        e = mass ? dmma_attr<true, true, true, false>() : dmma_attr<true, false, true, false>();
+    return e;
 }
 
 cudaError_t hi_prepare_pc(int N, bool mass) {
@@ -21,6 +25,9 @@ cudaError_t hi_prepare_pc(int N, bool mass) {
 
 cudaError_t launch_ax_cg_tma_pc(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne,
                                 int pidx0, cudaStream_t s) {
+    if (m.use_dmma)
+        return m.H ? launch_dmma_cg<true, true>(cg_args<true>(m, v, eb, ne, pidx0), m.nsm, s)
+                   : launch_dmma_cg<false, true>(cg_args<false>(m, v, eb, ne, pidx0), m.nsm, s);
     return m.H ? launch_ax_cg_tma_t<true, true>(m, v, eb, ne, pidx0, s)
                : launch_ax_cg_tma_t<false, true>(m, v, eb, ne, pidx0, s);
 }

@@ -3,12 +3,14 @@
 // with the DOT flag, w = A_L r plus per-CTA partials of (r, w).  Poisson
 // operator.  Its own translation unit and __constant__ copy of D.
 #include "ax_tma.cuh"
+#include "ax_dmma.cuh"
 
 namespace sem {
 
 cudaError_t upload_const_D_sr(int N, const double *D_host) { return upload_D_this_tu(N, D_host); }
 
 cudaError_t sr_prepare(const DevMesh &m) {
+    if (m.use_dmma) return dmma_attr<false, false, false, true>();
     if (m.use_hi) return hi_prepare_dot(m.N);
     if (m.use_tma) return tma_prepare_dot(m.N);
     return cudaErrorInvalidValue;
@@ -18,7 +20,9 @@ cudaError_t sr_prepare(const DevMesh &m) {
 // these; the CG kernel K1 has its own, larger or equal, grid)
 int ka_blocks(const DevMesh &m) {
     int nb = 0;
-    if (m.use_hi) {
+    if (m.use_dmma) {
+        nb = dmma_grid<false>(m.E, m.nsm);
+    } else if (m.use_hi) {
         SEM_HI_DISPATCH(m.N, nb = hi_grid<NN, false>(m.E, m.nsm));
     } else if (m.use_tma) {
         SEM_TMA_DISPATCH(m.N, nb = tma_grid<NN, false>(m.E, m.nsm));
@@ -27,6 +31,7 @@ int ka_blocks(const DevMesh &m) {
 }
 
 cudaError_t launch_ax_dot(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
+    if (m.use_dmma) return launch_dmma_plain<false, true>(sr_args(m, v), m.nsm, s);
     if (m.use_hi) return launch_ax_dot_hi_t(m, v, s);
     if (m.use_tma) return launch_ax_dot_tma_t(m, v, s);
     return cudaErrorInvalidValue;
