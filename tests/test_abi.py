@@ -199,3 +199,13 @@ def test_fd_host_calls(L, oracle):
     assert L.fd2d_step(ctypes.c_void_p(264), ctypes.c_void_p(512), ctypes.c_void_p(768), 16, 16,
                        1, om, 0.1, None) == sem.SEM_EINVAL   # misaligned
     assert L.fd_weights(0, 1.0, om) == sem.SEM_EINVAL
+
+
+def test_no_undefined_internal_symbols(L):
+    """Every internal (namespace sem) symbol the library references is defined
+    in it: a missing one only shows at dlopen time on the GPU box."""
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--undefined-only", sem.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    missing = [ln for ln in out.splitlines() if "_ZN3sem" in ln or "_ZN6sem_fd" in ln]
+    assert not missing, missing
