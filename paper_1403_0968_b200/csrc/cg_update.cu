@@ -42,6 +42,7 @@ struct K2Args {
 
 constexpr int kK2Threads = 256;
 constexpr int kK2BlocksPerSM = 3;
+constexpr int kK2IntU = 4;           // element-interior nodes per thread per chunk
 
 // groups per thread in one chunk, by multiplicity
 __host__ __device__ constexpr int k2_upb(int m) {
@@ -122,7 +123,7 @@ __device__ __forceinline__ void k2_interior_idx(int64_t E, int chunk, int (&l)[U
 template <int N, bool INIT, bool PC>
 __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __grid_constant__ K2Args a) {
     constexpr int ni = N - 1;
-    constexpr int U = 4;
+    constexpr int U = kK2IntU;
     __shared__ double sred[3 * (kK2Threads / 32)];
     if constexpr (!INIT) pdl_trigger();
     if constexpr (!INIT) pdl_wait();
@@ -297,7 +298,7 @@ cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t
     // chunk table: interior chunks first, then the group classes (Dirichlet
     // classes only at INIT)
     const int64_t nint = m.E * int64_t(m.N - 1) * (m.N - 1) * (m.N - 1);
-    a.nich = (int)((nint + 4 * kK2Threads - 1) / (4 * kK2Threads));
+    a.nich = (int)((nint + kK2IntU * kK2Threads - 1) / (kK2IntU * kK2Threads));
     int nch = 0;
     for (int c = 0; c < m.cls.n; ++c) {
         a.cchunk[c] = nch;
