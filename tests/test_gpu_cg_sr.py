@@ -162,3 +162,18 @@ def test_c3_cg_sr_full_size(dev):
     assert ok and st == 0
     assert abs(its - its_r) <= 2, (its, its_r, rel, rel_r)
     assert relerr(x.cpu().numpy(), xr) <= 1e-9
+
+
+@pytest.mark.parametrize("N", [3, 7])
+def test_cg_sr_relabelled_mesh(dev, N):
+    from paper_1403_0968_b200 import sem
+    xi, _ = oracle.gll(N)
+    m = meshgen.relabel(meshgen.box_mesh(N, xi, elems=(3, 3, 2), eps=0.05), seed=12)
+    G, J = oracle.geom(N, m.xyz)
+    ctx = sem.Context(m, N, device=0)
+    b = rhs(m, J)
+    x, its, rel, ok = ctx.cg(T(b, dev), tol=1e-8, maxit=2000, variant=SR)
+    xr, its_r, rel_r, st = oracle.cg_single_reduction(N, m.glo, m.dirichlet, G, b, tol=1e-8,
+                                                      maxit=2000)
+    assert ok and st == 0 and its == its_r, (its, its_r)
+    assert relerr(x.cpu().numpy(), xr) <= 1e-10
