@@ -1,0 +1,192 @@
+// ax_dmmag.cuh -- the plain Ax apply for N = 8..11 with the r/s contractions on
+// the FP64 tensor cores: the N = 7 recipe (ax_dmma.cuh) on n x n k-slices with
+// 9 <= n <= 12, covered by a 2 x 2 grid of 8 x 8 DMMA tiles (nodes outside the
+// slice masked) and ceil(n/4) k-steps of 4 (D fragments zero beyond n).
+// Element-staged by TMA like ax_tma_kernel (P and G^ of one element per
+// stage, double-buffered); a group of 8 warps works on one element: warp w owns
+// tile (w & 3) of the k-slices of parity w >> 2.  The CUDA-core kernels at these
+// orders are register/latency-bound (c4 fractions 0.68 / 0.70 / 0.44 / 0.43).
+// SLICE: G^ in the slice-major layout [k][6][n^2] of the high-order kernel.
+#pragma once
+#include "ax_tma.cuh"
+#include "ax_dmma.cuh"
+
+namespace sem {
+
+template <int N>
+struct DgCfg {
+    static constexpr int n = N + 1, n2 = n * n, n3 = n2 * n;
+    static constexpr int KS = (n + 3) / 4;                  // k-steps of the contractions
+    static constexpr int VL = ((n3 + 2 + 1) / 2) * 2;      // vector slot (doubles, even)
+    static constexpr int STAGE = VL + 6 * n3;              // u + G^ of one element
+    static constexpr int SMEM_MAX = 227 * 1024 - 1024;
+    static constexpr int NG_FIT = SMEM_MAX / (2 * STAGE * 8);
+    static constexpr int NG = NG_FIT > 2 ? 2 : NG_FIT;      // groups of 8 warps per CTA
+    static constexpr int GT = 256;
+    static constexpr int NT = NG * GT;
+    static constexpr size_t SMEM = size_t(NG) * 2 * STAGE * 8 + 128;
+    static_assert(n >= 9 && n <= 16 && NG >= 1, "2 x 2 tiles of 8, one element per stage");
+};
+
+template <int N, bool SLICE>
+__global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
+    using C = DgCfg<N>;
+    constexpr int n = C::n, n2 = C::n2, n3 = C::n3, KS = C::KS, VL = C::VL, STAGE = C::STAGE;
+    constexpr int NG = C::NG, GT = C::GT;
+    constexpr int DO = d_off(N);
+    extern __shared__ __align__(128) double smem[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + size_t(NG) * 2 * STAGE);
+
+    const int tid = threadIdx.x;
+    const int g = tid / GT;
+    const int gt = tid - g * GT;
+    const int warp = gt >> 5, lane = gt & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int tp = warp & 3, hpar = warp >> 2;
+    const int jt = tp >> 1, it = tp & 1;
+    const int j = jt * 8 + gid;                 // the lane's node row
+    const int i0 = it * 8 + 2 * tig;            // and its node pair (i0, i0+1)
+    const bool vj = j < n, v0 = vj && i0 < n, v1 = vj && i0 + 1 < n;
+    const bool leader = (gt == 0);
+    double *stage0 = smem + size_t(g) * 2 * STAGE;
+    uint64_t *gbar = bars + 2 * g;
+
+    const int64_t nunits = a.E;
+    const int64_t TG = int64_t(gridDim.x) * NG;
+    const int64_t u0 = int64_t(blockIdx.x) * NG + g;
+    const int64_t L = a.E * n3;
+
+    if (leader) {
+        mbar_init(gbar + 0, 1);
+        mbar_init(gbar + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint64_t pol = policy_evict_first();
+    auto issue = [&](int64_t e, int s) {
+        const int64_t first = e * n3;
+        const VecRange vr = vec_range(first, n3, L);
+        const uint32_t vb = (uint32_t)((vr.a1 - vr.a0) * 8), gb = (uint32_t)(6 * n3 * 8);
+        double *sb = stage0 + size_t(s) * STAGE;
+        mbar_expect_tx_only(gbar + s, vb + gb);
+        bulk_g2s(sb + VL, a.G + e * 6 * n3, gb, gbar + s, pol);
+        for (int64_t q = vr.a1; q < first + n3; ++q) sb[q - vr.a0] = __ldg(a.u + q);
+        mbar_arrive(gbar + s);
+        bulk_g2s(sb, a.u + vr.a0, vb, gbar + s, pol);
+    };
+    if (leader) {
+        if (u0 < nunits) issue(u0, 0);
+        if (u0 + TG < nunits) issue(u0 + TG, 1);
+    }
+
+    // D fragments: B of u_r = D[i][m], A of u_s = D[j][m], B of w_r = D[m][i],
+    // A of w_s = D[m][j]; rows / columns beyond n are zero
+    double urB[KS], usA[KS], wrB[KS], wsA[KS];
+    const int ib = it * 8 + gid, jb = jt * 8 + gid;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+        const int m = 4 * ks + tig;
+        urB[ks] = (ib < n && m < n) ? c_D[DO + ib * n + m] : 0.0;
+        usA[ks] = (jb < n && m < n) ? c_D[DO + jb * n + m] : 0.0;
+        wrB[ks] = (ib < n && m < n) ? c_D[DO + m * n + ib] : 0.0;
+        wsA[ks] = (jb < n && m < n) ? c_D[DO + m * n + jb] : 0.0;
+    }
+    // G^ factor f of node (k, jj, ii) within the staged element
+    auto gidx = [&](int f, int k, int jj, int ii) -> int {
+        return SLICE ? k * 6 * n2 + f * n2 + jj * n + ii : f * n3 + k * n2 + jj * n + ii;
+    };
+
+    int t = 0;
+    for (int64_t e = u0; e < nunits; e += TG, ++t) {
+        const int s = t & 1;
+        double *sb = stage0 + size_t(s) * STAGE;
+        const int sh = (int)((e * n3) & 1);
+        mbar_wait(gbar + s, (t >> 1) & 1);
+        const double *su = sb + sh;
+        double *sG = sb + VL;
+
+        double c0v[n], c1v[n];                  // the lane's two input columns
+#pragma unroll
+        for (int m = 0; m < n; ++m) {
+            c0v[m] = v0 ? su[m * n2 + j * n + i0] : 0.0;
+            c1v[m] = v1 ? su[m * n2 + j * n + i0 + 1] : 0.0;
+        }
+        // ---- phase A on the warp's tile of its slices ----
+        for (int k = hpar; k < n; k += 2) {
+            const double *uk = su + k * n2;
+            double r0 = 0.0, r1 = 0.0, s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                const int m = 4 * ks + tig;
+                const double aa = (jb < n && m < n) ? uk[jb * n + m] : 0.0;   // P_k[j][m]
+                const double bb = (ib < n && m < n) ? uk[m * n + ib] : 0.0;   // P_k[m][i]
+                dmma(r0, r1, aa, urB[ks]);
+                dmma(s0, s1, usA[ks], bb);
+            }
+            double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < n; ++m) {
+                const double d = c_D[DO + k * n + m];
+                t0 = fma(d, c0v[m], t0);
+                t1 = fma(d, c1v[m], t1);
+            }
+            if (v0) {
+                const double g0 = sG[gidx(0, k, j, i0)], g1 = sG[gidx(1, k, j, i0)];
+                const double g2 = sG[gidx(2, k, j, i0)], g3 = sG[gidx(3, k, j, i0)];
+                const double g4 = sG[gidx(4, k, j, i0)], g5 = sG[gidx(5, k, j, i0)];
+                sG[gidx(0, k, j, i0)] = g0 * r0 + g1 * s0 + g2 * t0;
+                sG[gidx(1, k, j, i0)] = g1 * r0 + g3 * s0 + g4 * t0;
+                sG[gidx(2, k, j, i0)] = g2 * r0 + g4 * s0 + g5 * t0;
+            }
+            if (v1) {
+                const double g0 = sG[gidx(0, k, j, i0 + 1)], g1 = sG[gidx(1, k, j, i0 + 1)];
+                const double g2 = sG[gidx(2, k, j, i0 + 1)], g3 = sG[gidx(3, k, j, i0 + 1)];
+                const double g4 = sG[gidx(4, k, j, i0 + 1)], g5 = sG[gidx(5, k, j, i0 + 1)];
+                sG[gidx(0, k, j, i0 + 1)] = g0 * r1 + g1 * s1 + g2 * t1;
+                sG[gidx(1, k, j, i0 + 1)] = g1 * r1 + g3 * s1 + g4 * t1;
+                sG[gidx(2, k, j, i0 + 1)] = g2 * r1 + g4 * s1 + g5 * t1;
+            }
+        }
+        group_bar(1 + g, GT);
+
+        // ---- phase B ----
+        double f0v[n], f1v[n];
+#pragma unroll
+        for (int m = 0; m < n; ++m) {
+            f0v[m] = v0 ? sG[gidx(2, m, j, i0)] : 0.0;
+            f1v[m] = v1 ? sG[gidx(2, m, j, i0 + 1)] : 0.0;
+        }
+        for (int k = hpar; k < n; k += 2) {
+            double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                const int m = 4 * ks + tig;
+                const double aa = (jb < n && m < n) ? sG[gidx(0, k, jb, m)] : 0.0;   // F_r,k[j][m]
+                const double bb = (ib < n && m < n) ? sG[gidx(1, k, m, ib)] : 0.0;   // F_s,k[m][i]
+                dmma(w0, w1, aa, wrB[ks]);
+                dmma(w0, w1, wsA[ks], bb);
+            }
+            double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < n; ++m) {
+                const double d = c_D[DO + m * n + k];
+                t0 = fma(d, f0v[m], t0);
+                t1 = fma(d, f1v[m], t1);
+            }
+            double *wo = a.w + e * n3 + k * n2 + j * n + i0;
+            if (v0) wo[0] = w0 + t0;
+            if (v1) wo[1] = w1 + t1;
+        }
+        fence_proxy_async();
+        group_bar(1 + g, GT);
+        if (leader && e + 2 * TG < nunits) issue(e + 2 * TG, s);
+    }
+}
+
+template <int N>
+static int dmmag_grid(int64_t E, int nsm) {
+    const int64_t need = (E + DgCfg<N>::NG - 1) / DgCfg<N>::NG;
+    return (int)(need < nsm ? (need < 1 ? 1 : need) : nsm);
+}
+
+}  // namespace sem

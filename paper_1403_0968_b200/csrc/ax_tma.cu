@@ -3,6 +3,7 @@
 // forwarded to ax_tma_mass.cu.
 #include "ax_tma.cuh"
 #include "ax_dmma.cuh"
+#include "ax_dmmag.cuh"
 
 namespace sem {
 
@@ -35,6 +36,44 @@ cudaError_t upload_const_D(int N, const double *D_host) {
 bool tma_supported(int N) { return N >= 1 && N <= kTmaMaxN; }
 bool dmma_supported(int N) { return N == 7; }
 bool hi_supported(int N) { return N >= 6 && N <= 15; }
+bool dmmag_supported(int N) { return N >= 8 && N <= 11; }
+
+#define SEM_DG_DISPATCH(N_, ...)                                             \
+    switch (N_) {                                                            \
+    case 8: { constexpr int NN = 8; __VA_ARGS__; } break;                    \
+    case 9: { constexpr int NN = 9; __VA_ARGS__; } break;                    \
+    case 10: { constexpr int NN = 10; __VA_ARGS__; } break;                  \
+    case 11: { constexpr int NN = 11; __VA_ARGS__; } break;                  \
+    default: break;                                                          \
+    }
+
+cudaError_t dmmag_prepare(int N) {
+    cudaError_t e = cudaSuccess;
+    SEM_DG_DISPATCH(N, (e = cudaFuncSetAttribute(ax_dmmag_kernel<NN, false>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)DgCfg<NN>::SMEM),
+                        e = (e == cudaSuccess ? cudaFuncSetAttribute(ax_dmmag_kernel<NN, true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)DgCfg<NN>::SMEM) : e)));
+    return e;
+}
+
+// plain Ax at N = 8..11 on the tensor cores (G^ in either layout)
+cudaError_t launch_ax_dmmag(const DevMesh &m, const double *u, double *w, cudaStream_t s) {
+    TmaArgs a{};
+    a.E = m.E;
+    a.G = m.G;
+    a.u = u;
+    a.w = w;
+    if (m.use_hi) {
+        SEM_DG_DISPATCH(m.N, (ax_dmmag_kernel<NN, true><<<dmmag_grid<NN>(m.E, m.nsm), DgCfg<NN>::NT,
+                                                           DgCfg<NN>::SMEM, s>>>(a)));
+    } else {
+        SEM_DG_DISPATCH(m.N, (ax_dmmag_kernel<NN, false><<<dmmag_grid<NN>(m.E, m.nsm), DgCfg<NN>::NT,
+                                                            DgCfg<NN>::SMEM, s>>>(a)));
+    }
+    return cudaGetLastError();
+}
 
 static cudaError_t dmma_prepare() {
     cudaError_t e = dmma_attr<false, false, false, false>();

@@ -64,6 +64,7 @@ struct DevMesh {
     bool use_tma;               // TMA element-staged Ax kernels (N <= kTmaMaxN)
     bool use_hi;                // TMA vector + register-streamed G^ kernels (high N)
     bool use_dmma;              // N = 7: r/s contractions on the FP64 tensor cores (ax_dmma.cuh)
+    bool use_dmmag;             // N = 8..11: the plain Ax on the tensor cores (ax_dmmag.cuh)
 };
 
 struct CgVecs {
@@ -147,6 +148,9 @@ cudaError_t launch_recip(const DevMesh &m, const double *d, double *dinv, cudaSt
 // ax_tma.cu
 bool tma_supported(int N);
 bool dmma_supported(int N);
+bool dmmag_supported(int N);
+cudaError_t dmmag_prepare(int N);
+cudaError_t launch_ax_dmmag(const DevMesh &m, const double *u, double *w, cudaStream_t s);
 int tma_blocks(int N, int64_t E, int nsm, bool cg);
 cudaError_t tma_prepare(int N, bool mass);
 cudaError_t upload_const_D(int N, const double *D_host);

@@ -513,6 +513,7 @@ cudaError_t launch_geom(const DevMesh &m, const double *xyz, const double *kappa
 
 cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t s) {
     if (m.E == 0) return cudaSuccess;
+    if (m.use_dmmag && !m.H) return launch_ax_dmmag(m, u, w, s);
     if (m.use_hi) return launch_ax_hi(m, u, w, s);
     if (m.use_tma) return launch_ax_tma(m, u, w, s);
     if (m.H) return cudaErrorInvalidValue;      // the simple kernel has no mass term
