@@ -1,4 +1,4 @@
-// ax_dmmag.cuh -- the plain Ax apply for N = 8..11 with the r/s contractions on
+// ax_dmmag.cuh -- the plain Ax apply for N = 8..14 with the r/s contractions on
 // the FP64 tensor cores: the N = 7 recipe (ax_dmma.cuh) on n x n k-slices with
 // 9 <= n <= 12, covered by a 2 x 2 grid of 8 x 8 DMMA tiles (nodes outside the
 // slice masked) and ceil(n/4) k-steps of 4 (D fragments zero beyond n).
@@ -20,11 +20,14 @@ struct DgCfg {
     static constexpr int VL = ((n3 + 2 + 1) / 2) * 2;      // vector slot (doubles, even)
     static constexpr int STAGE = VL + 6 * n3;              // u + G^ of one element
     static constexpr int SMEM_MAX = 227 * 1024 - 1024;
-    static constexpr int NG_FIT = SMEM_MAX / (2 * STAGE * 8);
+    // double-buffered while two stages fit (n <= 12), else one stage (n <= 15):
+    // the next element's copies then start after the current one is done
+    static constexpr int NS = (2 * STAGE * 8 <= SMEM_MAX) ? 2 : 1;
+    static constexpr int NG_FIT = SMEM_MAX / (NS * STAGE * 8);
     static constexpr int NG = NG_FIT > 2 ? 2 : NG_FIT;      // groups of 8 warps per CTA
     static constexpr int GT = 256;
     static constexpr int NT = NG * GT;
-    static constexpr size_t SMEM = size_t(NG) * 2 * STAGE * 8 + 128;
+    static constexpr size_t SMEM = size_t(NG) * NS * STAGE * 8 + 128;
     static_assert(n >= 9 && n <= 16 && NG >= 1, "2 x 2 tiles of 8, one element per stage");
 };
 
@@ -32,10 +35,10 @@ template <int N, bool SLICE>
 __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
     using C = DgCfg<N>;
     constexpr int n = C::n, n2 = C::n2, n3 = C::n3, KS = C::KS, VL = C::VL, STAGE = C::STAGE;
-    constexpr int NG = C::NG, GT = C::GT;
+    constexpr int NG = C::NG, GT = C::GT, NS = C::NS;
     constexpr int DO = d_off(N);
     extern __shared__ __align__(128) double smem[];
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + size_t(NG) * 2 * STAGE);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + size_t(NG) * NS * STAGE);
 
     const int tid = threadIdx.x;
     const int g = tid / GT;
@@ -48,7 +51,7 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
     const int i0 = it * 8 + 2 * tig;            // and its node pair (i0, i0+1)
     const bool vj = j < n, v0 = vj && i0 < n, v1 = vj && i0 + 1 < n;
     const bool leader = (gt == 0);
-    double *stage0 = smem + size_t(g) * 2 * STAGE;
+    double *stage0 = smem + size_t(g) * NS * STAGE;
     uint64_t *gbar = bars + 2 * g;
 
     const int64_t nunits = a.E;
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
     };
     if (leader) {
         if (u0 < nunits) issue(u0, 0);
-        if (u0 + TG < nunits) issue(u0 + TG, 1);
+        if (NS == 2 && u0 + TG < nunits) issue(u0 + TG, 1);
     }
 
     // D fragments: B of u_r = D[i][m], A of u_s = D[j][m], B of w_r = D[m][i],
@@ -98,10 +101,10 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
 
     int t = 0;
     for (int64_t e = u0; e < nunits; e += TG, ++t) {
-        const int s = t & 1;
+        const int s = NS == 2 ? (t & 1) : 0;
         double *sb = stage0 + size_t(s) * STAGE;
         const int sh = (int)((e * n3) & 1);
-        mbar_wait(gbar + s, (t >> 1) & 1);
+        mbar_wait(gbar + s, NS == 2 ? (t >> 1) & 1 : t & 1);
         const double *su = sb + sh;
         double *sG = sb + VL;
 
@@ -179,7 +182,7 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
         }
         fence_proxy_async();
         group_bar(1 + g, GT);
-        if (leader && e + 2 * TG < nunits) issue(e + 2 * TG, s);
+        if (leader && e + NS * TG < nunits) issue(e + NS * TG, s);
     }
 }
 
