@@ -36,7 +36,7 @@ cudaError_t upload_const_D(int N, const double *D_host) {
 bool tma_supported(int N) { return N >= 1 && N <= kTmaMaxN; }
 bool dmma_supported(int N) { return N == 7; }
 bool hi_supported(int N) { return N >= 6 && N <= 15; }
-bool dmmag_supported(int N) { return N >= 8 && N <= 11; }
+bool dmmag_supported(int N) { return N >= 8 && N <= 15; }
 
 #define SEM_DG_DISPATCH(N_, ...)                                             \
     switch (N_) {                                                            \
@@ -44,6 +44,10 @@ bool dmmag_supported(int N) { return N >= 8 && N <= 11; }
     case 9: { constexpr int NN = 9; __VA_ARGS__; } break;                    \
     case 10: { constexpr int NN = 10; __VA_ARGS__; } break;                  \
     case 11: { constexpr int NN = 11; __VA_ARGS__; } break;                  \
+    case 12: { constexpr int NN = 12; __VA_ARGS__; } break;                  \
+    case 13: { constexpr int NN = 13; __VA_ARGS__; } break;                  \
+    case 14: { constexpr int NN = 14; __VA_ARGS__; } break;                  \
+    case 15: { constexpr int NN = 15; __VA_ARGS__; } break;                  \
     default: break;                                                          \
     }
 

@@ -547,7 +547,7 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         // of 8 waste 68% / 61% of the DMMA work there); SEM_DMMAG=1 forces it
         // for 8..14, SEM_DMMAG=0 disables it; K1 keeps the CUDA-core kernels
         const char *dg = getenv("SEM_DMMAG");
-        const bool dg_on = dg ? dg[0] == '1' : (force_dmma || !impl || !*impl) && N >= 10;
+        const bool dg_on = dg ? dg[0] == '1' : (force_dmma || !impl || !*impl) && N >= 10 && N <= 14;
         dm.use_dmmag = dmmag_supported(N) && (dm.use_tma || dm.use_hi) && dg_on;
         if (dm.H && !dm.use_tma && !dm.use_hi) {   // only TMA / hi carry the mass term
             dm.use_hi = hi_supported(N) && N >= hi_min;
