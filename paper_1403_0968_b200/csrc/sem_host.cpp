@@ -543,11 +543,11 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         }
         // the plain Ax at N = 8..14 on the tensor cores: default where it wins
         // (c4: N=10 0.47 vs 0.44, 11 0.58 vs 0.43, 12 0.44 vs 0.30, 13 0.39 vs
-        // 0.36, 14 0.47 vs 0.29; N=8, 9 lose to the TMA kernel, the 2x2 tiles
+        // 0.36, 14 0.47 vs 0.29, 15 0.51 vs 0.38; N=8, 9 lose to the TMA kernel, the 2x2 tiles
         // of 8 waste 68% / 61% of the DMMA work there); SEM_DMMAG=1 forces it
         // for 8..14, SEM_DMMAG=0 disables it; K1 keeps the CUDA-core kernels
         const char *dg = getenv("SEM_DMMAG");
-        const bool dg_on = dg ? dg[0] == '1' : (force_dmma || !impl || !*impl) && N >= 10 && N <= 14;
+        const bool dg_on = dg ? dg[0] == '1' : (force_dmma || !impl || !*impl) && N >= 10;
         dm.use_dmmag = dmmag_supported(N) && (dm.use_tma || dm.use_hi) && dg_on;
         if (dm.H && !dm.use_tma && !dm.use_hi) {   // only TMA / hi carry the mass term
             dm.use_hi = hi_supported(N) && N >= hi_min;

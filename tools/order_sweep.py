@@ -63,7 +63,7 @@ for N in args.orders:
            "ax_us": us, "ax_gdof_s": L / (us * 1e-6) / 1e9, "ax_gbs": gbs, "ax_frac": gbs / peak,
            "ax_tflops": flops / (us * 1e-6) / 1e12,
            "kernel": os.environ.get("SEM_AX_KERNEL") or (
-               "ax_dmma_kernel" if N == 7 else "ax_dmmag_kernel" if 10 <= N <= 14 else
+               "ax_dmma_kernel" if N == 7 else "ax_dmmag_kernel" if N >= 10 else
                "ax_tma_kernel" if N <= 10 else "ax_hi_kernel"),
            "cg_us_per_it": cg_us, "cg_gdof_s": L / (cg_us * 1e-6) / 1e9,
            "setup_s": time.time() - t0}
