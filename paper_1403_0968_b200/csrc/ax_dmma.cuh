@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(TmaLayout<7, CG>::NT, 1) ax_dmma_kernel(TmaArg
 
     const int64_t nunits = a.E;
     const int64_t TG = int64_t(gridDim.x) * NG;
-    const int64_t u0 = int64_t(blockIdx.x) * NG + g;
+    // group-major: the extra elements of the last round land on different SMs
+    const int64_t u0 = int64_t(g) * gridDim.x + blockIdx.x;
     const int64_t L = a.E * n3;
 
     if (leader) {
