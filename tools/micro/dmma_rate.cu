@@ -1,3 +1,4 @@
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 dmma_rate.cu -o dmma_rate
 // Microbenchmark: FP64 DMMA (mma.sync m8n8k4 f64) vs DFMA issue rate on sm_100a.
 #include <cstdio>
 #include <cuda_runtime.h>
