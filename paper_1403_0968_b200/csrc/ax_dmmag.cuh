@@ -77,6 +77,29 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
         mbar_arrive(gbar + s);
         bulk_g2s(sb, a.u + vr.a0, vb, gbar + s, pol);
     };
+    // One stage, slice-major G^, even n: the next element's copies in two
+    // halves -- u and the factors 3..5 of every slice (not read after phase A)
+    // as soon as phase A is done, the factors 0..2 (f_r, f_s, f_t during phase
+    // B) after phase B -- so half the load overlaps phase B.  3 n^2 doubles
+    // per slice half: a multiple of 16 bytes for even n.
+    constexpr bool SPLIT = NS == 1 && SLICE && (n % 2 == 0);
+    auto issue_a = [&](int64_t e) {
+        const int64_t first = e * n3;
+        const VecRange vr = vec_range(first, n3, L);
+        const uint32_t vb = (uint32_t)((vr.a1 - vr.a0) * 8), hb = (uint32_t)(3 * n2 * 8);
+        double *sb = stage0;
+        mbar_expect_tx_only(gbar, vb + 2 * n * hb);
+        for (int64_t q = vr.a1; q < first + n3; ++q) sb[q - vr.a0] = __ldg(a.u + q);
+        mbar_arrive(gbar);
+        bulk_g2s(sb, a.u + vr.a0, vb, gbar, pol);
+        for (int k = 0; k < n; ++k)
+            bulk_g2s(sb + VL + k * 6 * n2 + 3 * n2, a.G + e * 6 * n3 + k * 6 * n2 + 3 * n2, hb, gbar, pol);
+    };
+    auto issue_b = [&](int64_t e) {
+        const uint32_t hb = (uint32_t)(3 * n2 * 8);
+        for (int k = 0; k < n; ++k)
+            bulk_g2s(stage0 + VL + k * 6 * n2, a.G + e * 6 * n3 + k * 6 * n2, hb, gbar, pol);
+    };
     if (leader) {
         if (u0 < nunits) issue(u0, 0);
         if (NS == 2 && u0 + TG < nunits) issue(u0 + TG, 1);
@@ -150,7 +173,11 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
                 sG[gidx(2, k, j, i0 + 1)] = g2 * r1 + g4 * s1 + g5 * t1;
             }
         }
+        if constexpr (SPLIT) fence_proxy_async();   // generic reads of u, G^ 3..5 done
         group_bar(1 + g, GT);
+        if constexpr (SPLIT) {
+            if (leader && e + TG < nunits) issue_a(e + TG);
+        }
 
         // ---- phase B ----
         double f0v[n], f1v[n];
@@ -182,7 +209,11 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
         }
         fence_proxy_async();
         group_bar(1 + g, GT);
-        if (leader && e + NS * TG < nunits) issue(e + NS * TG, s);
+        if constexpr (SPLIT) {
+            if (leader && e + TG < nunits) issue_b(e + TG);
+        } else {
+            if (leader && e + NS * TG < nunits) issue(e + NS * TG, s);
+        }
     }
 }
 
