@@ -77,26 +77,32 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
         mbar_arrive(gbar + s);
         bulk_g2s(sb, a.u + vr.a0, vb, gbar + s, pol);
     };
-    // One stage, slice-major G^, even n: the next element's copies in two
-    // halves -- u and the factors 3..5 of every slice (not read after phase A)
-    // as soon as phase A is done, the factors 0..2 (f_r, f_s, f_t during phase
-    // B) after phase B -- so half the load overlaps phase B.  3 n^2 doubles
-    // per slice half: a multiple of 16 bytes for even n.
-    constexpr bool SPLIT = NS == 1 && SLICE && (n % 2 == 0);
+    // One stage, slice-major G^: the next element's copies in two halves --
+    // u and the factors 3..5 of every slice (not read after phase A) as soon
+    // as phase A is done, the factors 0..2 (f_r, f_s, f_t during phase B)
+    // after phase B -- so half the load overlaps phase B.  Bulk copies need
+    // 16-byte sizes and addresses: for odd n^2 the second half starts one
+    // double late (3 n^2 - 1 doubles) and the first takes that double along
+    // (3 n^2 + 1; it is factor 3 of node 0, not read in phase B).
+    constexpr bool SPLIT = NS == 1 && SLICE;
+    constexpr int HO = n2 & 1;                  // 0 (even n) or 1 (odd n)
     auto issue_a = [&](int64_t e) {
         const int64_t first = e * n3;
         const VecRange vr = vec_range(first, n3, L);
-        const uint32_t vb = (uint32_t)((vr.a1 - vr.a0) * 8), hb = (uint32_t)(3 * n2 * 8);
+        const uint32_t vb = (uint32_t)((vr.a1 - vr.a0) * 8);
+        const uint32_t hb = (uint32_t)((3 * n2 - HO) * 8);
         double *sb = stage0;
-        mbar_expect_tx_only(gbar, vb + 2 * n * hb);
+        mbar_expect_tx_only(gbar, vb + (uint32_t)(6 * n3 * 8));
         for (int64_t q = vr.a1; q < first + n3; ++q) sb[q - vr.a0] = __ldg(a.u + q);
         mbar_arrive(gbar);
         bulk_g2s(sb, a.u + vr.a0, vb, gbar, pol);
-        for (int k = 0; k < n; ++k)
-            bulk_g2s(sb + VL + k * 6 * n2 + 3 * n2, a.G + e * 6 * n3 + k * 6 * n2 + 3 * n2, hb, gbar, pol);
+        for (int k = 0; k < n; ++k) {
+            const int o = k * 6 * n2 + 3 * n2 + HO;
+            bulk_g2s(sb + VL + o, a.G + e * 6 * n3 + o, hb, gbar, pol);
+        }
     };
     auto issue_b = [&](int64_t e) {
-        const uint32_t hb = (uint32_t)(3 * n2 * 8);
+        const uint32_t hb = (uint32_t)((3 * n2 + HO) * 8);
         for (int k = 0; k < n; ++k)
             bulk_g2s(stage0 + VL + k * 6 * n2, a.G + e * 6 * n3 + k * 6 * n2, hb, gbar, pol);
     };
