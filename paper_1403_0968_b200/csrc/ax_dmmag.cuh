@@ -20,9 +20,10 @@ struct DgCfg {
     static constexpr int VL = ((n3 + 2 + 1) / 2) * 2;      // vector slot (doubles, even)
     static constexpr int STAGE = VL + 6 * n3;              // u + G^ of one element
     static constexpr int SMEM_MAX = 227 * 1024 - 1024;
-    // double-buffered while two stages fit (n <= 12), else one stage (n <= 15):
-    // the next element's copies then start after the current one is done
-    static constexpr int NS = (2 * STAGE * 8 <= SMEM_MAX) ? 2 : 1;
+    // two double-buffered groups while they fit (n <= 10), else single-stage
+    // groups (two while they fit, n <= 12) whose next element's copies are
+    // split around phase B (SPLIT below)
+    static constexpr int NS = (4 * STAGE * 8 <= SMEM_MAX) ? 2 : 1;
     static constexpr int NG_FIT = SMEM_MAX / (NS * STAGE * 8);
     static constexpr int NG = NG_FIT > 2 ? 2 : NG_FIT;      // groups of 8 warps per CTA
     static constexpr int GT = 256;
@@ -84,8 +85,10 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
     // 16-byte sizes and addresses: for odd n^2 the second half starts one
     // double late (3 n^2 - 1 doubles) and the first takes that double along
     // (3 n^2 + 1; it is factor 3 of node 0, not read in phase B).
-    constexpr bool SPLIT = NS == 1 && SLICE;
+    // element-major G^: one copy per half, [3n^3 + HO3, 6n^3) and [0, 3n^3 + HO3)
+    constexpr bool SPLIT = NS == 1;
     constexpr int HO = n2 & 1;                  // 0 (even n) or 1 (odd n)
+    constexpr int HO3 = n3 & 1;
     auto issue_a = [&](int64_t e) {
         const int64_t first = e * n3;
         const VecRange vr = vec_range(first, n3, L);
@@ -96,15 +99,24 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
         for (int64_t q = vr.a1; q < first + n3; ++q) sb[q - vr.a0] = __ldg(a.u + q);
         mbar_arrive(gbar);
         bulk_g2s(sb, a.u + vr.a0, vb, gbar, pol);
-        for (int k = 0; k < n; ++k) {
-            const int o = k * 6 * n2 + 3 * n2 + HO;
-            bulk_g2s(sb + VL + o, a.G + e * 6 * n3 + o, hb, gbar, pol);
+        if constexpr (SLICE) {
+            for (int k = 0; k < n; ++k) {
+                const int o = k * 6 * n2 + 3 * n2 + HO;
+                bulk_g2s(sb + VL + o, a.G + e * 6 * n3 + o, hb, gbar, pol);
+            }
+        } else {
+            const int o = 3 * n3 + HO3;
+            bulk_g2s(sb + VL + o, a.G + e * 6 * n3 + o, (uint32_t)((3 * n3 - HO3) * 8), gbar, pol);
         }
     };
     auto issue_b = [&](int64_t e) {
-        const uint32_t hb = (uint32_t)((3 * n2 + HO) * 8);
-        for (int k = 0; k < n; ++k)
-            bulk_g2s(stage0 + VL + k * 6 * n2, a.G + e * 6 * n3 + k * 6 * n2, hb, gbar, pol);
+        if constexpr (SLICE) {
+            const uint32_t hb = (uint32_t)((3 * n2 + HO) * 8);
+            for (int k = 0; k < n; ++k)
+                bulk_g2s(stage0 + VL + k * 6 * n2, a.G + e * 6 * n3 + k * 6 * n2, hb, gbar, pol);
+        } else {
+            bulk_g2s(stage0 + VL, a.G + e * 6 * n3, (uint32_t)((3 * n3 + HO3) * 8), gbar, pol);
+        }
     };
     if (leader) {
         if (u0 < nunits) issue(u0, 0);
