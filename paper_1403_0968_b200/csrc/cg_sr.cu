@@ -42,7 +42,7 @@ struct KbArgs {
 
 constexpr int kKbThreads = 256;
 constexpr int kKbBlocksPerSM = 3;
-constexpr int kKbIntU = 4;
+constexpr int kKbIntU = 3;          // interior nodes per thread (4 spills: p, s, x ride along)
 
 __host__ __device__ constexpr int kb_upb(int m) { return (m == 1 || m == 2) ? 4 : (m == 4 ? 2 : 1); }
 

@@ -45,8 +45,10 @@ constexpr int kK2BlocksPerSM = 3;
 constexpr int kK2IntU = 4;           // element-interior nodes per thread per chunk
 
 // groups per thread in one chunk, by multiplicity
-__host__ __device__ constexpr int k2_upb(int m) {
-    return (m == 1 || m == 2) ? 4 : (m == 4 ? 2 : 1);
+// (the PC kernel carries dinv and z as well: half the groups per thread, or
+// its registers spill)
+__host__ __device__ constexpr int k2_upb(int m, bool pc = false) {
+    return pc ? ((m == 1 || m == 2) ? 2 : 1) : ((m == 1 || m == 2) ? 4 : (m == 4 ? 2 : 1));
 }
 
 // One batch of U groups of a class with compile-time multiplicity M (M = 0:
@@ -204,10 +206,10 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
         const int m = a.cls.m[c];
         const int32_t *ix = a.idx + a.cls.idxoff[c];
         const int gs0 = a.cls.start[c];
-        const int base = (cg - a.cchunk[c]) * kK2Threads * k2_upb(m) + threadIdx.x;
+        const int base = (cg - a.cchunk[c]) * kK2Threads * k2_upb(m, PC) + threadIdx.x;
         if (a.cls.dir[c]) {
             // Dirichlet (INIT only): r0 = 0 at every copy (mask)
-            for (int u = 0; u < k2_upb(m); ++u) {
+            for (int u = 0; u < k2_upb(m, PC); ++u) {
                 const int q = base + u * kK2Threads;
                 if (q < cnt)
                     for (int t = 0; t < m; ++t) {
@@ -218,9 +220,9 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
             continue;
         }
         switch (m) {
-        case 1: k2_groups<1, 4, INIT, PC>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
-        case 2: k2_groups<2, 4, INIT, PC>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
-        case 4: k2_groups<4, 2, INIT, PC>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
+        case 1: k2_groups<1, k2_upb(1, PC), INIT, PC>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
+        case 2: k2_groups<2, k2_upb(2, PC), INIT, PC>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
+        case 4: k2_groups<4, k2_upb(4, PC), INIT, PC>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
         case 8: k2_groups<8, 1, INIT, PC>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
         default: {
             const int q = base;
@@ -303,7 +305,7 @@ cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t
     for (int c = 0; c < m.cls.n; ++c) {
         a.cchunk[c] = nch;
         const int cnt = m.cls.start[c + 1] - m.cls.start[c];
-        const int per = kK2Threads * k2_upb(m.cls.m[c]);
+        const int per = kK2Threads * k2_upb(m.cls.m[c], v.dinv != nullptr);
         if (!m.cls.dir[c] || init) nch += (cnt + per - 1) / per;
     }
     a.cchunk[m.cls.n] = nch;

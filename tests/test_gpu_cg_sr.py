@@ -63,8 +63,12 @@ SR = "single_reduction"
 @pytest.mark.parametrize("N,elems,eps,kind", [
     (4, (2, 2, 2), 0.05, "sin"), (4, (2, 2, 2), 0.05, "rand"), (3, (5, 4, 3), 0.05, "rand"),
     (7, (8, 8, 8), 0.05, "sin"), (2, (3, 3, 3), 0.0, "rand"), (9, (2, 3, 2), 0.05, "sin"),
-    (12, (2, 2, 1), 0.05, "sin"), (1, (4, 3, 3), 0.05, "rand")])
+    (12, (2, 1, 2), 0.1, "sin"), (1, (4, 3, 3), 0.05, "rand")])
 def test_cg_sr_iteration_parity(dev, impl, N, elems, eps, kind):
+    # (the recursively updated residual of this recurrence drifts a few % from
+    # the oracle's over a solve, R7: the N=12 case is one whose
+    # oracle residual crosses the tolerance by a wider margin (7% / 15% at
+    # the last two iterations) than the 2x2x1 eps=0.05 mesh (3%))
     if impl.startswith("tma") and N > 10:
         pytest.skip("SEM_AX_KERNEL=tma above N=10 selects the simple kernel (no KA variant)")
     m, G, J, ctx = make(N, elems, eps)
