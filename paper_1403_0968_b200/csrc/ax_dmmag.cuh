@@ -38,6 +38,10 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
     constexpr int n = C::n, n2 = C::n2, n3 = C::n3, KS = C::KS, VL = C::VL, STAGE = C::STAGE;
     constexpr int NG = C::NG, GT = C::GT, NS = C::NS;
     constexpr int DO = d_off(N);
+    // even n: a lane's node pair (i0, i0 + 1) is one 16-byte-aligned double2 in
+    // every staged array (n^2, n^3, VL even, shift 0) -- one conflict-free
+    // 128-bit access instead of two 4-way-conflicted 64-bit ones (ncu r01aw)
+    constexpr bool VEC = (n % 2) == 0;
     extern __shared__ __align__(128) double smem[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + size_t(NG) * NS * STAGE);
 
@@ -152,8 +156,15 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
         double c0v[n], c1v[n];                  // the lane's two input columns
 #pragma unroll
         for (int m = 0; m < n; ++m) {
-            c0v[m] = v0 ? su[m * n2 + j * n + i0] : 0.0;
-            c1v[m] = v1 ? su[m * n2 + j * n + i0 + 1] : 0.0;
+            if constexpr (VEC) {                // even n: node pairs are 16-byte aligned
+                const double2 c = v0 ? *reinterpret_cast<const double2 *>(su + m * n2 + j * n + i0)
+                                     : make_double2(0.0, 0.0);
+                c0v[m] = c.x;
+                c1v[m] = c.y;
+            } else {
+                c0v[m] = v0 ? su[m * n2 + j * n + i0] : 0.0;
+                c1v[m] = v1 ? su[m * n2 + j * n + i0 + 1] : 0.0;
+            }
         }
         // ---- phase A on the warp's tile of its slices ----
         for (int k = hpar; k < n; k += 2) {
@@ -173,6 +184,20 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
                 const double d = c_D[DO + k * n + m];
                 t0 = fma(d, c0v[m], t0);
                 t1 = fma(d, c1v[m], t1);
+            }
+            if constexpr (VEC) {
+                if (v0) {
+                    double2 g[6];
+#pragma unroll
+                    for (int f = 0; f < 6; ++f) g[f] = *reinterpret_cast<const double2 *>(sG + gidx(f, k, j, i0));
+                    *reinterpret_cast<double2 *>(sG + gidx(0, k, j, i0)) =
+                        make_double2(g[0].x * r0 + g[1].x * s0 + g[2].x * t0, g[0].y * r1 + g[1].y * s1 + g[2].y * t1);
+                    *reinterpret_cast<double2 *>(sG + gidx(1, k, j, i0)) =
+                        make_double2(g[1].x * r0 + g[3].x * s0 + g[4].x * t0, g[1].y * r1 + g[3].y * s1 + g[4].y * t1);
+                    *reinterpret_cast<double2 *>(sG + gidx(2, k, j, i0)) =
+                        make_double2(g[2].x * r0 + g[4].x * s0 + g[5].x * t0, g[2].y * r1 + g[4].y * s1 + g[5].y * t1);
+                }
+                continue;
             }
             if (v0) {
                 const double g0 = sG[gidx(0, k, j, i0)], g1 = sG[gidx(1, k, j, i0)];
@@ -201,8 +226,15 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
         double f0v[n], f1v[n];
 #pragma unroll
         for (int m = 0; m < n; ++m) {
-            f0v[m] = v0 ? sG[gidx(2, m, j, i0)] : 0.0;
-            f1v[m] = v1 ? sG[gidx(2, m, j, i0 + 1)] : 0.0;
+            if constexpr (VEC) {
+                const double2 f = v0 ? *reinterpret_cast<const double2 *>(sG + gidx(2, m, j, i0))
+                                     : make_double2(0.0, 0.0);
+                f0v[m] = f.x;
+                f1v[m] = f.y;
+            } else {
+                f0v[m] = v0 ? sG[gidx(2, m, j, i0)] : 0.0;
+                f1v[m] = v1 ? sG[gidx(2, m, j, i0 + 1)] : 0.0;
+            }
         }
         for (int k = hpar; k < n; k += 2) {
             double w0 = 0.0, w1 = 0.0;
