@@ -23,7 +23,8 @@
  *  - Vectors u, w, b, x, f are DEVICE pointers (CUDA global memory on the
  *    context's device) of nlocal = E * (N+1)^3 doubles in "local" (E-vector)
  *    storage: node (i,j,k) of element e at e*(N+1)^3 + i + (N+1)*j + (N+1)^2*k,
- *    i (the r direction) fastest.  They must be 8-byte aligned.  The caller owns
+ *    i (the r direction) fastest.  They must be 16-byte aligned (the kernels
+ *    stage them with bulk copies and 128-bit accesses).  The caller owns
  *    them (PyTorch tensors in the Python binding).
  *  - All device work is enqueued on the CUDA stream given to sem_setup and the
  *    call returns without a host synchronisation, except sem_setup and sem_cg,

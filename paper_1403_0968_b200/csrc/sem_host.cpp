@@ -721,11 +721,12 @@ extern "C" int64_t sem_launch_count(const sem_ctx *ctx) { return ctx ? ctx->laun
         if (ctx->broken) return fail(ctx, SEM_ECUDA, "context unusable after a CUDA error"); \
     } while (0)
 
-static bool aligned8(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
+// vectors are staged by 16-byte bulk copies and read / written as double2
+static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 extern "C" int sem_ax(sem_ctx *ctx, const double *u, double *w) {
     CHECK_CTX();
-    if (!u || !w || !aligned8(u) || !aligned8(w)) return fail(ctx, SEM_EINVAL, "sem_ax: bad pointer");
+    if (!u || !w || !aligned16(u) || !aligned16(w)) return fail(ctx, SEM_EINVAL, "sem_ax: bad pointer");
     if (u == w) return fail(ctx, SEM_EINVAL, "sem_ax: u and w must not alias");
     LAUNCHP(kProfAx, (ctx->dm.H ? 72.0 : 64.0) * ctx->L, -1, launch_ax(ctx->dm, u, w, ctx->stream));
     return SEM_OK;
@@ -756,20 +757,20 @@ static int dssum_impl(sem_ctx *ctx, double *w, int mode, int k, cudaStream_t s) 
 
 extern "C" int sem_dssum(sem_ctx *ctx, double *w) {
     CHECK_CTX();
-    if (!w || !aligned8(w)) return fail(ctx, SEM_EINVAL, "sem_dssum: bad pointer");
+    if (!w || !aligned16(w)) return fail(ctx, SEM_EINVAL, "sem_dssum: bad pointer");
     return dssum_impl(ctx, w, 0, -1, ctx->stream);
 }
 
 extern "C" int sem_mask(sem_ctx *ctx, double *w) {
     CHECK_CTX();
-    if (!w || !aligned8(w)) return fail(ctx, SEM_EINVAL, "sem_mask: bad pointer");
+    if (!w || !aligned16(w)) return fail(ctx, SEM_EINVAL, "sem_mask: bad pointer");
     if (ctx->dm.ndir > 0) LAUNCH(launch_mask(ctx->dm, w, ctx->stream));
     return SEM_OK;
 }
 
 extern "C" int sem_mass(sem_ctx *ctx, const double *f, double *b) {
     CHECK_CTX();
-    if (!f || !b || !aligned8(f) || !aligned8(b)) return fail(ctx, SEM_EINVAL, "sem_mass: bad pointer");
+    if (!f || !b || !aligned16(f) || !aligned16(b)) return fail(ctx, SEM_EINVAL, "sem_mass: bad pointer");
     LAUNCH(launch_mass(ctx->dm, f, b, ctx->stream));
     return SEM_OK;
 }
@@ -904,7 +905,7 @@ static int diag_impl(sem_ctx *ctx, double *d, cudaStream_t s) {
 
 extern "C" int sem_diag(sem_ctx *ctx, double *d) {
     CHECK_CTX();
-    if (!d || !aligned8(d)) return fail(ctx, SEM_EINVAL, "sem_diag: bad pointer");
+    if (!d || !aligned16(d)) return fail(ctx, SEM_EINVAL, "sem_diag: bad pointer");
     return diag_impl(ctx, d, ctx->stream);
 }
 
@@ -980,7 +981,7 @@ static int run_chunks(sem_ctx *ctx, int maxit, bool graph, cudaGraphExec_t gexec
 
 static int cg_sr_impl(sem_ctx *ctx, const double *b, double *x, double tol, int maxit,
                       int *iters, double *rel_res) {
-    if (!b || !x || !aligned8(b) || !aligned8(x)) return fail(ctx, SEM_EINVAL, "sem_cg_sr: bad pointer");
+    if (!b || !x || !aligned16(b) || !aligned16(x)) return fail(ctx, SEM_EINVAL, "sem_cg_sr: bad pointer");
     if (!(tol >= 0.0) || maxit < 0) return fail(ctx, SEM_EINVAL, "sem_cg_sr: tol >= 0 and maxit >= 0 required");
     if (!ctx->dm.use_tma && !ctx->dm.use_hi)
         return fail(ctx, SEM_EINVAL, "sem_cg_sr: needs the TMA / high-order Ax kernels (not SEM_AX_KERNEL=simple)");
@@ -1025,7 +1026,7 @@ static int cg_sr_impl(sem_ctx *ctx, const double *b, double *x, double tol, int 
 
 static int cg_impl(sem_ctx *ctx, int precond, const double *b, double *x, double tol, int maxit,
                    int *iters, double *rel_res) {
-    if (!b || !x || !aligned8(b) || !aligned8(x)) return fail(ctx, SEM_EINVAL, "sem_cg: bad pointer");
+    if (!b || !x || !aligned16(b) || !aligned16(x)) return fail(ctx, SEM_EINVAL, "sem_cg: bad pointer");
     if (!(tol >= 0.0) || maxit < 0) return fail(ctx, SEM_EINVAL, "sem_cg: tol >= 0 and maxit >= 0 required");
     cudaStream_t s = ctx->stream;
     CgVecs &v = ctx->cv;

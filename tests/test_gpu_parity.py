@@ -227,6 +227,24 @@ def test_bad_arguments_raise(dev):
     assert sem.lib().sem_ax(ctx._ctx, ptr, ptr) == sem.SEM_EINVAL   # u, w alias
 
 
+@pytest.mark.parametrize("N", [2, 7, 13])
+def test_8_byte_offset_vectors_rejected(dev, N):
+    """include/sem.h: vectors must be 16-byte aligned (bulk copies, 128-bit
+    accesses); an 8-byte-offset view is refused with SEM_EINVAL before any
+    launch, and the context stays usable."""
+    from paper_1403_0968_b200 import sem
+    m, G, J, ctx = make(N, (2, 1, 1), 0.05)
+    big = torch.zeros(2 * m.nlocal + 2, dtype=torch.float64, device=dev)
+    u, w = big[1:m.nlocal + 1], big[m.nlocal + 2:]
+    assert u.data_ptr() % 16 == 8
+    for fn in (lambda: ctx.ax(u, w), lambda: ctx.dssum(u), lambda: ctx.cg(u, w, tol=1e-8)):
+        with pytest.raises(sem.SemError) as ei:
+            fn()
+        assert ei.value.code == sem.SEM_EINVAL
+    uu = meshgen.random_field(m.nlocal, 3)
+    assert relerr(ctx.ax(T(uu, dev)).cpu().numpy(), oracle.ax(N, G, uu)) <= 1e-12
+
+
 # --- full-size configuration c3 (4096 el, N=7, eps=0.05), as bench.py runs it ---
 @pytest.fixture(scope="module")
 def c3(dev):
