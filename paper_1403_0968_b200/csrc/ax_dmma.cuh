@@ -150,6 +150,13 @@ __global__ void __launch_bounds__(TmaLayout<7, CG>::NT, 1) ax_dmma_kernel(TmaArg
     }
     const int kb = 4 * warp;                  // this warp's k-slices kb .. kb+3
     const int lq = gid * n + i0;              // the lane's first node within a slice
+    // f_r is stored with its column halves swapped on rows 2, 3, 6, 7 (i ^ 4),
+    // so the phase-B A-fragment loads F_r,k[gid][4ks + tig] of a warp hit all
+    // 16 bank pairs (2 wavefronts) instead of 8 (4 wavefronts)
+    // (not with the mass term: measured 9% slower there, r01az)
+    constexpr bool SWZ = !MASS;
+    const int swz = SWZ ? (((gid >> 1) & 1) << 2) : 0;
+    const int lqr = gid * n + (i0 ^ swz);
 
     double pap = 0.0;
     int t = 0;
@@ -223,7 +230,8 @@ __global__ void __launch_bounds__(TmaLayout<7, CG>::NT, 1) ax_dmma_kernel(TmaArg
             const double2 g3 = *reinterpret_cast<const double2 *>(G0 + 3 * n3);
             const double2 g4 = *reinterpret_cast<const double2 *>(G0 + 4 * n3);
             const double2 g5 = *reinterpret_cast<const double2 *>(G0 + 5 * n3);
-            *reinterpret_cast<double2 *>(G0 + 0 * n3) =
+            if constexpr (SWZ) __syncwarp();   // the slice's G^_0 pairs are read before the swizzled f_r lands
+            *reinterpret_cast<double2 *>(sG + k * n2 + lqr) =
                 make_double2(g0.x * r0 + g1.x * s0 + g2.x * t0, g0.y * r1 + g1.y * s1 + g2.y * t1);
             *reinterpret_cast<double2 *>(G0 + 1 * n3) =
                 make_double2(g1.x * r0 + g3.x * s0 + g4.x * t0, g1.y * r1 + g3.y * s1 + g4.y * t1);
@@ -247,7 +255,7 @@ __global__ void __launch_bounds__(TmaLayout<7, CG>::NT, 1) ax_dmma_kernel(TmaArg
             double w0 = 0.0, w1 = 0.0;
 #pragma unroll
             for (int ks = 0; ks < 2; ++ks) {
-                dmma(w0, w1, frk[gid * n + 4 * ks + tig], dB[ks]);   // F_r,k D
+                dmma(w0, w1, frk[gid * n + ((4 * ks + tig) ^ swz)], dB[ks]);   // F_r,k D
                 dmma(w0, w1, dB[ks], fsk[(4 * ks + tig) * n + gid]); // D^T F_s,k
             }
             double t0 = 0.0, t1 = 0.0;
