@@ -322,9 +322,35 @@ def run_fd(args, rank, world):
         dist.destroy_process_group()
 
 
+def spawn_ranks(args):
+    """`--gpus N > 1` without a torchrun environment: re-launch this script as
+    N ranks (one process per GPU) through torch.distributed.run on 127.0.0.1.
+    Exits non-zero when the node has fewer than N GPUs."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible", file=sys.stderr)
+        sys.exit(2)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        spawn_ranks(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
@@ -407,8 +433,11 @@ def main():
     value = L_all * its * args.steps / t / 1e9
     cg_its_per_s = its * args.steps / t
 
-    # ---- per-kernel device time: the same solves again, each launch bracketed
-    # by CUDA events on the library stream (kept out of the timed region) ----
+    # ---- per-kernel device time: the same solves again, with sem_profile on:
+    # the library runs them through a second CUDA graph of the same chunk
+    # whose kernels are bracketed by event-record nodes, read back after every
+    # chunk (kept out of the timed region; ungraphed per-launch events only if
+    # SEM_CG_GRAPH=0) ----
     prof_steps = max(1, min(3, args.steps))
     ctx.profile(True)
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -455,7 +484,9 @@ def main():
     traffic = ncu_traffic(("ax_dmma_kernel<1, 0, 0, 0>",) if dmma else
                           (f"ax_tma_kernel<{args.N}, true, false>", f"ax_tma_kernel<{args.N}, 1>")) \
         if alpha is None and args.precond == "none" and args.cg_variant == "standard" else None
-    shares = {k: v[0] / prof_ms for k, v in prof.items() if v[1]}
+    # share of the timed solve: per-solve device ms of each class (inside the
+    # graph) over the timed region's ms per solve
+    shares = {k: v[0] / prof_steps / (ms / args.steps) for k, v in prof.items() if v[1]}
     # every CG kernel inside the solve (per-launch CUDA events, profiled pass):
     # K2 reads the w K1 just wrote from L2, unlike its back-to-back replay
     in_solve = {}
@@ -569,12 +600,14 @@ def main():
                                        "algorithmic_bytes": bpn_k1 * L + (k2_bytes or 0.0),
                                        "frac": (bpn_k1 * L + (k2_bytes or 0.0)) /
                                                (ms / args.steps / its * 1e-3) / 1e9 / peak},
-                         "timing": "achieved: CUDA events around every K1 launch on the library "
-                                   f"stream over {prof_steps} solves of the same workload run right "
-                                   "after the timed region (also step_share); kernels_replayed: "
-                                   "CUDA events around a graph of 50 back-to-back launches "
-                                   "(sem_kernel_replay, no CG neighbours in L2); kernels_in_solve: "
-                                   "the per-launch events of the profiled solves"},
+                         "profiled_solve_ms": prof_ms / prof_steps,
+                         "timing": "achieved / kernels_in_solve / step_share: event-record "
+                                   "nodes around every kernel INSIDE the CG chunk graph "
+                                   f"(sem_profile), {prof_steps} solves of the same workload run "
+                                   "right after the timed region, step_share against the timed "
+                                   "ms per solve; kernels_replayed: CUDA events around a graph of "
+                                   "50 back-to-back launches of one kernel (sem_kernel_replay, no "
+                                   "CG neighbours in L2)"},
             "gpu_launches": gpu_launches,
             "e2e": e2e,
             "cpu_baseline": cpu,

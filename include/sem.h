@@ -39,7 +39,9 @@
  *    malformed mesh (non-positive Jacobian, inconsistent Dirichlet flags across
  *    copies of a global node, an element-interior node that is shared or
  *    Dirichlet), or a misaligned pointer; SEM_ECUDA for a CUDA runtime failure
- *    (the context is then unusable); SEM_ENCCL for an NCCL failure;
+ *    (the context is then unusable); SEM_ENCCL for an NCCL failure, including
+ *    an asynchronous one (ncclCommGetAsyncError, polled while sem_cg waits for
+ *    the device; the communicator is then aborted and the context unusable);
  *    SEM_ENOCONV when sem_cg reached maxit with tol > 0 (x holds the last
  *    iterate; not a failure for tol == 0); SEM_ESTATE for a NULL/freed context.
  */
@@ -191,6 +193,20 @@ int sem_diag(sem_ctx *ctx, double *d);
  * the other ranks before sem_setup (HOST buffer of sem_nccl_id_bytes()). */
 int sem_nccl_id_bytes(void);
 int sem_nccl_get_unique_id(void *id_out);
+
+/* TEST-ONLY in-process transport (no NCCL): an id (HOST buffer of
+ * sem_nccl_id_bytes() bytes) that, passed as sem_mesh.nccl_id to the nranks
+ * contexts of ONE process -- one host thread per rank, all on one device, each
+ * with its own stream -- makes their interface exchange and scalar all-gathers
+ * device-to-device copies between the ranks' buffers, ordered by CUDA events
+ * and a host rendezvous (a7 on a single GPU, where NCCL
+ * refuses two ranks).  Everything else -- the exchange plan, pack/combine
+ * kernels, rank-ordered sums, boundary/interior K1 split, the multi-rank CG
+ * prologues -- runs exactly as with NCCL.  CUDA-graph capture of the CG chunks
+ * is disabled for such contexts.  A rank that fails or stops calling the
+ * collectives makes its peers fail with SEM_ENCCL after
+ * SEM_LOOPBACK_TIMEOUT_MS (default 120000) instead of hanging. */
+int sem_loopback_unique_id(void *id_out);
 
 /* Device timing per kernel class, for the benchmark's roofline report.
  * sem_profile(ctx, 1) resets the accumulators and brackets every later launch

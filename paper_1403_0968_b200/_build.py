@@ -38,36 +38,48 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = True) -> str:
-    """Compile every translation unit in parallel (nvcc -c), then link."""
+    """Compile the translation units in parallel (nvcc -c; objects cached under
+    build/ and recompiled when their source or any header is newer), then link."""
     if not force and not needs_build():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
-    import tempfile
     inc, lib = nccl_dirs()
-    tmpdir = tempfile.mkdtemp(prefix="semobj_")
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
     common = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-O2", "-Xptxas", "-warn-spills",
               "-I", os.path.join(ROOT, "include"), "-I", inc]
-    objs = [os.path.join(tmpdir, os.path.splitext(f)[0] + ".o") for f in SOURCES]
-    cmds = [common + ["-c", os.path.join(CSRC, f), "-o", o] for f, o in zip(SOURCES, objs)]
-    if verbose:
+    hdr = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "sem.h"),
+                                                     os.path.join(ROOT, "include", "fd.h"),
+                                                     os.path.abspath(__file__)]
+    newest_hdr = max(os.path.getmtime(h) for h in hdr)
+    objs = [os.path.join(objdir, os.path.splitext(f)[0] + ".o") for f in SOURCES]
+
+    def stale(f, o):
+        if force or not os.path.exists(o):
+            return True
+        t = os.path.getmtime(o)
+        return os.path.getmtime(os.path.join(CSRC, f)) > t or newest_hdr > t
+
+    cmds = [common + ["-c", os.path.join(CSRC, f), "-o", o]
+            for f, o in zip(SOURCES, objs) if stale(f, o)]
+    if verbose and cmds:
         print(" ".join(cmds[0]), "... (x%d, parallel)" % len(cmds), file=sys.stderr)
-    with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+    with ThreadPoolExecutor(max_workers=max(1, len(cmds))) as ex:
         procs = list(ex.map(lambda c: subprocess.run(c, cwd=CSRC, capture_output=True, text=True),
                             cmds))
     for c, p in zip(cmds, procs):
         if verbose and p.stderr:
             sys.stderr.write(p.stderr)
         if p.returncode != 0:
+            if os.path.exists(c[-1]):
+                os.remove(c[-1])
             raise subprocess.CalledProcessError(p.returncode, c, p.stdout, p.stderr)
     tmp = LIB + ".tmp"
     link = ["nvcc", *ARCH, "--shared", *objs, "-o", tmp, "-L", lib, "-l:libnccl.so.2",
             "-Xlinker", f"-rpath={lib}", "-lcudart"]
     subprocess.check_call(link, cwd=CSRC)
     os.replace(tmp, LIB)
-    for o in objs:
-        os.remove(o)
-    os.rmdir(tmpdir)
     return LIB
 
 

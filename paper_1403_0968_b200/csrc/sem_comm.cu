@@ -3,7 +3,13 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <thread>
 
 #include "cg_device.cuh"
 #include "sem_comm.h"
@@ -106,16 +112,86 @@ int build_exchange_plan(const sem_mesh *mesh, const std::vector<int64_t> &surf_i
 // ---------------------------------------------------------------------------
 // device
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// loopback transport (TEST ONLY): P ranks as P contexts in ONE process on ONE
+// GPU, one host thread per rank.  Every rank's exchange and all-gather become
+// device-to-device copies between the ranks' own buffers, ordered by CUDA
+// events and two host rendezvous per collective:
+//   1. each rank enqueues its producer (pack / reduction kernel), records
+//      ev_ready[rank] on its stream and posts its buffer pointer;   barrier
+//   2. each rank makes its stream wait for ev_ready of every peer, copies the
+//      peers' values it needs into its own receive buffer / slots, records
+//      ev_done[rank];                                                barrier
+//   3. each rank's stream waits for ev_done of every peer (the peers have read
+//      its send buffer / slot before it is overwritten).
+// The pack / combine kernels, the plan, the rank-ordered sums and every
+// multi-rank branch of the CG kernels run exactly as with NCCL; only the
+// transfer differs.  Selected by an id from sem_loopback_unique_id() in
+// sem_mesh.nccl_id.  CUDA-graph capture is off for loopback contexts (the
+// host rendezvous cannot be captured).
+// ---------------------------------------------------------------------------
+static const char kLoopMagic[16] = {'S', 'E', 'M', '-', 'L', 'O', 'O', 'P', 'B', 'A', 'C', 'K', 0, 1, 2, 3};
+
+struct LoopWorld {
+    int P = 0;
+    int refs = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    int64_t gen = 0;
+    bool failed = false;
+    std::vector<cudaEvent_t> ev_ready, ev_done;
+    std::vector<double *> post;          // per rank: buffer posted for the current collective
+    std::vector<double *> sendbuf;       // per rank: its exchange send buffer
+    std::vector<std::vector<int>> peer;  // per rank: its peers (ascending)
+    std::vector<std::vector<int64_t>> peer_off;
+    std::vector<int> joined;
+};
+
+static std::mutex g_loop_mu;
+static std::map<std::string, LoopWorld *> g_loop;
+
+static int loop_timeout_ms() {
+    const char *e = getenv("SEM_LOOPBACK_TIMEOUT_MS");
+    return e ? atoi(e) : 120000;
+}
+
+// Host rendezvous of all P ranks (false: a peer failed or timed out).
+static bool loop_barrier(LoopWorld &w) {
+    std::unique_lock<std::mutex> lk(w.mu);
+    if (w.failed) return false;
+    const int64_t g = w.gen;
+    if (++w.arrived == w.P) {
+        w.arrived = 0;
+        ++w.gen;
+        w.cv.notify_all();
+        return true;
+    }
+    const bool ok = w.cv.wait_for(lk, std::chrono::milliseconds(loop_timeout_ms()),
+                                  [&] { return w.gen != g || w.failed; });
+    if (!ok || w.failed) {
+        w.failed = true;
+        w.cv.notify_all();
+        return false;
+    }
+    return true;
+}
+
 struct Comm {
     ncclComm_t nccl = nullptr;
+    LoopWorld *lw = nullptr;             // loopback transport (tests) instead of NCCL
+    std::string lw_key;
     int rank = 0, nranks = 1;
     std::vector<int> peer;
     std::vector<int64_t> peer_off;
+    std::vector<int64_t> peer_src_off;   // loopback: offset of my slots in each peer's send buffer
     int64_t nslot = 0;
     int nif = 0;
     double *sendbuf = nullptr, *recvbuf = nullptr;
     int32_t *send_group = nullptr, *if_group = nullptr, *if_off = nullptr, *if_src = nullptr;
 };
+
+bool comm_capturable(const Comm *c) { return c && !c->lw; }
 
 __device__ __forceinline__ void group_loc(const GsClasses &cls, int g, int &m, int &cnt, int &q,
                                           int &off) {
@@ -184,6 +260,92 @@ __global__ void combine_kernel(const __grid_constant__ GsClasses cls, const int3
         }                                                                           \
     } while (0)
 
+// Register this rank in the loopback world named by the id (created by the
+// first rank to arrive), then learn where the peers keep the slots this rank
+// receives.
+static int loop_join(Comm &c, const sem_mesh *mesh, std::string &err) {
+    c.lw_key.assign(static_cast<const char *>(mesh->nccl_id), 128);
+    LoopWorld *w;
+    {
+        std::lock_guard<std::mutex> g(g_loop_mu);
+        auto it = g_loop.find(c.lw_key);
+        if (it == g_loop.end()) {
+            w = new LoopWorld;
+            w->P = c.nranks;
+            w->ev_ready.assign(c.nranks, nullptr);
+            w->ev_done.assign(c.nranks, nullptr);
+            w->post.assign(c.nranks, nullptr);
+            w->sendbuf.assign(c.nranks, nullptr);
+            w->peer.assign(c.nranks, {});
+            w->peer_off.assign(c.nranks, {});
+            w->joined.assign(c.nranks, 0);
+            g_loop[c.lw_key] = w;
+        } else {
+            w = it->second;
+        }
+        if (w->P != c.nranks || w->joined[c.rank]) {
+            err = "loopback: nranks mismatch or rank joined twice";
+            return SEM_EINVAL;
+        }
+        w->joined[c.rank] = 1;
+        ++w->refs;
+    }
+    c.lw = w;
+    CC(cudaEventCreateWithFlags(&w->ev_ready[c.rank], cudaEventDisableTiming));
+    CC(cudaEventCreateWithFlags(&w->ev_done[c.rank], cudaEventDisableTiming));
+    w->sendbuf[c.rank] = c.sendbuf;
+    w->peer[c.rank] = c.peer;
+    w->peer_off[c.rank] = c.peer_off;
+    if (!loop_barrier(*w)) {
+        err = "loopback: setup rendezvous failed (a peer failed or timed out)";
+        return SEM_ENCCL;
+    }
+    c.peer_src_off.resize(c.peer.size());
+    for (size_t p = 0; p < c.peer.size(); ++p) {
+        const int q = c.peer[p];
+        const auto &qp = w->peer[q];
+        const auto at = std::find(qp.begin(), qp.end(), c.rank);
+        if (at == qp.end()) {
+            err = "loopback: asymmetric exchange plan";
+            return SEM_EINVAL;
+        }
+        const size_t qi = size_t(at - qp.begin());
+        if (w->peer_off[q][qi + 1] - w->peer_off[q][qi] != c.peer_off[p + 1] - c.peer_off[p]) {
+            err = "loopback: shared-set sizes differ between peers";
+            return SEM_EINVAL;
+        }
+        c.peer_src_off[p] = w->peer_off[q][qi];
+    }
+    if (!loop_barrier(*w)) {
+        err = "loopback: setup rendezvous failed (a peer failed or timed out)";
+        return SEM_ENCCL;
+    }
+    return SEM_OK;
+}
+
+// One loopback collective (steps 1-3 above).  copy(s) enqueues this rank's
+// reads of the peers' posted buffers.
+template <typename F>
+static int loop_collective(Comm &c, double *mine, cudaStream_t s, std::string &err, F copy) {
+    LoopWorld &w = *c.lw;
+    CC(cudaEventRecord(w.ev_ready[c.rank], s));
+    w.post[c.rank] = mine;
+    if (!loop_barrier(w)) {
+        err = "loopback: a peer failed or timed out";
+        return SEM_ENCCL;
+    }
+    int rc = copy();
+    if (rc) return rc;
+    CC(cudaEventRecord(w.ev_done[c.rank], s));
+    if (!loop_barrier(w)) {
+        err = "loopback: a peer failed or timed out";
+        return SEM_ENCCL;
+    }
+    for (int q = 0; q < c.nranks; ++q)
+        if (q != c.rank) CC(cudaStreamWaitEvent(s, w.ev_done[q], 0));
+    return SEM_OK;
+}
+
 int comm_setup(Comm *&cp, const sem_mesh *mesh, const ExchangePlan &ep, const DevMesh &,
                cudaStream_t s, std::string &err) {
     cp = new Comm;
@@ -194,9 +356,12 @@ int comm_setup(Comm *&cp, const sem_mesh *mesh, const ExchangePlan &ep, const De
     c.peer_off = ep.peer_off;
     c.nslot = (int64_t)ep.shared_ids.size();
     c.nif = (int)ep.if_group.size();
-    ncclUniqueId id;
-    std::memcpy(&id, mesh->nccl_id, sizeof id);
-    NC(ncclCommInitRank(&c.nccl, c.nranks, id, c.rank));
+    const bool loop = std::memcmp(mesh->nccl_id, kLoopMagic, sizeof kLoopMagic) == 0;
+    if (!loop) {
+        ncclUniqueId id;
+        std::memcpy(&id, mesh->nccl_id, sizeof id);
+        NC(ncclCommInitRank(&c.nccl, c.nranks, id, c.rank));
+    }
     const size_t ns = std::max<int64_t>(c.nslot, 1);
     CC(cudaMalloc(&c.sendbuf, sizeof(double) * ns));
     CC(cudaMalloc(&c.recvbuf, sizeof(double) * ns));
@@ -216,6 +381,7 @@ int comm_setup(Comm *&cp, const sem_mesh *mesh, const ExchangePlan &ep, const De
     CC(cudaMemcpyAsync(c.if_off, ep.if_off.data(), sizeof(int32_t) * (c.nif + 1),
                        cudaMemcpyHostToDevice, s));
     CC(cudaStreamSynchronize(s));
+    if (loop) return loop_join(c, mesh, err);
     return SEM_OK;
 }
 
@@ -233,13 +399,27 @@ int comm_exchange(Comm *cp, const DevMesh &m, double *w, cudaStream_t s, int64_t
         CC(cudaGetLastError());
         ++nlaunch;
     }
-    NC(ncclGroupStart());
-    for (size_t p = 0; p < c.peer.size(); ++p) {
-        const size_t o = (size_t)c.peer_off[p], n = (size_t)(c.peer_off[p + 1] - c.peer_off[p]);
-        NC(ncclSend(c.sendbuf + o, n, ncclDouble, c.peer[p], c.nccl, s));
-        NC(ncclRecv(c.recvbuf + o, n, ncclDouble, c.peer[p], c.nccl, s));
+    if (c.lw) {
+        int rc = loop_collective(c, c.sendbuf, s, err, [&]() -> int {
+            for (size_t p = 0; p < c.peer.size(); ++p) {
+                const int q = c.peer[p];
+                const size_t n = (size_t)(c.peer_off[p + 1] - c.peer_off[p]);
+                CC(cudaStreamWaitEvent(s, c.lw->ev_ready[q], 0));
+                CC(cudaMemcpyAsync(c.recvbuf + c.peer_off[p], c.lw->sendbuf[q] + c.peer_src_off[p],
+                                   sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+            }
+            return SEM_OK;
+        });
+        if (rc) return rc;
+    } else {
+        NC(ncclGroupStart());
+        for (size_t p = 0; p < c.peer.size(); ++p) {
+            const size_t o = (size_t)c.peer_off[p], n = (size_t)(c.peer_off[p + 1] - c.peer_off[p]);
+            NC(ncclSend(c.sendbuf + o, n, ncclDouble, c.peer[p], c.nccl, s));
+            NC(ncclRecv(c.recvbuf + o, n, ncclDouble, c.peer[p], c.nccl, s));
+        }
+        NC(ncclGroupEnd());
     }
-    NC(ncclGroupEnd());
     if (c.nif) {
         combine_kernel<<<(c.nif + 255) / 256, 256, 0, s>>>(m.cls, m.gs_idx, w, c.if_group, c.if_off,
                                                            c.if_src, c.nif, c.recvbuf);
@@ -254,8 +434,7 @@ int comm_allgather_scalar(Comm *cp, double *slot_base, cudaStream_t s, std::stri
         err = "no communicator";
         return SEM_ESTATE;
     }
-    NC(ncclAllGather(slot_base + cp->rank, slot_base, 1, ncclDouble, cp->nccl, s));
-    return SEM_OK;
+    return comm_allgather(cp, slot_base, 1, s, err);
 }
 
 int comm_allgather(Comm *cp, double *slot_base, int count, cudaStream_t s, std::string &err) {
@@ -263,13 +442,67 @@ int comm_allgather(Comm *cp, double *slot_base, int count, cudaStream_t s, std::
         err = "no communicator";
         return SEM_ESTATE;
     }
-    NC(ncclAllGather(slot_base + size_t(cp->rank) * count, slot_base, count, ncclDouble, cp->nccl, s));
+    Comm &c = *cp;
+    if (c.lw) {
+        return loop_collective(c, slot_base, s, err, [&]() -> int {
+            for (int q = 0; q < c.nranks; ++q) {
+                if (q == c.rank) continue;
+                CC(cudaStreamWaitEvent(s, c.lw->ev_ready[q], 0));
+                CC(cudaMemcpyAsync(slot_base + size_t(q) * count, c.lw->post[q] + size_t(q) * count,
+                                   sizeof(double) * count, cudaMemcpyDeviceToDevice, s));
+            }
+            return SEM_OK;
+        });
+    }
+    NC(ncclAllGather(slot_base + size_t(c.rank) * count, slot_base, count, ncclDouble, c.nccl, s));
     return SEM_OK;
+}
+
+// Asynchronous NCCL failure of a peer / the network: polled by
+// the CG drivers while they wait for the device.
+int comm_poll(Comm *cp, std::string &err) {
+    if (!cp || cp->lw || !cp->nccl) return SEM_OK;
+    ncclResult_t ar = ncclSuccess;
+    ncclResult_t r = ncclCommGetAsyncError(cp->nccl, &ar);
+    if (r != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress)) {
+        err = std::string("NCCL asynchronous error: ") + ncclGetErrorString(r != ncclSuccess ? r : ar);
+        return SEM_ENCCL;
+    }
+    return SEM_OK;
+}
+
+// Abort the communicator after a failure (pending NCCL work is cancelled so
+// the stream can drain); the context is unusable afterwards.
+void comm_abort(Comm *cp) {
+    if (!cp) return;
+    if (cp->nccl) {
+        ncclCommAbort(cp->nccl);
+        cp->nccl = nullptr;
+    }
+    if (cp->lw) {
+        std::lock_guard<std::mutex> g(cp->lw->mu);
+        cp->lw->failed = true;
+        cp->lw->cv.notify_all();
+    }
 }
 
 void comm_free(Comm *c) {
     if (!c) return;
     if (c->nccl) ncclCommDestroy(c->nccl);
+    if (c->lw) {
+        // the events belong to the world: a peer still leaving its last
+        // collective may wait on them after this rank is gone
+        LoopWorld *w = c->lw;
+        std::lock_guard<std::mutex> g(g_loop_mu);
+        if (--w->refs == 0) {
+            for (auto e : w->ev_ready)
+                if (e) cudaEventDestroy(e);
+            for (auto e : w->ev_done)
+                if (e) cudaEventDestroy(e);
+            g_loop.erase(c->lw_key);
+            delete w;
+        }
+    }
     cudaFree(c->sendbuf);
     cudaFree(c->recvbuf);
     cudaFree(c->send_group);
@@ -280,6 +513,24 @@ void comm_free(Comm *c) {
 }
 
 }  // namespace sem
+
+extern "C" int sem_loopback_unique_id(void *id_out) {
+    if (!id_out) return SEM_EINVAL;
+    static std::mutex mu;
+    static uint64_t counter = 0;
+    uint64_t serial;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        serial = ++counter;
+    }
+    unsigned char id[128] = {0};
+    std::memcpy(id, sem::kLoopMagic, sizeof sem::kLoopMagic);
+    const uint64_t t = (uint64_t)std::chrono::steady_clock::now().time_since_epoch().count();
+    std::memcpy(id + 16, &serial, sizeof serial);
+    std::memcpy(id + 24, &t, sizeof t);
+    std::memcpy(id_out, id, sizeof id);
+    return SEM_OK;
+}
 
 extern "C" int sem_nccl_id_bytes(void) { return (int)sizeof(ncclUniqueId); }
 extern "C" int sem_nccl_get_unique_id(void *id_out) {

@@ -54,5 +54,11 @@ int comm_allgather_scalar(Comm *c, double *slot_base, cudaStream_t s, std::strin
 // `count` doubles per rank, rank-major at slot_base (in place)
 int comm_allgather(Comm *c, double *slot_base, int count, cudaStream_t s, std::string &err);
 void comm_free(Comm *c);
+// false for the loopback transport (its host rendezvous cannot be graph-captured)
+bool comm_capturable(const Comm *c);
+// SEM_ENCCL (with a message) if the communicator reported an asynchronous error
+int comm_poll(Comm *c, std::string &err);
+// abort after a failure (cancels pending NCCL work); wakes loopback peers
+void comm_abort(Comm *c);
 
 }  // namespace sem

@@ -15,6 +15,8 @@
 #include <new>
 #include <string>
 #include <vector>
+#include <thread>
+#include <chrono>
 
 #include "../../include/sem.h"
 #include "sem_internal.h"
@@ -621,6 +623,7 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
             ctx->nglobal = ep.nglobal;
             crc = comm_setup(ctx->comm, mesh, ep, dm, s, cerr);
             if (crc) return fail(ctx, crc, "%s", cerr.c_str());
+            if (!comm_capturable(ctx->comm)) ctx->use_graph = false;   // loopback transport
             // (r,r) ownership of interface groups: the lowest sharing rank counts them
             std::vector<uint32_t> own((hp.ngroups + 31) / 32 + 1, 0xffffffffu);
             for (int32_t g : ep.not_owned) own[g >> 5] &= ~(1u << (g & 31));
@@ -689,6 +692,7 @@ extern "C" void sem_free(sem_ctx *ctx) {
         cudaStreamSynchronize(ctx->stream);
     for (auto &g : ctx->graph_exec)
         if (g) cudaGraphExecDestroy(g);
+
     if (ctx->replay_exec) cudaGraphExecDestroy(ctx->replay_exec);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->side) cudaStreamDestroy(ctx->side);
@@ -897,6 +901,17 @@ static int build_cg_graph(sem_ctx *ctx) {
     return SEM_OK;
 }
 
+// The chunk graph of the current method (captured on first use); none while
+// profiling (per-launch events) or with graphs off (SEM_CG_GRAPH=0, loopback).
+static int chunk_graph(sem_ctx *ctx, cudaGraphExec_t &gexec) {
+    gexec = nullptr;
+    if (ctx->prof || !ctx->use_graph) return SEM_OK;
+    int rc;
+    if (!ctx->graph_exec[ctx->method] && (rc = build_cg_graph(ctx))) return rc;
+    gexec = ctx->graph_exec[ctx->method];
+    return SEM_OK;
+}
+
 // d = Q Q^T diag(A_L) (local storage, unmasked), the assembled diagonal.
 static int diag_impl(sem_ctx *ctx, double *d, cudaStream_t s) {
     LAUNCH(launch_diag(ctx->dm, d, s));
@@ -947,12 +962,41 @@ extern "C" int sem_cg_sr(sem_ctx *ctx, const double *b, double *x, double tol, i
     return cg_sr_impl(ctx, b, x, tol, maxit, iters, rel_res);
 }
 
-// Poll the device state one chunk behind (see cg_impl) until the sticky stop
-// flag is set; returns with the stream's work for the last chunk enqueued.
-static int run_chunks(sem_ctx *ctx, int maxit, bool graph, cudaGraphExec_t gexec, cudaStream_t s) {
+// Wait for an event recorded on the context stream.  With several ranks the
+// wait polls, so an asynchronous NCCL failure of a peer (ncclCommGetAsyncError)
+// ends it with SEM_ENCCL -- the communicator is aborted and the context marked
+// unusable -- instead of blocking forever (SURVEY.md §5 failure detection).
+static int wait_event(sem_ctx *ctx, cudaEvent_t ev) {
+    if (ctx->nranks == 1) {
+        CU(cudaEventSynchronize(ev));
+        return SEM_OK;
+    }
+    for (int spin = 0;; ++spin) {
+        cudaError_t e = cudaEventQuery(ev);
+        if (e == cudaSuccess) return SEM_OK;
+        if (e != cudaErrorNotReady) CU(e);
+        std::string cerr;
+        if (comm_poll(ctx->comm, cerr)) {
+            comm_abort(ctx->comm);
+            ctx->broken = true;
+            return fail(ctx, SEM_ENCCL, "%s", cerr.c_str());
+        }
+        if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+}
+
+// Iterations in chunks of kChunk (a multiple of 4: the all-gather slot of
+// position q in a chunk is q & 3 == k & 3).  The device decides when to stop;
+// the host polls the sticky flag one chunk behind and launches no more chunks
+// once it is set (later kernels of a chunk are no-ops).  Each chunk is one
+// CUDA-graph launch unless profiling (per-launch events) or graphs are off.
+// Returns with the stream's work for the last chunk enqueued.
+static int run_chunks(sem_ctx *ctx, int maxit, cudaGraphExec_t gexec, cudaStream_t s) {
     CgVecs &v = ctx->cv;
+    const bool graph = gexec != nullptr;
     int rc;
-    int k = 0, c = 0;
+    int64_t k = 0;
+    int c = 0;
     while (true) {
         if (graph) {
             CU(cudaGraphLaunch(gexec, s));
@@ -960,18 +1004,20 @@ static int run_chunks(sem_ctx *ctx, int maxit, bool graph, cudaGraphExec_t gexec
             k += kChunk;
         } else {
             for (int q = 0; q < kChunk; ++q, ++k) {
-                rc = ctx->method == 2 ? enqueue_iteration_sr(ctx, k, s) : enqueue_iteration(ctx, k, s);
+                // (the host k only selects all-gather slots (k & 3) and profiling records)
+                const int kk = (int)(k & 0x3fffffff);
+                rc = ctx->method == 2 ? enqueue_iteration_sr(ctx, kk, s) : enqueue_iteration(ctx, kk, s);
                 if (rc) return rc;
             }
         }
         CU(cudaMemcpyAsync(&ctx->host_state[c & 1], v.st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
         CU(cudaEventRecord(ctx->ev[c & 1], s));
         if (c > 0) {
-            CU(cudaEventSynchronize(ctx->ev[(c - 1) & 1]));
+            if ((rc = wait_event(ctx, ctx->ev[(c - 1) & 1]))) return rc;
             if (ctx->host_state[(c - 1) & 1].done) break;
         }
-        if (k > maxit + 3 * kChunk) {  // the device must have stopped by now
-            CU(cudaEventSynchronize(ctx->ev[c & 1]));
+        if (k > (int64_t)maxit + 3 * kChunk) {  // the device must have stopped by now
+            if ((rc = wait_event(ctx, ctx->ev[c & 1]))) return rc;
             break;
         }
         ++c;
@@ -1005,10 +1051,9 @@ static int cg_sr_impl(sem_ctx *ctx, const double *b, double *x, double tol, int 
     if ((rc = exchange_impl(ctx, v.w, s))) return rc;
     LAUNCH(launch_sr_init(ctx->dm, v, s));
     LAUNCH(launch_k2(ctx->dm, v, true, s));
-    const bool graph = !ctx->prof && ctx->use_graph;
-    cudaGraphExec_t &gexec = ctx->graph_exec[2];
-    if (graph && !gexec && (rc = build_cg_graph(ctx))) return rc;
-    if ((rc = run_chunks(ctx, maxit, graph, gexec, s))) return rc;
+    cudaGraphExec_t gexec = nullptr;
+    if ((rc = chunk_graph(ctx, gexec))) return rc;
+    if ((rc = run_chunks(ctx, maxit, gexec, s))) return rc;
     LAUNCH(launch_sr_finish(ctx->dm, v, s));
     CU(cudaMemcpyAsync(&ctx->host_state[0], v.st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
@@ -1059,36 +1104,9 @@ static int cg_impl(sem_ctx *ctx, int precond, const double *b, double *x, double
         }
     }
 
-    // Iterations in chunks of kChunk (a multiple of 4: the all-gather slot of
-    // position q in a chunk is q & 3 == k & 3).  The device decides when to
-    // stop; the host polls the sticky flag one chunk behind and launches no
-    // more chunks once it is set (later kernels of a chunk are no-ops).  Each
-    // chunk is one CUDA-graph launch unless profiling (per-launch events).
-    const bool graph = !ctx->prof && ctx->use_graph;
-    cudaGraphExec_t &gexec = ctx->graph_exec[ctx->method];
-    if (graph && !gexec && (rc = build_cg_graph(ctx))) return rc;
-    int k = 0, c = 0;
-    while (true) {
-        if (graph) {
-            CU(cudaGraphLaunch(gexec, s));
-            ctx->launches += ctx->graph_kernels[ctx->method];
-            k += kChunk;
-        } else {
-            for (int q = 0; q < kChunk; ++q, ++k)
-                if ((rc = enqueue_iteration(ctx, k, s))) return rc;
-        }
-        CU(cudaMemcpyAsync(&ctx->host_state[c & 1], v.st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
-        CU(cudaEventRecord(ctx->ev[c & 1], s));
-        if (c > 0) {
-            CU(cudaEventSynchronize(ctx->ev[(c - 1) & 1]));
-            if (ctx->host_state[(c - 1) & 1].done) break;
-        }
-        if (k > maxit + 3 * kChunk) {  // the device must have stopped by now
-            CU(cudaEventSynchronize(ctx->ev[c & 1]));
-            break;
-        }
-        ++c;
-    }
+    cudaGraphExec_t gexec = nullptr;
+    if ((rc = chunk_graph(ctx, gexec))) return rc;
+    if ((rc = run_chunks(ctx, maxit, gexec, s))) return rc;
     LAUNCH(launch_cg_finish(ctx->dm, v, s));
     CU(cudaMemcpyAsync(&ctx->host_state[0], v.st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));

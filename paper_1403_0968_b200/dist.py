@@ -7,6 +7,12 @@
   gloo group, CUDA tensors on an NCCL group.
 The per-iteration data path (interface exchange, dot products) runs on the
 library's own NCCL communicator, not through here.
+
+``LoopbackGroup`` is the test harness for that data path on ONE GPU (NCCL
+refuses two ranks on one device): P ranks as P host threads of this process,
+each with its own torch stream and libsem context, joined by the library's
+in-process loopback transport (include/sem.h sem_loopback_unique_id).  The
+setup-time all-gather is a threading rendezvous.
 """
 from __future__ import annotations
 
@@ -94,3 +100,81 @@ def exchange_plan(mesh, N: int, group):
                              ctypes.byref(nslot), ctypes.byref(ng))
     sem._check(rc)
     return counts, ids[: nslot.value].copy(), int(ng.value)
+
+
+class LoopbackRank:
+    """Rank ``rank`` of a ``LoopbackGroup`` (pass as ``sem.Context(loopback=...)``)."""
+
+    def __init__(self, group, rank):
+        self.group, self.rank, self.nranks, self.id = group, rank, group.nranks, group.id
+
+    def allgather_fn(self):
+        return self.group._allgather_fn(self.rank)
+
+
+class LoopbackGroup:
+    """P in-process ranks on one device (test transport).  ``run(fn)`` calls
+    ``fn(rank: LoopbackRank)`` on P threads at once, each inside its own
+    ``torch.cuda.stream``, and returns the P results in rank order (the first
+    exception is re-raised after every thread has ended)."""
+
+    def __init__(self, nranks: int, device: int = 0):
+        import threading
+
+        from . import sem
+        self.nranks = int(nranks)
+        self.device = int(device)
+        nb = sem.lib().sem_nccl_id_bytes()
+        self.id = (ctypes.c_uint8 * nb)()
+        rc = sem.lib().sem_loopback_unique_id(ctypes.cast(self.id, ctypes.c_void_p))
+        if rc != 0:
+            raise sem.SemError(rc, "sem_loopback_unique_id failed")
+        self._barrier = threading.Barrier(self.nranks, timeout=300)
+        self._slots = [None] * self.nranks
+
+    def _allgather_fn(self, rank):
+        from .sem import ALLGATHER_FN
+
+        def _cb(user, send, nbytes, recv):
+            try:
+                self._slots[rank] = ctypes.string_at(send, nbytes)
+                self._barrier.wait()
+                blob = b"".join(self._slots)
+                ctypes.memmove(recv, blob, len(blob))
+                self._barrier.wait()
+                return 0
+            except Exception:  # never raise across the C ABI
+                self._barrier.abort()
+                return 1
+
+        return ALLGATHER_FN(_cb)
+
+    def rank(self, r: int) -> LoopbackRank:
+        return LoopbackRank(self, r)
+
+    def run(self, fn):
+        import threading
+
+        import torch
+        out = [None] * self.nranks
+        errs = [None] * self.nranks
+
+        def _body(r):
+            try:
+                torch.cuda.set_device(self.device)
+                with torch.cuda.stream(torch.cuda.Stream(self.device)):
+                    out[r] = fn(self.rank(r))
+                    torch.cuda.current_stream().synchronize()
+            except BaseException as e:  # noqa: BLE001 -- re-raised below
+                errs[r] = e
+                self._barrier.abort()
+
+        th = [threading.Thread(target=_body, args=(r,), daemon=True) for r in range(self.nranks)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        for e in errs:
+            if e is not None:
+                raise e
+        return out

@@ -43,7 +43,7 @@ class SemMesh(ctypes.Structure):
 EXPORTS = ["sem_version", "sem_gll", "sem_workspace_bytes", "sem_setup", "sem_sizes",
            "sem_ax", "sem_dssum", "sem_mask", "sem_mass", "sem_cg", "sem_launch_count",
            "sem_free", "sem_strerror", "sem_last_error", "sem_nccl_id_bytes",
-           "sem_nccl_get_unique_id", "sem_profile", "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan",
+           "sem_nccl_get_unique_id", "sem_loopback_unique_id", "sem_profile", "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan",
            "sem_pcg", "sem_diag", "sem_cg_sr", "fd_weights", "fd2d_step", "fd2d_run"]
 
 # preconditioners of sem_pcg (include/sem.h enum sem_precond)
@@ -99,11 +99,12 @@ def lib():
     L.sem_profile_read.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                    ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double)]
     L.sem_nccl_get_unique_id.argtypes = [P]
+    L.sem_loopback_unique_id.argtypes = [P]
     L.sem_kernel_replay.argtypes = [P, ctypes.c_int, ctypes.c_int]
     L.sem_exchange_plan.argtypes = [ctypes.POINTER(SemMesh), ctypes.c_int, P, P, i64,
                                     ctypes.POINTER(i64), ctypes.POINTER(i64)]
     for f in ("sem_gll", "sem_workspace_bytes", "sem_setup", "sem_sizes", "sem_ax", "sem_dssum",
-              "sem_mask", "sem_mass", "sem_cg", "sem_nccl_get_unique_id", "sem_profile",
+              "sem_mask", "sem_mass", "sem_cg", "sem_nccl_get_unique_id", "sem_loopback_unique_id", "sem_profile",
               "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan", "sem_pcg", "sem_diag", "sem_cg_sr"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
@@ -138,10 +139,14 @@ class Context:
     xyz [E,3,n^3] f64, glo [E,n^3] i64, dirichlet [E,n^3] u8 and optional
     nboundary).  ``group``: torch.distributed process group for nranks > 1.
     ``kappa`` / ``alpha``: per-local-node screened-Coulomb coefficients
-    (host arrays, [E*n^3]; None = Poisson), see include/sem.h."""
+    (host arrays, [E*n^3]; None = Poisson), see include/sem.h.
+    ``loopback``: a ``dist.LoopbackRank`` -- this context is one rank of an
+    in-process multi-rank world on one GPU (test transport, include/sem.h
+    sem_loopback_unique_id); the device work goes on the CALLING thread's
+    current torch stream."""
 
     def __init__(self, mesh, N: int | None = None, device: int | None = None, group=None,
-                 kappa=None, alpha=None):
+                 kappa=None, alpha=None, loopback=None):
         import torch
         L = lib()
         self.N = int(mesh.N if N is None else N)
@@ -168,7 +173,14 @@ class Context:
         m.alpha = None if self._alpha is None else self._alpha.ctypes.data
         self._group = group
         self._keep = []
-        if group is not None and torch.distributed.get_world_size(group) > 1:
+        if loopback is not None:
+            m.rank, m.nranks = int(loopback.rank), int(loopback.nranks)
+            self._keep.append(loopback.id)
+            m.nccl_id = ctypes.cast(loopback.id, ctypes.c_void_p)
+            cb = loopback.allgather_fn()
+            self._keep.append(cb)
+            m.allgather = cb
+        elif group is not None and torch.distributed.get_world_size(group) > 1:
             from . import dist as _dist
             m.rank = torch.distributed.get_rank(group)
             m.nranks = torch.distributed.get_world_size(group)
