@@ -256,16 +256,16 @@ def run_fd(args, rank, world):
     sampler = ClockSampler(local_rank)
     sampler.start()
     time.sleep(0.3)
-    for r in args.fd_radii:
+    def timed(r, regrouped):
         om = fd.weights(r, 2.0 / n)
         dt = 0.2 * 2.0 / n
-        fd.run(u1, u2, u3, om, dt, max(args.warmup, 3))
+        fd.run(u1, u2, u3, om, dt, max(args.warmup, 3), regrouped=regrouped)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        fd.run(u1, u2, u3, om, dt, args.steps)
+        fd.run(u1, u2, u3, om, dt, args.steps, regrouped=regrouped)
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
@@ -274,11 +274,18 @@ def run_fd(args, rank, world):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         nodes = float(n) * n * args.steps * world
-        sweep[2 * r + 1] = {"mnodes_s": nodes / (ms * 1e-3) / 1e6, "us_per_step": 1e3 * ms / args.steps,
-                            "achieved_gbs": 24.0 * n * n / (ms / args.steps * 1e-3) / 1e9}
-        # input data was rotated: refresh so every radius starts from finite values
+        # input data was rotated: refresh so every run starts from finite values
         u1.uniform_(-1, 1)
         u2.uniform_(-1, 1)
+        return {"mnodes_s": nodes / (ms * 1e-3) / 1e6, "us_per_step": 1e3 * ms / args.steps,
+                "achieved_gbs": 24.0 * n * n / (ms / args.steps * 1e-3) / 1e9}
+
+    # default (the listing's operation order, bit-exact with the oracle) and
+    # the opt-in pair-regrouped FMA form (fd2d_run_ex FD_REGROUPED, reading R6c)
+    regrouped = {}
+    for r in args.fd_radii:
+        sweep[2 * r + 1] = timed(r, False)
+        regrouped[2 * r + 1] = timed(r, True)
     clocks = sampler.stop()
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -307,15 +314,18 @@ def run_fd(args, rank, world):
                "config": {"workload": f"fd2d (lst:fdCode) {n}x{n} periodic grid per GPU, stencil "
                                       f"size {rmax} (headline) and the sweep 3..15",
                           "grid": [n, n], "stencil_size": rmax,
+                          "arithmetic": "the listing's operation order (bit-exact with the "
+                                        "oracle); sweep_regrouped: FD_REGROUPED",
                           "l2": "inputs larger than L2: 3 x 512 MiB fields"},
                "sweep": {str(k): v for k, v in sweep.items()},
+               "sweep_regrouped": {str(k): v for k, v in regrouped.items()},
                "roofline": {"bound": "hbm", "kernel": f"fd2d_kernel<{args.fd_radii[-1]}>",
                             "achieved": head["achieved_gbs"], "peak": peak, "unit": "GB/s",
                             "frac": head["achieved_gbs"] / peak, "traffic": None,
                             "peak_source": peak_src,
                             "bytes_per_node": "24 (u1, u2 read; u3 written)",
                             "timing": "CUDA events around fd2d_run(steps) on the launching stream"},
-               "gpu_launches": args.steps * len(args.fd_radii),
+               "gpu_launches": 2 * args.steps * len(args.fd_radii),
                "cpu_baseline": cpu, "clocks": clocks}
         print(json.dumps(out), flush=True)
     if world > 1:

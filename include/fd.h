@@ -51,6 +51,17 @@ int fd2d_step(const double *u1, const double *u2, double *u3, int64_t w, int64_t
 int fd2d_run(double *u1, double *u2, double *u3, int64_t w, int64_t h, int r, const double *omega,
              double dt, int steps, void *stream, int *latest);
 
+/* fd2d_run with options.  flags = 0: exactly fd2d_run (the listing's operation
+ * order, bit-identical to a plain C evaluation).  FD_REGROUPED: the
+ * pair-regrouped FMA form (reading R6c)
+ *   lap = omega_0 (u + u) + sum_k omega_k ((u_{i-k} + u_{i+k}) + (u_{j-k} + u_{j+k}))
+ * -- 4r+3 FP64 operations per node instead of 8r+8, equal to the listing up
+ * to rounding; requires exactly symmetric weights (omega_{-k} == omega_k, as
+ * fd_weights returns), else SEM_EINVAL.  Unknown flags: SEM_EINVAL. */
+#define FD_REGROUPED 1
+int fd2d_run_ex(double *u1, double *u2, double *u3, int64_t w, int64_t h, int r,
+                const double *omega, double dt, int steps, int flags, void *stream, int *latest);
+
 #ifdef __cplusplus
 }
 #endif

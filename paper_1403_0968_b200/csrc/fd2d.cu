@@ -10,10 +10,13 @@
 // by cp.async, kP rows ahead; each thread owns two adjacent columns, keeps
 // their 2r+1 u1 values of the column in registers (the y-neighbours) and
 // reads the x-neighbours of the center row from shared memory as 16-byte
-// pairs.  omega lives in constant memory (uniform operands).  The arithmetic
+// pairs.  omega is a __grid_constant__ kernel parameter (uniform operands in
+// the parameter bank; no process-wide __constant__ state, so concurrent calls
+// with different weights on different streams cannot race).  The arithmetic
 // is the listing's, operation by operation, with explicit round-to-nearest
 // intrinsics (no FMA contraction), so every u3 is bit-identical to a plain C
-// evaluation of lst:fdCode.  SYM (symmetric weights, omega_{-k} = omega_k, as
+// evaluation of lst:fdCode -- the default of fd2d_step / fd2d_run.  SYM
+// (fd2d_run_ex with FD_REGROUPED; symmetric weights omega_{-k} = omega_k, as
 // every central stencil has): the same sum regrouped by pairs,
 //   lap = omega_0 (u + u) + sum_{k=1..r} omega_k ((u_{i-k} + u_{i+k}) + (u_{j-k} + u_{j+k}))
 // with FMAs: 4r + 3 FP64 operations per node instead of 8r + 8 (the kernel is
@@ -21,6 +24,7 @@
 // (reading R6c; tests bound the difference).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -37,7 +41,9 @@ constexpr int kNT = 128;          // threads per CTA
 constexpr int kTW = 2 * kNT;      // tile width (columns), two per thread
 constexpr int kP = 4;             // rows in flight
 
-__constant__ double c_omega[2 * FD_RMAX + 1];
+struct Omega {
+    double w[2 * FD_RMAX + 1];
+};
 
 template <int R>
 struct FdCfg {
@@ -78,7 +84,9 @@ template <int R, bool SYM>
 __global__ void __launch_bounds__(kNT, 3) fd2d_kernel(const double *__restrict__ u1,
                                                     const double *__restrict__ u2,
                                                     double *__restrict__ u3, int64_t w, int64_t h,
-                                                    int ty, double dt2) {
+                                                    int ty, double dt2,
+                                                    const __grid_constant__ Omega om_) {
+    const double *c_omega = om_.w;
     using C = FdCfg<R>;
     constexpr int NB = C::NB, RW = C::RW, LP = C::LP, XO = C::XO;
     extern __shared__ __align__(16) double smem[];
@@ -232,50 +240,50 @@ static int strip_rows(int r) {
 
 template <int R, bool SYM>
 static cudaError_t launch_rs(const double *u1, const double *u2, double *u3, int64_t w, int64_t h,
-                             double dt2, cudaStream_t s) {
+                             double dt2, const Omega &om, cudaStream_t s) {
     using C = FdCfg<R>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(fd2d_kernel<R, SYM>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    // the shared-memory opt-in is per device: one bit per ordinal (set after a
+    // successful call; a racing second call just repeats it)
+    static std::atomic<uint64_t> attr_set{0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = dev < 64 ? (uint64_t(1) << dev) : 0;
+    if (!bit || !(attr_set.load(std::memory_order_acquire) & bit)) {
+        e = cudaFuncSetAttribute(fd2d_kernel<R, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)C::SMEM);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr_set.fetch_or(bit, std::memory_order_acq_rel);
     }
     const int ty = strip_rows(R);
     dim3 grid((unsigned)((w + kTW - 1) / kTW), (unsigned)((h + ty - 1) / ty));
-    fd2d_kernel<R, SYM><<<grid, kNT, C::SMEM, s>>>(u1, u2, u3, w, h, ty, dt2);
+    fd2d_kernel<R, SYM><<<grid, kNT, C::SMEM, s>>>(u1, u2, u3, w, h, ty, dt2, om);
     return cudaGetLastError();
 }
 
 template <int R>
 static cudaError_t launch_r(bool sym, const double *u1, const double *u2, double *u3, int64_t w,
-                            int64_t h, double dt2, cudaStream_t s) {
-    return sym ? launch_rs<R, true>(u1, u2, u3, w, h, dt2, s)
-               : launch_rs<R, false>(u1, u2, u3, w, h, dt2, s);
+                            int64_t h, double dt2, const Omega &om, cudaStream_t s) {
+    return sym ? launch_rs<R, true>(u1, u2, u3, w, h, dt2, om, s)
+               : launch_rs<R, false>(u1, u2, u3, w, h, dt2, om, s);
 }
 
 static cudaError_t launch(int r, bool sym, const double *u1, const double *u2, double *u3,
-                          int64_t w, int64_t h, double dt2, cudaStream_t s) {
+                          int64_t w, int64_t h, double dt2, const Omega &om, cudaStream_t s) {
     switch (r) {
-    case 1: return launch_r<1>(sym, u1, u2, u3, w, h, dt2, s);
-    case 2: return launch_r<2>(sym, u1, u2, u3, w, h, dt2, s);
-    case 3: return launch_r<3>(sym, u1, u2, u3, w, h, dt2, s);
-    case 4: return launch_r<4>(sym, u1, u2, u3, w, h, dt2, s);
-    case 5: return launch_r<5>(sym, u1, u2, u3, w, h, dt2, s);
-    case 6: return launch_r<6>(sym, u1, u2, u3, w, h, dt2, s);
-    case 7: return launch_r<7>(sym, u1, u2, u3, w, h, dt2, s);
+    case 1: return launch_r<1>(sym, u1, u2, u3, w, h, dt2, om, s);
+    case 2: return launch_r<2>(sym, u1, u2, u3, w, h, dt2, om, s);
+    case 3: return launch_r<3>(sym, u1, u2, u3, w, h, dt2, om, s);
+    case 4: return launch_r<4>(sym, u1, u2, u3, w, h, dt2, om, s);
+    case 5: return launch_r<5>(sym, u1, u2, u3, w, h, dt2, om, s);
+    case 6: return launch_r<6>(sym, u1, u2, u3, w, h, dt2, om, s);
+    case 7: return launch_r<7>(sym, u1, u2, u3, w, h, dt2, om, s);
     default: return cudaErrorInvalidValue;
     }
 }
 
-// the pair-regrouped kernel for exactly symmetric weights, unless
-// SEM_FD_EXACT=1 forces the listing's operation order
-static bool use_sym(int r, const double *omega) {
-    static const bool exact = [] {
-        const char *e = getenv("SEM_FD_EXACT");
-        return e && e[0] == '1';
-    }();
-    if (exact) return false;
+// FD_REGROUPED needs exactly symmetric weights (the pairs share one omega)
+static bool symmetric(int r, const double *omega) {
     for (int k = 1; k <= r; ++k)
         if (!(omega[r - k] == omega[r + k])) return false;
     return true;
@@ -296,11 +304,10 @@ static int check(const double *u1, const double *u2, const double *u3, int64_t w
     return SEM_OK;
 }
 
-static int upload(int r, const double *omega, cudaStream_t s) {
-    cudaError_t e = cudaMemcpyToSymbolAsync(c_omega, omega, sizeof(double) * (2 * r + 1), 0,
-                                            cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return fd_fail(SEM_ECUDA, cudaGetErrorString(e));
-    return SEM_OK;
+static Omega pack(int r, const double *omega) {
+    Omega o{};
+    for (int k = 0; k <= 2 * r; ++k) o.w[k] = omega[k];
+    return o;
 }
 
 }  // namespace sem_fd
@@ -348,29 +355,37 @@ extern "C" int fd2d_step(const double *u1, const double *u2, double *u3, int64_t
                          const double *omega, double dt, void *stream) {
     int rc = check(u1, u2, u3, w, h, r, omega, dt);
     if (rc) return rc;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if ((rc = upload(r, omega, s))) return rc;
-    cudaError_t e = launch(r, use_sym(r, omega), u1, u2, u3, w, h, dt * dt, s);
+    cudaError_t e = launch(r, false, u1, u2, u3, w, h, dt * dt, pack(r, omega),
+                           static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return fd_fail(SEM_ECUDA, cudaGetErrorString(e));
     return SEM_OK;
 }
 
-extern "C" int fd2d_run(double *u1, double *u2, double *u3, int64_t w, int64_t h, int r,
-                        const double *omega, double dt, int steps, void *stream, int *latest) {
+extern "C" int fd2d_run_ex(double *u1, double *u2, double *u3, int64_t w, int64_t h, int r,
+                           const double *omega, double dt, int steps, int flags, void *stream,
+                           int *latest) {
     int rc = check(u1, u2, u3, w, h, r, omega, dt);
     if (rc) return rc;
     if (steps < 0) return fd_fail(SEM_EINVAL, "fd2d_run: steps < 0");
+    if (flags & ~FD_REGROUPED) return fd_fail(SEM_EINVAL, "fd2d_run_ex: unknown flags");
+    const bool sym = (flags & FD_REGROUPED) != 0;
+    if (sym && !symmetric(r, omega))
+        return fd_fail(SEM_EINVAL, "fd2d_run_ex: FD_REGROUPED needs omega_{-k} == omega_k");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if ((rc = upload(r, omega, s))) return rc;
-    const bool sym = use_sym(r, omega);
+    const Omega om = pack(r, omega);
     double *b[3] = {u1, u2, u3};
     int role[3] = {0, 1, 2};     // argument buffer playing u1, u2, u3
     for (int t = 0; t < steps; ++t) {
-        cudaError_t e = launch(r, sym, b[role[0]], b[role[1]], b[role[2]], w, h, dt * dt, s);
+        cudaError_t e = launch(r, sym, b[role[0]], b[role[1]], b[role[2]], w, h, dt * dt, om, s);
         if (e != cudaSuccess) return fd_fail(SEM_ECUDA, cudaGetErrorString(e));
         const int n1 = role[2], n2 = role[0], n3 = role[1];   // (u1, u2, u3) <- (u3, u1, u2)
         role[0] = n1, role[1] = n2, role[2] = n3;
     }
     if (latest) *latest = role[0];
     return SEM_OK;
+}
+
+extern "C" int fd2d_run(double *u1, double *u2, double *u3, int64_t w, int64_t h, int r,
+                        const double *omega, double dt, int steps, void *stream, int *latest) {
+    return fd2d_run_ex(u1, u2, u3, w, h, r, omega, dt, steps, 0, stream, latest);
 }

@@ -22,7 +22,9 @@ def lib():
         L.fd2d_step.argtypes = [P, P, P, i64, i64, ctypes.c_int, P, ctypes.c_double, P]
         L.fd2d_run.argtypes = [P, P, P, i64, i64, ctypes.c_int, P, ctypes.c_double, ctypes.c_int,
                                P, ctypes.POINTER(ctypes.c_int)]
-        for f in (L.fd_weights, L.fd2d_step, L.fd2d_run):
+        L.fd2d_run_ex.argtypes = [P, P, P, i64, i64, ctypes.c_int, P, ctypes.c_double,
+                                  ctypes.c_int, ctypes.c_int, P, ctypes.POINTER(ctypes.c_int)]
+        for f in (L.fd_weights, L.fd2d_step, L.fd2d_run, L.fd2d_run_ex):
             f.restype = ctypes.c_int
         _fd = L
     return _fd
@@ -63,16 +65,22 @@ def step(u1, u2, u3, omega, dt: float, stream=None):
     return u3
 
 
-def run(u1, u2, u3, omega, dt: float, steps: int, stream=None):
+FD_REGROUPED = 1
+
+
+def run(u1, u2, u3, omega, dt: float, steps: int, stream=None, regrouped: bool = False):
     """`steps` steps with (u1, u2, u3) <- (u3, u1, u2) after each (reading R6b).
-    Returns (newest, previous) tensors."""
+    regrouped=True: fd2d_run_ex with FD_REGROUPED (pair-regrouped FMA form,
+    reading R6c; symmetric weights only); default: the listing's order,
+    bit-identical to the oracle.  Returns (newest, previous) tensors."""
     import torch
     h, w = u1.shape
     om = np.ascontiguousarray(omega, dtype=np.float64)
     s = (stream or torch.cuda.current_stream()).cuda_stream
     latest = ctypes.c_int(-1)
-    _check(lib().fd2d_run(_grid(u1, "u1"), _grid(u2, "u2"), _grid(u3, "u3"), w, h, om.size // 2,
-                          om.ctypes.data_as(ctypes.c_void_p), float(dt), int(steps),
-                          ctypes.c_void_p(s), ctypes.byref(latest)))
+    _check(lib().fd2d_run_ex(_grid(u1, "u1"), _grid(u2, "u2"), _grid(u3, "u3"), w, h,
+                             om.size // 2, om.ctypes.data_as(ctypes.c_void_p), float(dt),
+                             int(steps), FD_REGROUPED if regrouped else 0, ctypes.c_void_p(s),
+                             ctypes.byref(latest)))
     bufs = (u1, u2, u3)
     return bufs[latest.value], bufs[(latest.value + 1) % 3]

@@ -44,7 +44,7 @@ EXPORTS = ["sem_version", "sem_gll", "sem_workspace_bytes", "sem_setup", "sem_si
            "sem_ax", "sem_dssum", "sem_mask", "sem_mass", "sem_cg", "sem_launch_count",
            "sem_free", "sem_strerror", "sem_last_error", "sem_nccl_id_bytes",
            "sem_nccl_get_unique_id", "sem_loopback_unique_id", "sem_profile", "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan",
-           "sem_pcg", "sem_diag", "sem_cg_sr", "fd_weights", "fd2d_step", "fd2d_run"]
+           "sem_pcg", "sem_diag", "sem_cg_sr", "fd_weights", "fd2d_step", "fd2d_run", "fd2d_run_ex"]
 
 # preconditioners of sem_pcg (include/sem.h enum sem_precond)
 PRECOND = {"none": 0, "jacobi": 1}

@@ -3,11 +3,11 @@
 C ABI (include/fd.h) against the oracle's ora_fd_step on the same seeded
 inputs and the same weights.
 
-* General weights: the kernel evaluates the listing's operations in the same
-  order without FMA contraction -> BIT-EXACT equality (tested with slightly
-  asymmetric weights, which select that kernel).
-* Symmetric weights (every central stencil; the benchmark's): the pair-
-  regrouped FMA kernel (reading R6c) -> within the rounding bound
+* fd2d_step / fd2d_run (the default, any weights -- the central stencils of
+  fd_weights included): the kernel evaluates the listing's operations in the
+  same order without FMA contraction -> BIT-EXACT equality.
+* fd2d_run_ex(FD_REGROUPED), symmetric weights only: the pair-regrouped FMA
+  kernel (reading R6c) -> within the rounding bound
   (4r + 8) eps (2|u1| + |u2| + dt^2 sum|omega| 2 max|u1|), eps = 2^-53."""
 import numpy as np
 import pytest
@@ -38,7 +38,7 @@ def T(a, dev):
 
 
 def asym(om):
-    """The same weights with omega_{+r} nudged: not symmetric -> listing-order kernel."""
+    """The same weights with omega_{+r} nudged (not symmetric)."""
     om = om.copy()
     om[-1] *= 1.0 + 2.0 ** -20
     return om
@@ -55,12 +55,15 @@ SHAPES = [(64, 256), (100, 300), (37, 513), (129, 17), (15, 15), (70, 1024)]
 
 @pytest.mark.parametrize("r", range(1, 8))
 @pytest.mark.parametrize("h,w", SHAPES)
-def test_fd_step_bit_exact(dev, r, h, w):
+@pytest.mark.parametrize("weights", ["central", "asym"])
+def test_fd_step_bit_exact(dev, r, h, w, weights):
     from paper_1403_0968_b200 import fd
     if min(h, w) < 2 * r + 1:
         pytest.skip("grid smaller than the stencil")
     u1, u2 = fields(h, w, r * 1000 + h + w)
-    om = asym(oracle.fd_weights(r, 2.0 / w))
+    om = oracle.fd_weights(r, 2.0 / w)
+    if weights == "asym":
+        om = asym(om)
     dt = 0.3 * 2.0 / w
     ref = oracle.fd_step(u1, u2, om, dt)
     u3 = torch.empty((h, w), dtype=torch.float64, device=dev)
@@ -70,7 +73,7 @@ def test_fd_step_bit_exact(dev, r, h, w):
 
 @pytest.mark.parametrize("r", range(1, 8))
 @pytest.mark.parametrize("h,w", SHAPES)
-def test_fd_step_symmetric_within_rounding(dev, r, h, w):
+def test_fd_regrouped_within_rounding(dev, r, h, w):
     from paper_1403_0968_b200 import fd
     if min(h, w) < 2 * r + 1:
         pytest.skip("grid smaller than the stencil")
@@ -79,9 +82,20 @@ def test_fd_step_symmetric_within_rounding(dev, r, h, w):
     dt = 0.3 * 2.0 / w
     ref = oracle.fd_step(u1, u2, om, dt)
     u3 = torch.empty((h, w), dtype=torch.float64, device=dev)
-    fd.step(T(u1, dev), T(u2, dev), u3, om, dt)
+    new, _ = fd.run(T(u1, dev), T(u2, dev), u3, om, dt, 1, regrouped=True)
+    assert new is u3
     err = np.abs(u3.cpu().numpy() - ref)
     assert np.all(err <= sym_bound(u1, u2, om, dt)), err.max()
+
+
+def test_fd_regrouped_rejects_asymmetric_weights(dev):
+    from paper_1403_0968_b200 import fd, sem
+    h, w, r = 32, 64, 3
+    u1, u2 = fields(h, w, 1)
+    g = [T(u1, dev), T(u2, dev), torch.empty((h, w), dtype=torch.float64, device=dev)]
+    with pytest.raises(sem.SemError) as ei:
+        fd.run(*g, asym(oracle.fd_weights(r, 2.0 / w)), 0.01, 1, regrouped=True)
+    assert ei.value.code == sem.SEM_EINVAL
 
 
 @pytest.mark.parametrize("r", [1, 3, 7])
@@ -106,9 +120,9 @@ def test_fd_run_rotation_bit_exact(dev, r):
 
 
 def test_fd_full_size_r7(dev):
-    """The benchmark grid (8192 x 8192, stencil size 15): the symmetric kernel
-    bench.py --workload fd times, within the rounding bound everywhere, and
-    the listing-order kernel bit-exact."""
+    """The benchmark grid (8192 x 8192, stencil size 15): the default kernel
+    bench.py --workload fd times bit-exact with the central weights, the
+    regrouped variant within the rounding bound everywhere."""
     from paper_1403_0968_b200 import fd
     h = w = 8192
     r = 7
@@ -119,15 +133,15 @@ def test_fd_full_size_r7(dev):
     g1, g2 = T(u1, dev), T(u2, dev)
     u3 = torch.empty((h, w), dtype=torch.float64, device=dev)
     fd.step(g1, g2, u3, om, dt)
+    np.testing.assert_array_equal(u3.cpu().numpy(), ref)
+    fd.run(g1, g2, u3, om, dt, 1, regrouped=True)
     assert np.all(np.abs(u3.cpu().numpy() - ref) <= sym_bound(u1, u2, om, dt))
-    oa = asym(om)
-    fd.step(g1, g2, u3, oa, dt)
-    np.testing.assert_array_equal(u3.cpu().numpy(), oracle.fd_step(u1, u2, oa, dt))
 
 
 def test_fd_library_weights_drive_the_kernel(dev):
-    """The library's own (Fornberg) weights, used end to end, stay within
-    rounding of the oracle's closed-form ones."""
+    """The library's own (Fornberg) weights, used end to end: bit-exact with
+    the oracle's step on the same weights, and within rounding of the oracle's
+    closed-form weights."""
     from paper_1403_0968_b200 import fd
     h, w, r = 64, 512, 5
     u1, u2 = fields(h, w, 5)
@@ -136,12 +150,35 @@ def test_fd_library_weights_drive_the_kernel(dev):
     dt = 0.3 * 2.0 / w
     u3 = torch.empty((h, w), dtype=torch.float64, device=dev)
     fd.step(T(u1, dev), T(u2, dev), u3, om_lib, dt)
+    np.testing.assert_array_equal(u3.cpu().numpy(), oracle.fd_step(u1, u2, om_lib, dt))
     ref = oracle.fd_step(u1, u2, om_ora, dt)
     np.testing.assert_allclose(u3.cpu().numpy(), ref, rtol=0, atol=1e-12 * np.abs(ref).max())
 
 
+@pytest.mark.parametrize("r", [1, 3, 7])
+@pytest.mark.parametrize("h,w", [(17, 17), (32, 32), (48, 64)])
+def test_fd_run_default_weights_bit_exact(dev, r, h, w):
+    """10 steps with the library's central weights on SPEC.md's shapes: the
+    default path is bit-exact with the oracle (no regrouping
+    unless asked for)."""
+    from paper_1403_0968_b200 import fd
+    if min(h, w) < 2 * r + 1:
+        pytest.skip("grid smaller than the stencil")
+    steps = 10
+    u1, u2 = fields(h, w, 3 + r + h)
+    om = fd.weights(r, 2.0 / w)
+    dt = 0.25 * 2.0 / w
+    a, b = u1.copy(), u2.copy()
+    for _ in range(steps):
+        a, b = oracle.fd_step(a, b, om, dt), a
+    g1, g2 = T(u1, dev), T(u2, dev)
+    new, prev = fd.run(g1, g2, torch.empty_like(g1), om, dt, steps)
+    np.testing.assert_array_equal(new.cpu().numpy(), a)
+    np.testing.assert_array_equal(prev.cpu().numpy(), b)
+
+
 @pytest.mark.parametrize("r", [2, 7])
-def test_fd_run_symmetric(dev, r):
+def test_fd_run_regrouped(dev, r):
     from paper_1403_0968_b200 import fd
     h, w, steps = 64, 512, 4
     u1, u2 = fields(h, w, 3 + r)
@@ -151,7 +188,29 @@ def test_fd_run_symmetric(dev, r):
     for _ in range(steps):
         a, b = oracle.fd_step(a, b, om, dt), a
     g1, g2 = T(u1, dev), T(u2, dev)
-    new, prev = fd.run(g1, g2, torch.empty_like(g1), om, dt, steps)
+    new, prev = fd.run(g1, g2, torch.empty_like(g1), om, dt, steps, regrouped=True)
     # the literal update amplifies (|-2 - dt^2 s| > 1): bound relative to the size
     np.testing.assert_allclose(new.cpu().numpy(), a, rtol=0, atol=1e-12 * np.abs(a).max())
     np.testing.assert_allclose(prev.cpu().numpy(), b, rtol=0, atol=1e-12 * np.abs(b).max())
+
+
+def test_fd_concurrent_streams_different_weights(dev):
+    """Two streams with different radii and weights interleaved: each result
+    bit-exact (omega travels with the launch, no shared __constant__ state)."""
+    from paper_1403_0968_b200 import fd
+    h, w = 96, 512
+    outs = []
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    jobs = []
+    for q, r in enumerate((2, 6)):
+        u1, u2 = fields(h, w, 40 + q)
+        om = asym(oracle.fd_weights(r, 2.0 / w))
+        g = [T(u1, dev), T(u2, dev), torch.empty((h, w), dtype=torch.float64, device=dev)]
+        jobs.append((u1, u2, om, g))
+    torch.cuda.synchronize()
+    for _ in range(20):
+        for (u1, u2, om, g), st in zip(jobs, streams):
+            fd.step(g[0], g[1], g[2], om, 0.01, stream=st)
+    torch.cuda.synchronize()
+    for u1, u2, om, g in jobs:
+        np.testing.assert_array_equal(g[2].cpu().numpy(), oracle.fd_step(u1, u2, om, 0.01))
