@@ -60,8 +60,12 @@ def parse():
     ap.add_argument("--fd-radii", type=int, nargs="+", default=[1, 2, 3, 4, 5, 6, 7])
     ap.add_argument("--cpu-its", type=int, default=100,
                     help="oracle CG iterations timed for cpu_baseline (bounded sample)")
-    ap.add_argument("--ref-its", type=int, default=3,
+    ap.add_argument("--ref-its", type=int, default=10,
                     help="oracle CG iterations per --impl reference step")
+    ap.add_argument("--cpu-threads", type=int, default=0,
+                    help="oracle threads for the all-core baseline (0 = the affinity count)")
+    ap.add_argument("--cpu-c4", action="store_true",
+                    help="cpu_baseline also times one oracle Ax per N = 3..15 at ~16M DOF (c4; slow)")
     return ap.parse_args()
 
 
@@ -180,9 +184,22 @@ def coefficients(args, m):
     return meshgen.coefficients(m) if args.operator == "screened" else (None, None)
 
 
+def host_cores():
+    """Cores this process may run on (sched_getaffinity), and the oracle
+    thread count for the all-core baseline."""
+    try:
+        n = len(os.sched_getaffinity(0))
+    except Exception:
+        n = os.cpu_count() or 1
+    return n
+
+
 def oracle_sample(args, its_per_call, calls):
     """Time the plain-C oracle's CG (tol = 0, fixed iterations) on rank 0's c3
-    mesh.  Returns (seconds per call list, L)."""
+    mesh.  Returns (seconds per call list, L); each entry is the time of a
+    maxit = its_per_call solve minus that of a maxit = 0 solve (the oracle's
+    own setup inside the call: sorting the global ids, the initial residual),
+    so it covers exactly its_per_call iterations."""
     import oracle
     from paper_1403_0968_b200 import meshgen
     xi, _ = oracle.gll(args.N)
@@ -192,38 +209,112 @@ def oracle_sample(args, its_per_call, calls):
     b = oracle.mass_rhs(args.N, m.glo, m.dirichlet, J, f)
     kappa, alpha = coefficients(args, m)
     co = {} if kappa is None else {"J": J, "kappa": kappa, "alpha": alpha}
-    times = []
-    for _ in range(calls):
+    def solve(its):
         t0 = time.perf_counter()
         if args.cg_variant == "single_reduction":
-            oracle.cg_single_reduction(args.N, m.glo, m.dirichlet, G, b, tol=0.0, maxit=its_per_call)
+            oracle.cg_single_reduction(args.N, m.glo, m.dirichlet, G, b, tol=0.0, maxit=its)
         else:
-            oracle.cg(args.N, m.glo, m.dirichlet, G, b, tol=0.0, maxit=its_per_call,
+            oracle.cg(args.N, m.glo, m.dirichlet, G, b, tol=0.0, maxit=its,
                       precond=args.precond, **co)
-        times.append(time.perf_counter() - t0)
+        return time.perf_counter() - t0
+
+    t_setup = min(solve(0) for _ in range(2))
+    times = [max(solve(its_per_call) - t_setup, 1e-9) for _ in range(calls)]
     return times, m.nlocal
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    import oracle
     steps, warm = args.steps, args.warmup
+    cores = args.cpu_threads or host_cores()
+    oracle.set_threads(cores)
     times, L = oracle_sample(args, args.ref_its, steps + warm)
+    oracle.set_threads(1)
     t = sum(times[warm:])
     value = L * args.ref_its * steps / t / 1e9
-    sample = (f"oracle (plain C, 1 thread) CG, {args.ref_its} iterations (tol=0) per step on the "
-              f"c3 mesh of rank 0 ({L} local DOF); setup untimed")
+    sample = (f"oracle (plain C, operator element loop on {cores} OpenMP threads, sequential "
+              f"dot products / DSSUM) CG, {args.ref_its} iterations (tol=0) per step on the "
+              f"c3 mesh of rank 0 ({L} local DOF); the oracle's setup (maxit = 0 call) "
+              "subtracted")
     out = {"metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": steps,
            "warmup": warm, "ms_per_step": 1e3 * t / steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "impl": "reference",
            "config": {"workload": workload_name(args, world), "N": args.N,
                       "elements_per_gpu": args.elems[0] * args.elems[1] * args.elems[2]},
-           "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": 1, "kind": "oracle",
-                            "sample": sample, "cpu": cpu_info()},
+           "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "oracle",
+                            "sample": sample, "cpu": cpu_info(),
+                            "affinity_cores": host_cores()},
            "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def cpu_baseline(args):
+    """The plain-C oracle on this host (rank 0, N = 1): c3 CG throughput on 1
+    core and on all cores (OpenMP over the operator's elements; dot products,
+    DSSUM and the recurrence sequential -- bit-identical results), plus the
+    other BASELINE.md §3 configs: c1 in full (setup + Ax + DSSUM + 20 CG
+    iterations), c2 Ax + DSSUM x 10, and with --cpu-c4 one Ax per N at ~16M DOF.
+    Bounded: ~10-30 s in total by default."""
+    import oracle
+    from paper_1403_0968_b200 import meshgen
+    pc = "CG" if args.precond == "none" else "Jacobi PCG"
+    cores = args.cpu_threads or host_cores()
+    oracle.set_threads(1)
+    t1, Lc = oracle_sample(args, args.cpu_its, 1)
+    oracle.set_threads(cores)
+    tn, _ = oracle_sample(args, args.cpu_its, 1)
+    one = Lc * args.cpu_its / t1[0] / 1e9
+    allc = Lc * args.cpu_its / tn[0] / 1e9
+    out = {"value": allc, "unit": "GDOF/s", "cores": cores, "kind": "oracle", "cpu": cpu_info(),
+           "affinity_cores": host_cores(), "omp_threads": cores,
+           "sample": f"plain-C oracle {pc}, {args.cpu_its} iterations (tol=0) on the same c3 mesh "
+                     f"({Lc} local DOF), operator element loop on {cores} OpenMP threads "
+                     f"(sequential dot products / DSSUM / recurrence), {tn[0]:.1f} s; the oracle's "
+                     "setup (maxit = 0 call) subtracted",
+           "one_core": {"value": one, "unit": "GDOF/s", "cores": 1, "seconds": t1[0]}}
+    cfg = {}
+    # c1: 8 hex (2x2x2), N = 4: setup + 1 Ax + DSSUM + 20 CG iterations
+    t0 = time.perf_counter()
+    xi, _ = oracle.gll(4)
+    m1 = meshgen.box_mesh(4, xi, elems=(2, 2, 2), eps=0.05)
+    G1, J1 = oracle.geom(4, m1.xyz)
+    u1 = meshgen.random_field(m1.nlocal, 0)
+    oracle.dssum(m1.glo, oracle.ax(4, G1, u1))
+    _, f1 = meshgen.manufactured(m1)
+    b1 = oracle.mass_rhs(4, m1.glo, m1.dirichlet, J1, f1)
+    oracle.cg(4, m1.glo, m1.dirichlet, G1, b1, tol=0.0, maxit=20)
+    cfg["c1_full_ms"] = 1e3 * (time.perf_counter() - t0)
+    # c2: 512 elements, N = 7: Ax + DSSUM, 10 repetitions (setup untimed)
+    xi7, _ = oracle.gll(7)
+    m2 = meshgen.box_mesh(7, xi7, elems=(8, 8, 8), eps=0.05)
+    G2, _ = oracle.geom(7, m2.xyz)
+    u2 = meshgen.random_field(m2.nlocal, 0)
+    t0 = time.perf_counter()
+    for _ in range(10):
+        oracle.dssum(m2.glo, oracle.ax(7, G2, u2))
+    dt = (time.perf_counter() - t0) / 10
+    cfg["c2_ax_dssum"] = {"ms": 1e3 * dt, "gdof_s": m2.nlocal / dt / 1e9, "cores": cores}
+    if args.cpu_c4:
+        sweep = {}
+        for N in range(3, 16):
+            xiN, _ = oracle.gll(N)
+            e = round(256 / (N + 1))
+            mN = meshgen.box_mesh(N, xiN, elems=(e, e, e), eps=0.05)
+            GN, _ = oracle.geom(N, mN.xyz)
+            uN = meshgen.random_field(mN.nlocal, 0)
+            t0 = time.perf_counter()
+            oracle.ax(N, GN, uN)
+            d = time.perf_counter() - t0
+            sweep[str(N)] = {"gdof_s": mN.nlocal / d / 1e9, "s": d}
+            del mN, GN, uN
+        cfg["c4_ax"] = {"cores": cores, "per_N": sweep}
+    oracle.set_threads(1)
+    out["configs"] = cfg
+    return out
 
 
 FD_METRIC = "FD wave step MNodes/s vs stencil size (lst:fdCode), % of HBM roofline"
@@ -571,11 +662,7 @@ def main():
     # ---- oracle on the host cores (rank 0, N=1 only), bounded sample ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        times, Lc = oracle_sample(args, args.cpu_its, 1)
-        cpu = {"value": Lc * args.cpu_its / times[0] / 1e9, "unit": "GDOF/s", "cores": 1,
-               "kind": "oracle", "cpu": cpu_info(),
-               "sample": f"plain-C oracle {'CG' if args.precond == 'none' else 'Jacobi PCG'}, {args.cpu_its} iterations (tol=0) on the same c3 "
-                         f"mesh ({Lc} local DOF), 1 thread, {times[0]:.1f} s; setup untimed"}
+        cpu = cpu_baseline(args)
 
     if rank == 0:
         ws = 16 * L + ctx.workspace.numel()

@@ -22,8 +22,10 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 # Plain build: -O2, no -ffast-math, no FMA contraction (FP64 rounding order is
 # exactly the order written in the C source).
+# -fopenmp: the element loop of the operator may use several host threads
+# (set_threads; CPU baseline timing only, results bit-identical).
 GCC_CMD = ["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", "-ffp-contract=off",
-           "-fno-fast-math", _SRC, _SRC_FD, "-o", _LIB, "-lm"]
+           "-fno-fast-math", "-fopenmp", _SRC, _SRC_FD, "-o", _LIB, "-lm"]
 
 _lib = None
 
@@ -60,7 +62,9 @@ def lib():
         L.ora_diag_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P]
         L.ora_pcg_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P, P, ctypes.c_int, P, P,
                                        ctypes.c_double, ctypes.c_int, P, P]
-        for f in (L.ora_gll, L.ora_deriv, L.ora_geom, L.ora_ax, L.ora_dssum,
+        L.ora_set_threads.argtypes = [ctypes.c_int]
+        L.ora_get_threads.argtypes = []
+        for f in (L.ora_set_threads, L.ora_get_threads, L.ora_gll, L.ora_deriv, L.ora_geom, L.ora_ax, L.ora_dssum,
                   L.ora_multiplicity, L.ora_cg, L.ora_ax_screened, L.ora_cg_screened,
                   L.ora_diag_screened, L.ora_pcg_screened, L.ora_fd_weights, L.ora_fd_step, L.ora_cg_cgs):
             f.restype = ctypes.c_int
@@ -92,6 +96,18 @@ class OracleError(RuntimeError):
 def _check(rc, what):
     if rc != 0:
         raise OracleError(f"{what} failed with status {rc}")
+
+
+def set_threads(n: int) -> None:
+    """Host threads of the operator's element loop (1 = the plain sequential
+    oracle).  Dot products, DSSUM and the CG recurrence stay sequential, so
+    every result is bit-identical for any n."""
+    if lib().ora_set_threads(int(n)) != 0:
+        raise OracleError(f"ora_set_threads({n})")
+
+
+def get_threads() -> int:
+    return int(lib().ora_get_threads())
 
 
 def gll(N: int):

@@ -197,6 +197,17 @@ int ora_geom(int N, int64_t E, const double *xyz, double *G, double *Jout)
  *   - the mass operator is the lumped diagonal J w_abc of :605-614, scaled by
  *     alpha(x) at the node:  w[ijk] += alpha_ijk w_i w_j w_k J_ijk u[ijk]
  * kappa == NULL means kappa = 1; alpha == NULL means alpha = 0 (J unused).  */
+/* Host threads of the element loop of ora_ax_screened (default 1).  Only
+ * the timing of the CPU baseline changes; results are bit-identical. */
+static int ora_threads = 1;
+int ora_set_threads(int nthreads)
+{
+    if (nthreads < 1) return ORA_EINVAL;
+    ora_threads = nthreads;
+    return ORA_OK;
+}
+int ora_get_threads(void) { return ora_threads; }
+
 int ora_ax_screened(int N, int64_t E, const double *G, const double *J, const double *kappa,
                     const double *alpha, const double *u, double *w)
 {
@@ -205,11 +216,18 @@ int ora_ax_screened(int N, int64_t E, const double *G, const double *J, const do
     int n = N + 1, n3 = n * n * n;
     double xi[33], wq[33];
     double *D = (double *)malloc(sizeof(double) * n * n);
+    ora_gll(N, xi, wq);
+    ora_deriv(N, xi, D);
+    /* Elements are independent (each w_e depends on u_e only), so the element
+     * loop may run on several host threads (ora_set_threads; the CPU baseline
+     * of bench.py): every w value is computed by the same operations in the
+     * same order whatever the thread count -- bit-identical results. */
+#pragma omp parallel num_threads(ora_threads)
+    {
     double *fr = (double *)malloc(sizeof(double) * n3);
     double *fs = (double *)malloc(sizeof(double) * n3);
     double *ft = (double *)malloc(sizeof(double) * n3);
-    ora_gll(N, xi, wq);
-    ora_deriv(N, xi, D);
+#pragma omp for schedule(static)
     for (int64_t e = 0; e < E; ++e) {
         const double *ue = u + e * n3;
         const double *Ge = G + e * 6 * n3;
@@ -249,10 +267,11 @@ int ora_ax_screened(int N, int64_t E, const double *G, const double *J, const do
                     we[q] = s;
                 }
     }
-    free(D);
     free(fr);
     free(fs);
     free(ft);
+    }
+    free(D);
     return ORA_OK;
 }
 
