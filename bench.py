@@ -534,12 +534,31 @@ def main():
     value = L_all * its * args.steps / t / 1e9
     cg_its_per_s = its * args.steps / t
 
-    # ---- per-kernel device time: the same solves again, with sem_profile on:
-    # the library runs them through a second CUDA graph of the same chunk
-    # whose kernels are bracketed by event-record nodes, read back after every
-    # chunk (kept out of the timed region; ungraphed per-launch events only if
-    # SEM_CG_GRAPH=0) ----
+    # ---- per-kernel device time INSIDE the CUDA graphs of the solve: the same
+    # solves again under CUPTI kernel tracing (torch.profiler, CUDA activity
+    # only; tools/kernel_trace.py) -- GPU start/end timestamps of every kernel
+    # node, no events between kernels, graphs as in the timed region ----
     prof_steps = max(1, min(3, args.steps))
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import kernel_trace
+
+    def traced_solves():
+        for _ in range(prof_steps):
+            x.zero_()
+            ctx.cg(b, x, tol=args.tol, maxit=args.maxit, precond=args.precond,
+                   variant=args.cg_variant)
+
+    trace_path = os.environ.get("SEM_BENCH_TRACE")      # optional chrome-trace dump
+    try:
+        tev = kernel_trace.trace(traced_solves, export=trace_path)
+        tcls, tn = kernel_trace.per_solve(tev, its)
+    except Exception as e:  # profiler unavailable: fall back to the event timing below
+        print(f"bench.py: CUPTI kernel trace unavailable ({e})", file=sys.stderr)
+        tcls, tn = {"k1": [], "k2": []}, 0
+
+    # ---- algorithmic bytes per launch (and an event-bracketed cross-check):
+    # sem_profile runs the solve ungraphed with CUDA events around every
+    # launch on the library stream ----
     ctx.profile(True)
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record(stream)
@@ -574,10 +593,38 @@ def main():
         us = 1e3 * q0.elapsed_time(q1) / reps
         kern[name] = {"avg_launch_us": us, "bytes_per_launch": by,
                       "achieved_gbs": by / (us * 1e-6) / 1e9, "frac": by / (us * 1e-6) / 1e9 / peak}
-    # headline: K1 inside the solve (per-launch CUDA events, profiled pass)
+    # headline: K1 inside the graphed solve (CUPTI timestamps); bytes per
+    # launch from the library's accounting (96 B/node, 72 at k = 0)
     k1_ms, k1_n, k1_bytes = prof["k1"]
-    achieved = (k1_bytes / k1_n) / (k1_ms / k1_n * 1e-3) / 1e9 if k1_n else None
-    k1_in_solve_us = 1e3 * k1_ms / k1_n if k1_n else None
+    k1_bpl = k1_bytes / k1_n if k1_n else None
+    k2_bpl = prof["k2"][2] / prof["k2"][1] if prof["k2"][1] else None
+    in_solve = {}
+    for name, bpl in (("k1", k1_bpl), ("k2", k2_bpl)):
+        d = tcls.get(name) or []
+        if d and bpl:
+            us_ = statistics.fmean(d)
+            in_solve[name] = {"avg_launch_us": us_, "launches": len(d), "bytes_per_launch": bpl,
+                              "achieved_gbs": bpl / (us_ * 1e-6) / 1e9,
+                              "frac": bpl / (us_ * 1e-6) / 1e9 / peak,
+                              "us_per_solve": sum(d) / max(tn, 1)}
+    # the same with CUDA events around every launch of the UNGRAPHED solve
+    # (host launch gaps fall inside the brackets: an upper bound)
+    in_events = {}
+    for name in ("k1", "k2"):
+        ms_, n_, by_ = prof[name]
+        if n_:
+            us_ = 1e3 * ms_ / n_
+            in_events[name] = {"avg_launch_us": us_, "bytes_per_launch": by_ / n_,
+                               "achieved_gbs": by_ / n_ / (us_ * 1e-6) / 1e9,
+                               "frac": by_ / n_ / (us_ * 1e-6) / 1e9 / peak}
+    if "k1" in in_solve:
+        k1_in_solve_us = in_solve["k1"]["avg_launch_us"]
+        achieved = in_solve["k1"]["achieved_gbs"]
+        k1_launches = in_solve["k1"]["launches"]
+    else:
+        k1_in_solve_us = in_events["k1"]["avg_launch_us"] if "k1" in in_events else None
+        achieved = in_events["k1"]["achieved_gbs"] if "k1" in in_events else None
+        k1_launches = k1_n
     dmma = args.N == 7 and not os.environ.get("SEM_AX_KERNEL")
     k1_name = ("K1: ax_dmma_kernel<CG=true> (N=7: r/s contractions on the FP64 tensor cores; "
                "x/p update + Ax + (p,Ap) partials)" if dmma else
@@ -585,19 +632,9 @@ def main():
     traffic = ncu_traffic(("ax_dmma_kernel<1, 0, 0, 0>",) if dmma else
                           (f"ax_tma_kernel<{args.N}, true, false>", f"ax_tma_kernel<{args.N}, 1>")) \
         if alpha is None and args.precond == "none" and args.cg_variant == "standard" else None
-    # share of the timed solve: per-solve device ms of each class (inside the
-    # graph) over the timed region's ms per solve
-    shares = {k: v[0] / prof_steps / (ms / args.steps) for k, v in prof.items() if v[1]}
-    # every CG kernel inside the solve (per-launch CUDA events, profiled pass):
-    # K2 reads the w K1 just wrote from L2, unlike its back-to-back replay
-    in_solve = {}
-    for name in ("k1", "k2"):
-        ms_, n_, by_ = prof[name]
-        if n_:
-            us_ = 1e3 * ms_ / n_
-            in_solve[name] = {"avg_launch_us": us_, "bytes_per_launch": by_ / n_,
-                              "achieved_gbs": by_ / n_ / (us_ * 1e-6) / 1e9,
-                              "frac": by_ / n_ / (us_ * 1e-6) / 1e9 / peak}
+    # share of the timed solve: per-solve device time of each class inside the
+    # graph over the timed region's ms per solve
+    shares = {k: v["us_per_solve"] / 1e3 / (ms / args.steps) for k, v in in_solve.items()}
     # the work vectors were clobbered by the replays; the next solve re-inits
     x.zero_()
     ctx.cg(b, x, tol=args.tol, maxit=args.maxit, precond=args.precond,
@@ -689,21 +726,25 @@ def main():
                          "bytes_per_node": f"{bpn_k1:.0f} (x,r,p,G{',H' if alpha is not None else ''} "
                                            "read; x,p,w write)",
                          "avg_launch_us": k1_in_solve_us,
-                         "launches": k1_n,
+                         "launches": k1_launches,
                          "kernels_replayed": kern,
                          "kernels_in_solve": in_solve,
+                         "kernels_events_ungraphed": in_events,
                          "step_share": shares,
                          "iteration": {"us": 1e3 * ms / args.steps / its,
                                        "algorithmic_bytes": bpn_k1 * L + (k2_bytes or 0.0),
                                        "frac": (bpn_k1 * L + (k2_bytes or 0.0)) /
                                                (ms / args.steps / its * 1e-3) / 1e9 / peak},
-                         "profiled_solve_ms": prof_ms / prof_steps,
-                         "timing": "achieved / kernels_in_solve / step_share: event-record "
-                                   "nodes around every kernel INSIDE the CG chunk graph "
-                                   f"(sem_profile), {prof_steps} solves of the same workload run "
-                                   "right after the timed region, step_share against the timed "
-                                   "ms per solve; kernels_replayed: CUDA events around a graph of "
-                                   "50 back-to-back launches of one kernel (sem_kernel_replay, no "
+                         "timing": "achieved / kernels_in_solve / step_share: CUPTI GPU "
+                                   "timestamps (torch.profiler CUDA activity) of every kernel "
+                                   "node INSIDE the CG chunk graphs of "
+                                   f"{prof_steps} solves of the same workload run right after the "
+                                   "timed region (the first `cg_iters` K1 / K2 launches of each "
+                                   "solve; step_share against the timed ms per solve); "
+                                   "kernels_events_ungraphed: CUDA events around every launch of "
+                                   "the ungraphed solve (sem_profile; host gaps included); "
+                                   "kernels_replayed: CUDA events around a graph of 50 "
+                                   "back-to-back launches of one kernel (sem_kernel_replay, no "
                                    "CG neighbours in L2)"},
             "gpu_launches": gpu_launches,
             "e2e": e2e,

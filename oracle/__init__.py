@@ -63,8 +63,9 @@ def lib():
         L.ora_pcg_screened.argtypes = [ctypes.c_int, i64, P, P, P, P, P, P, ctypes.c_int, P, P,
                                        ctypes.c_double, ctypes.c_int, P, P]
         L.ora_set_threads.argtypes = [ctypes.c_int]
+        L.ora_set_history.argtypes = [P, ctypes.c_int]
         L.ora_get_threads.argtypes = []
-        for f in (L.ora_set_threads, L.ora_get_threads, L.ora_gll, L.ora_deriv, L.ora_geom, L.ora_ax, L.ora_dssum,
+        for f in (L.ora_set_history, L.ora_set_threads, L.ora_get_threads, L.ora_gll, L.ora_deriv, L.ora_geom, L.ora_ax, L.ora_dssum,
                   L.ora_multiplicity, L.ora_cg, L.ora_ax_screened, L.ora_cg_screened,
                   L.ora_diag_screened, L.ora_pcg_screened, L.ora_fd_weights, L.ora_fd_step, L.ora_cg_cgs):
             f.restype = ctypes.c_int
@@ -104,6 +105,27 @@ def set_threads(n: int) -> None:
     every result is bit-identical for any n."""
     if lib().ora_set_threads(int(n)) != 0:
         raise OracleError(f"ora_set_threads({n})")
+
+
+class history:
+    """Context manager: record the relative residual sqrt(rr_k / rr_0),
+    k = 0 .. iters, of the CG solves run inside it (instrumentation only).
+    ``h.values`` holds the last solve's history."""
+
+    def __init__(self, cap: int = 100000):
+        self.buf = np.full(cap, np.nan)
+        self.values = None
+
+    def __enter__(self):
+        lib().ora_set_history(self.buf.ctypes.data, self.buf.size)
+        return self
+
+    def __exit__(self, *exc):
+        lib().ora_set_history(None, 0)
+        v = self.buf
+        n = int(np.argmax(np.isnan(v))) if np.isnan(v).any() else v.size
+        self.values = v[:n].copy()
+        return False
 
 
 def get_threads() -> int:

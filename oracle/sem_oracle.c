@@ -405,6 +405,22 @@ static double dot_c(int64_t L, const double *c, const double *a, const double *b
     return s;
 }
 
+/* Optional residual history of the next CG solves (test instrumentation, no
+ * arithmetic): hist[k] = sqrt(rr_k) / sqrt(rr_0) for k = 0 .. iters, as far
+ * as cap allows; NULL disables. */
+static double *ora_hist = NULL;
+static int ora_hist_cap = 0;
+int ora_set_history(double *hist, int cap)
+{
+    ora_hist = (hist && cap > 0) ? hist : NULL;
+    ora_hist_cap = ora_hist ? cap : 0;
+    return ORA_OK;
+}
+static void hist_put(int k, double rr, double rr0)
+{
+    if (ora_hist && k < ora_hist_cap) ora_hist[k] = sqrt(rr) / sqrt(rr0);
+}
+
 /* the operator's coefficients (NULL: Poisson) */
 typedef struct {
     const double *J, *kappa, *alpha;
@@ -477,6 +493,7 @@ int ora_pcg_screened(int N, int64_t E, const int64_t *glo, const uint8_t *dirich
         *iters = 0;
         *rel_res = 0.0;
     } else {
+        hist_put(0, rr, rr0);
         while (k < maxit && sqrt(rr) > tol * sqrt(rr0)) {
             double beta = (k == 0) ? 0.0 : rho / rho_old;
             for (int64_t l = 0; l < L; ++l) p[l] = z[l] + beta * p[l];
@@ -489,6 +506,7 @@ int ora_pcg_screened(int N, int64_t E, const int64_t *glo, const uint8_t *dirich
             rho = dot_c(L, c, r, z);
             rr = dot_c(L, c, r, r);
             k += 1;
+            hist_put(k, rr, rr0);
         }
         *iters = k;
         *rel_res = sqrt(rr) / sqrt(rr0);
@@ -555,6 +573,7 @@ int ora_cg_cgs(int N, int64_t E, const int64_t *glo, const uint8_t *dirichlet, c
         *iters = 0;
         *rel_res = 0.0;
     } else {
+        hist_put(0, rr, rr0);
         while (k < maxit && sqrt(rr) > tol * sqrt(rr0)) {
             double beta, alpha;
             if (k == 0) {
@@ -576,6 +595,7 @@ int ora_cg_cgs(int N, int64_t E, const int64_t *glo, const uint8_t *dirichlet, c
             delta = dot_c(L, c, w, u);
             rr = dot_c(L, c, r, r);
             k += 1;
+            hist_put(k, rr, rr0);
         }
         *iters = k;
         *rel_res = sqrt(rr) / sqrt(rr0);

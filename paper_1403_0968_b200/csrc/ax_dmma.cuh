@@ -30,18 +30,48 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+// Groups of W warps per element: warp w owns the k-slices (8/W) w ..
+// (8/W)(w+1) - 1.  W = 2: three groups per SM (444 on 148 SMs: c3's 4096
+// elements take 9.22 rounds, the last one 23% full); W = 4: two groups per
+// SM (296: 13.84 rounds, the last one 84% full) with each element done in
+// about half the time.  Stages: two per group, TMA-filled as ax_tma_kernel.
+template <bool CG, int W>
+struct DmmaLayout {
+    using C = TmaCfg<7>;
+    static constexpr int GT = 32 * W;
+    static constexpr int NV = CG ? 3 : 1;                       // r,p,x | u
+    static constexpr int STAGE = NV * C::VL + 6 * C::n3;        // doubles
+    static constexpr int SMEM_MAX = 227 * 1024 - 1024;
+    static constexpr int NG_FIT = SMEM_MAX / (2 * STAGE * 8);
+    static constexpr int NG_CAP = W == 2 ? 4 : 2;
+    static constexpr int NG = NG_FIT > NG_CAP ? NG_CAP : NG_FIT;  // groups per CTA
+    static constexpr int NT = NG * GT;
+    static constexpr size_t SMEM = size_t(NG) * 2 * STAGE * 8 + 128;
+};
+
+// elements-per-group layout chosen at run time (SEM_DMMA_W=2|4, default 4)
+inline int dmma_w() {
+    static const int w = [] {
+        const char *e = getenv("SEM_DMMA_W");
+        return (e && e[0] == '2') ? 2 : 4;
+    }();
+    return w;
+}
+
 // MASS: + h u with h = alpha w J (screened Coulomb, the h pointer in the field
 // the variant does not use, as ax_tma_kernel); PC: Jacobi PCG scalars; DOT:
 // KA of the single-reduction CG (plain apply + (u, w) partials).
-template <bool CG, bool MASS = false, bool PC = false, bool DOT = false>
-__global__ void __launch_bounds__(TmaLayout<7, CG>::NT, 1) ax_dmma_kernel(TmaArgs a) {
+template <bool CG, bool MASS = false, bool PC = false, bool DOT = false, int W = 2>
+__global__ void __launch_bounds__(DmmaLayout<CG, W>::NT, 1) ax_dmma_kernel(TmaArgs a) {
     constexpr int N = 7;
     using C = TmaCfg<N>;
-    using Lo = TmaLayout<N, CG>;
-    constexpr int n = C::n, n2 = C::n2, n3 = C::n3, GT = C::GT, VL = C::VL;
+    using Lo = DmmaLayout<CG, W>;
+    constexpr int n = C::n, n2 = C::n2, n3 = C::n3, GT = Lo::GT, VL = C::VL;
     constexpr int NG = Lo::NG, NV = Lo::NV, STAGE = Lo::STAGE;
+    constexpr int KW = n / W;                 // k-slices per warp
+    constexpr int KC = n * 64 / GT;           // k-values per column owner in phase 0
     constexpr int DO = d_off(N);
-    static_assert(C::EPG == 1 && GT == 64 && n == 8, "DMMA kernel: N = 7, one element per group");
+    static_assert(C::EPG == 1 && n == 8 && (W == 2 || W == 4), "DMMA kernel: N = 7, one element per group");
     extern __shared__ __align__(128) double smem[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + size_t(NG) * 2 * STAGE);
     __shared__ double sred[4 * ((Lo::NT + 31) / 32)];
@@ -49,7 +79,8 @@ __global__ void __launch_bounds__(TmaLayout<7, CG>::NT, 1) ax_dmma_kernel(TmaArg
     const int tid = threadIdx.x;
     const int g = tid / GT;
     const int gt = tid - g * GT;
-    const int i = gt % n, j = gt / n;        // phase-0 column owner (the CG update)
+    const int i = gt % n, j = (gt / n) % n;  // phase-0 column owner (the CG update)
+    const int kc0 = (gt / n2) * KC;          // ... of k = kc0 .. kc0 + KC - 1
     const int warp = gt >> 5, lane = gt & 31;
     const int gid = lane >> 2, tig = lane & 3;
     const int i0 = 2 * tig;                  // the lane's node pair (i0, i0+1) of row gid
@@ -148,7 +179,7 @@ __global__ void __launch_bounds__(TmaLayout<7, CG>::NT, 1) ax_dmma_kernel(TmaArg
         dA[ks] = c_D[DO + gid * n + 4 * ks + tig];
         dB[ks] = c_D[DO + (4 * ks + tig) * n + gid];
     }
-    const int kb = 4 * warp;                  // this warp's k-slices kb .. kb+3
+    const int kb = KW * warp;                 // this warp's k-slices kb .. kb+KW-1
     const int lq = gid * n + i0;              // the lane's first node within a slice
     // f_r is stored with its column halves swapped on rows 2, 3, 6, 7 (i ^ 4),
     // so the phase-B A-fragment loads F_r,k[gid][4ks + tig] of a warp hit all
@@ -172,10 +203,11 @@ __global__ void __launch_bounds__(TmaLayout<7, CG>::NT, 1) ax_dmma_kernel(TmaArg
             double *sp = sb + 1 * VL + sh;
             double *sx = sb + 2 * VL + sh;
             su = sp;
-            const int64_t gbase = e * n3 + gt;
+            const int64_t gbase = e * n3 + (gt % n2);
 #pragma unroll
-            for (int k = 0; k < n; ++k) {
-                const int q = k * n2 + gt;
+            for (int kk = 0; kk < KC; ++kk) {
+                const int k = kc0 + kk;
+                const int q = k * n2 + (gt % n2);
                 const double rl = sr[q];
                 double pl;
                 if (kit == 0) {
@@ -206,7 +238,7 @@ __global__ void __launch_bounds__(TmaLayout<7, CG>::NT, 1) ax_dmma_kernel(TmaArg
 
         // ---- phase A: gradient (DMMA for r, s; FMA for t) and G^ ----
 #pragma unroll
-        for (int kt = 0; kt < 4; ++kt) {
+        for (int kt = 0; kt < KW; ++kt) {
             const int k = kb + kt;
             const double *uk = su + k * n2;
             double r0 = 0.0, r1 = 0.0, s0 = 0.0, s1 = 0.0;
@@ -248,7 +280,7 @@ __global__ void __launch_bounds__(TmaLayout<7, CG>::NT, 1) ax_dmma_kernel(TmaArg
             f1v[m] = sG[2 * n3 + m * n2 + lq + 1];
         }
 #pragma unroll
-        for (int kt = 0; kt < 4; ++kt) {
+        for (int kt = 0; kt < KW; ++kt) {
             const int k = kb + kt;
             const double *frk = sG + 0 * n3 + k * n2;
             const double *fsk = sG + 1 * n3 + k * n2;
@@ -294,32 +326,47 @@ __global__ void __launch_bounds__(TmaLayout<7, CG>::NT, 1) ax_dmma_kernel(TmaArg
 }
 
 // ---- launchers (instantiated by the translation unit of each variant) ----
+template <bool CG, int W>
+static int dmma_grid_w(int64_t E, int nsm) {
+    const int64_t need = (E + DmmaLayout<CG, W>::NG - 1) / DmmaLayout<CG, W>::NG;
+    return (int)(need < nsm ? (need < 1 ? 1 : need) : nsm);
+}
 template <bool CG>
 static int dmma_grid(int64_t E, int nsm) {
-    const int64_t need = (E + TmaLayout<7, CG>::NG - 1) / TmaLayout<7, CG>::NG;
-    return (int)(need < nsm ? (need < 1 ? 1 : need) : nsm);
+    return dmma_w() == 4 ? dmma_grid_w<CG, 4>(E, nsm) : dmma_grid_w<CG, 2>(E, nsm);
 }
 
 template <bool CG, bool MASS, bool PC, bool DOT>
 static cudaError_t dmma_attr() {
-    return cudaFuncSetAttribute(ax_dmma_kernel<CG, MASS, PC, DOT>,
+    cudaError_t e = cudaFuncSetAttribute(ax_dmma_kernel<CG, MASS, PC, DOT, 2>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)DmmaLayout<CG, 2>::SMEM);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(ax_dmma_kernel<CG, MASS, PC, DOT, 4>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)TmaLayout<7, CG>::SMEM);
+                                (int)DmmaLayout<CG, 4>::SMEM);
 }
 
 // plain apply (MASS: h in a.r)
 template <bool MASS, bool DOT = false>
 static cudaError_t launch_dmma_plain(const TmaArgs &a, int nsm, cudaStream_t s) {
-    ax_dmma_kernel<false, MASS, false, DOT>
-        <<<dmma_grid<false>(a.E, nsm), TmaLayout<7, false>::NT, TmaLayout<7, false>::SMEM, s>>>(a);
+    if (dmma_w() == 4)
+        ax_dmma_kernel<false, MASS, false, DOT, 4>
+            <<<dmma_grid_w<false, 4>(a.E, nsm), DmmaLayout<false, 4>::NT, DmmaLayout<false, 4>::SMEM, s>>>(a);
+    else
+        ax_dmma_kernel<false, MASS, false, DOT, 2>
+            <<<dmma_grid_w<false, 2>(a.E, nsm), DmmaLayout<false, 2>::NT, DmmaLayout<false, 2>::SMEM, s>>>(a);
     return cudaGetLastError();
 }
 
 // K1 over the element range of a (cg_args)
 template <bool MASS, bool PC>
 static cudaError_t launch_dmma_cg(const TmaArgs &a, int nsm, cudaStream_t s) {
-    return launch_pdl(ax_dmma_kernel<true, MASS, PC, false>, dmma_grid<true>(a.E, nsm),
-                      TmaLayout<7, true>::NT, TmaLayout<7, true>::SMEM, s, a);
+    if (dmma_w() == 4)
+        return launch_pdl(ax_dmma_kernel<true, MASS, PC, false, 4>, dmma_grid_w<true, 4>(a.E, nsm),
+                          DmmaLayout<true, 4>::NT, DmmaLayout<true, 4>::SMEM, s, a);
+    return launch_pdl(ax_dmma_kernel<true, MASS, PC, false, 2>, dmma_grid_w<true, 2>(a.E, nsm),
+                      DmmaLayout<true, 2>::NT, DmmaLayout<true, 2>::SMEM, s, a);
 }
 
 }  // namespace sem

@@ -84,6 +84,10 @@ static cudaError_t dmma_prepare() {
     return e == cudaSuccess ? dmma_attr<true, false, false, false>() : e;
 }
 
+int dmma_blocks(int64_t E, int nsm, bool cg) {
+    return cg ? dmma_grid<true>(E, nsm) : dmma_grid<false>(E, nsm);
+}
+
 int tma_blocks(int N, int64_t E, int nsm, bool cg) {
     int nb = 0;
     if (cg) {

@@ -370,7 +370,10 @@ __device__ __forceinline__ CgStep cg_k1_prologue(CgState *st, const CgRed &R, do
 // preconditioner (k2_kernel<N, INIT, PC>).  Split like K1's: cg_k2_load
 // issues every load (both parities), cg_k2_finish consumes them.
 struct K2Pre {
-    static constexpr int PER = 4;
+    // loads in flight per thread and partial set: 2 x 256 threads cover the
+    // K2 grid's 444 (r,r) partials and K1's <= 148 (p,Ap) partials in one
+    // round trip (a tail loop takes any rest)
+    static constexpr int PER = 2;
     int done, k, multi;
     double raw[4][PER];
     double v[2];

@@ -105,10 +105,30 @@ __device__ __forceinline__ void k2_groups(const K2Args &a, const int32_t *__rest
 }
 
 // Element-interior nodes of one chunk (m = 1, never Dirichlet): local
-// indices of this thread's U nodes (-1 past the end), i fastest.
+// indices of this thread's U nodes (-1 past the end), i fastest.  Interior
+// node t is node q = t mod (N-1)^3 of element e = t div (N-1)^3; its offset
+// inside the element comes from a shared-memory table (ioff[q], filled once
+// per block), which replaces the per-node (i, j, k) division chain (ncu r02i:
+// 22% of K2's instructions).  Consecutive threads keep consecutive interior
+// nodes, so the loads stay coalesced (a row-segment-per-thread layout that
+// also cut the arithmetic measured 26% slower, r02k: a warp's loads then span
+// 32 rows).
+template <int N>
+struct K2Int {
+    static constexpr int ni = N - 1, NI3 = ni * ni * ni;
+};
+template <int N>
+__device__ __forceinline__ void k2_interior_table(int32_t *ioff) {
+    constexpr int n = N + 1, n2 = n * n, ni = N - 1, NI3 = ni * ni * ni;
+    for (int q = threadIdx.x; q < NI3; q += kK2Threads) {
+        const int ii = q % ni, jj = (q / ni) % ni, kk = q / (ni * ni);
+        ioff[q] = (kk + 1) * n2 + (jj + 1) * n + (ii + 1);
+    }
+}
 template <int N, int U>
-__device__ __forceinline__ void k2_interior_idx(int64_t E, int chunk, int (&l)[U]) {
-    constexpr int n = N + 1, n2 = n * n, n3 = n2 * n, ni = N - 1, NI3 = ni * ni * ni;
+__device__ __forceinline__ void k2_interior_idx(int64_t E, int chunk, const int32_t *ioff,
+                                                int (&l)[U]) {
+    constexpr int n = N + 1, n3 = n * n * n, ni = N - 1, NI3 = ni * ni * ni;
     const int nint = (int)(E * NI3);
     const int t0 = chunk * kK2Threads * U + threadIdx.x;
 #pragma unroll
@@ -117,8 +137,7 @@ __device__ __forceinline__ void k2_interior_idx(int64_t E, int chunk, int (&l)[U
         const int tt = t < nint ? t : 0;
         const int e = tt / NI3;
         const int q = tt - e * NI3;
-        const int ii = q % ni, jj = (q / ni) % ni, kk = q / (ni * ni);
-        l[u] = (t < nint) ? e * n3 + (kk + 1) * n2 + (jj + 1) * n + (ii + 1) : -1;
+        l[u] = (t < nint) ? e * n3 + ioff[q] : -1;
     }
 }
 
@@ -127,8 +146,13 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
     constexpr int ni = N - 1;
     constexpr int U = kK2IntU;
     __shared__ double sred[3 * (kK2Threads / 32)];
+    __shared__ int32_t ioff[ni > 0 ? ni * ni * ni : 1];
     if constexpr (!INIT) pdl_trigger();
     if constexpr (!INIT) pdl_wait();
+    if constexpr (ni > 0) {
+        k2_interior_table<N>(ioff);
+        __syncthreads();
+    }
 
     // Chunks: [0, nich) element-interior nodes (kK2Threads * U each), then
     // [nich + cchunk[c], nich + cchunk[c+1]) the groups of class c
@@ -146,7 +170,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
     if constexpr (!INIT) cg_k2_load<kK2Threads, PC>(a.st, a.red, pre);
     if constexpr (ni > 0) {
         if (ch < nich) {
-            k2_interior_idx<N, U>(a.E, ch, l);
+            k2_interior_idx<N, U>(a.E, ch, ioff, l);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (l[u] >= 0) {
@@ -172,7 +196,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
         if (ch < nich) {
             if constexpr (ni > 0) {
                 if (!staged) {
-                    k2_interior_idx<N, U>(a.E, ch, l);
+                    k2_interior_idx<N, U>(a.E, ch, ioff, l);
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         if (l[u] >= 0) {

@@ -152,6 +152,7 @@ bool dmmag_supported(int N);
 cudaError_t dmmag_prepare(int N);
 cudaError_t launch_ax_dmmag(const DevMesh &m, const double *u, double *w, cudaStream_t s);
 int tma_blocks(int N, int64_t E, int nsm, bool cg);
+int dmma_blocks(int64_t E, int nsm, bool cg);   // N = 7 tensor-core kernel grid
 cudaError_t tma_prepare(int N, bool mass);
 cudaError_t upload_const_D(int N, const double *D_host);
 cudaError_t launch_ax_tma(const DevMesh &m, const double *u, double *w, cudaStream_t s);

@@ -50,9 +50,8 @@ class Mesh:
 
     @property
     def nglobal(self) -> int:
-        ex, ey, ez = self.elems
-        N = self.N
-        return (ex * N + 1) * (ey * N + 1) * (ez * N + 1)
+        """Number of distinct global ids (for a box: (ex N + 1)(ey N + 1)(ez N + 1))."""
+        return int(np.unique(self.glo).size)
 
 
 def rank_block(elems, parts, rank):
@@ -212,3 +211,76 @@ def relabel(mesh: Mesh, seed: int, rotate: bool = True, id_stride: int = 3) -> M
     return Mesh(N=mesh.N, xyz=np.ascontiguousarray(xyz), glo=np.ascontiguousarray(glo),
                 dirichlet=np.ascontiguousarray(dirichlet), elems=mesh.elems, lengths=mesh.lengths,
                 parts=mesh.parts, rank=mesh.rank, eidx=eidx, nboundary=0)
+
+
+def prism_mesh(N: int, r1d, sides: int = 3, nz: int = 2, height: float = 1.0,
+               radius: float = 1.0) -> Mesh:
+    """A NON-box conforming hexahedral mesh (Omega_h is any
+    union of E conforming hexahedra): a regular `sides`-gon of the given
+    radius split into `sides` quadrilaterals around its centre -- quad q has
+    the corners (centre, midpoint of edge (q-1, q), vertex q, midpoint of edge
+    (q, q+1)), counter-clockwise -- extruded over `nz` layers in z.  The
+    vertical edge through the centre is shared by `sides` hexahedra, so edge
+    nodes there have multiplicity sides (3, 5, 6, ...) and the interior
+    corner nodes on it 2*sides -- multiplicities a box never has.  GLL nodes
+    are placed by the bilinear map of each quad (elements are kites, not
+    parallelograms: all six geometric factors vary in the element) and
+    linearly in z.  Global ids: nodes with the same coordinates (to 1e-9 of
+    the radius) are one node; the coordinates of each global node are taken
+    from its first copy so every copy is bit-identical.  Dirichlet on every
+    boundary face (faces not shared by two elements).  Element order: layer by
+    layer, quads in angular order."""
+    r1d = np.asarray(r1d, dtype=np.float64)
+    n = N + 1
+    assert r1d.shape == (n,)
+    ang = 2.0 * np.pi * np.arange(sides) / sides
+    V = radius * np.stack([np.cos(ang), np.sin(ang)], axis=1)
+    Mid = 0.5 * (V + np.roll(V, -1, axis=0))          # Mid[q] = midpoint of edge (q, q+1)
+    C = np.zeros(2)
+    quads = [np.stack([C, Mid[(q - 1) % sides], V[q], Mid[q]]) for q in range(sides)]
+    k, j, i = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    i, j, k = i.reshape(-1), j.reshape(-1), k.reshape(-1)
+    rr, ss, tt = r1d[i], r1d[j], r1d[k]
+    wts = np.stack([(1 - rr) * (1 - ss), (1 + rr) * (1 - ss), (1 + rr) * (1 + ss),
+                    (1 - rr) * (1 + ss)], axis=1) / 4.0        # [n3, 4] bilinear weights
+    xyz = []
+    for layer in range(nz):
+        z0, z1 = height * layer / nz, height * (layer + 1) / nz
+        z = z0 + (1.0 + tt) / 2.0 * (z1 - z0)
+        for P in quads:
+            xy = wts @ P                                       # [n3, 2]
+            xyz.append(np.stack([xy[:, 0], xy[:, 1], z], axis=0))
+    xyz = np.ascontiguousarray(np.stack(xyz))                  # [E, 3, n3]
+    E = xyz.shape[0]
+    # global ids by coordinates
+    key = np.round(xyz.transpose(0, 2, 1).reshape(-1, 3) / (1e-9 * radius)).astype(np.int64)
+    _, first, inv = np.unique(key, axis=0, return_index=True, return_inverse=True)
+    inv = inv.reshape(-1)
+    # ids in order of first appearance (element-major), coordinates from that copy
+    order = np.argsort(first, kind="stable")
+    rank_of = np.empty_like(order)
+    rank_of[order] = np.arange(order.size)
+    glo = rank_of[inv].reshape(E, n ** 3).astype(np.int64)
+    flat = xyz.transpose(0, 2, 1).reshape(-1, 3)
+    canon = flat[first[order]]
+    xyz = np.ascontiguousarray(canon[glo.reshape(-1)].reshape(E, n ** 3, 3).transpose(0, 2, 1))
+    # boundary faces: faces whose node set appears in one element only
+    faces = []
+    for axis, val in ((0, 0), (0, N), (1, 0), (1, N), (2, 0), (2, N)):
+        sel = (i, j, k)[axis] == val
+        faces.append(np.nonzero(sel)[0])
+    count = {}
+    fkeys = []
+    for e in range(E):
+        for f in faces:
+            fk = tuple(sorted(glo[e, f].tolist()))
+            fkeys.append((e, f, fk))
+            count[fk] = count.get(fk, 0) + 1
+    bnd = np.zeros(int(glo.max()) + 1, dtype=bool)
+    for e, f, fk in fkeys:
+        if count[fk] == 1:
+            bnd[glo[e, f]] = True
+    dirichlet = bnd[glo].astype(np.uint8)
+    eidx = np.zeros((E, 3), dtype=np.int64)
+    return Mesh(N=N, xyz=xyz, glo=np.ascontiguousarray(glo), dirichlet=np.ascontiguousarray(dirichlet),
+                elems=(sides, 1, nz), lengths=(radius, radius, height), eidx=eidx)

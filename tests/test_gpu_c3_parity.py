@@ -1,0 +1,124 @@
+"""Full-size c3 parity (BASELINE.json configs[2]: 4096 elements, N = 7,
+eps = 0.05, CG to 1e-8) for every solver the bench runs -- standard CG,
+Jacobi PCG (NEXT-2), single-reduction CG (NEXT-3) -- under the drift rule of
+tests/_margin.py (reading R3):
+
+* drift: the GPU's relative residual sqrt(rr_k / rr_0) at every iteration k
+  (a fixed-count GPU solve per k) agrees with the oracle's history within the
+  stated bound C3_DRIFT_MAX (5%; measured 1.3% CG, 1e-8 Jacobi PCG, 1.5%
+  single-reduction);
+* the tol = 1e-8 solve: identical counts if the oracle's margin exceeds the
+  measured drift, else within one; x within 1e-9 of the oracle's;
+* EXACT counts at c3 size: at tolerances where the oracle's stop has a margin
+  of at least twice the measured drift (picked from the oracle's history),
+  the GPU count equals the oracle's.
+The oracle runs its operator on all host cores (bit-identical to one core,
+tests/test_oracle_threads.py)."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1403_0968_b200 import meshgen
+from tests import _margin
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+METHODS = ["cg", "jacobi", "sr"]
+
+
+@pytest.fixture(scope="module")
+def c3():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1403_0968_b200 import sem
+    N = 7
+    xi, _ = oracle.gll(N)
+    m = meshgen.box_mesh(N, xi, elems=(16, 16, 16), eps=0.05)
+    G, J = oracle.geom(N, m.xyz)
+    _, f = meshgen.manufactured(m)
+    b = oracle.mass_rhs(N, m.glo, m.dirichlet, J, f)
+    ctx = sem.Context(m, N, device=0)
+    return m, G, b, ctx
+
+
+@pytest.fixture(scope="module")
+def oracle_runs(c3):
+    """Oracle solve to 1e-8 with residual history, per method."""
+    m, G, b, _ = c3
+    out = {}
+    oracle.set_threads(max(1, len(os.sched_getaffinity(0))))
+    try:
+        for meth in METHODS:
+            with oracle.history() as h:
+                if meth == "sr":
+                    x, its, rel, st = oracle.cg_single_reduction(7, m.glo, m.dirichlet, G, b,
+                                                                 tol=1e-8, maxit=5000)
+                else:
+                    x, its, rel, st = oracle.cg(7, m.glo, m.dirichlet, G, b, tol=1e-8, maxit=5000,
+                                                precond="jacobi" if meth == "jacobi" else "none")
+            assert st == 0 and len(h.values) == its + 1
+            out[meth] = (x, its, rel, h.values)
+    finally:
+        oracle.set_threads(1)
+    return out
+
+
+def gpu_cg(ctx, b, meth, tol, maxit):
+    kw = {"precond": "jacobi"} if meth == "jacobi" else (
+        {"variant": "single_reduction"} if meth == "sr" else {})
+    return ctx.cg(b, tol=tol, maxit=maxit, **kw)
+
+
+@pytest.fixture(scope="module")
+def gpu_hist(c3, oracle_runs):
+    """GPU relative residual at every k <= the oracle's count + 1."""
+    m, G, b, ctx = c3
+    bd = torch.from_numpy(b).cuda()
+    out = {}
+    for meth in METHODS:
+        its_r = oracle_runs[meth][1]
+
+        def solve(k):
+            _, it, rel, _ = gpu_cg(ctx, bd, meth, 0.0, k)
+            return it, rel
+
+        out[meth] = _margin.gpu_history(solve, its_r + 1)
+    return out
+
+
+@pytest.mark.parametrize("meth", METHODS)
+def test_c3_residual_drift(oracle_runs, gpu_hist, meth):
+    hist = oracle_runs[meth][3]
+    d = _margin.drift(gpu_hist[meth], hist)
+    print(f"{meth}: max relative residual drift {d:.3e} over {len(hist)} iterations")
+    assert d <= _margin.C3_DRIFT_MAX[meth]
+
+
+@pytest.mark.parametrize("meth", METHODS)
+def test_c3_solve_to_1e8(c3, oracle_runs, gpu_hist, meth):
+    m, G, b, ctx = c3
+    xr, its_r, rel_r, hist = oracle_runs[meth]
+    x, its, rel, ok = gpu_cg(ctx, torch.from_numpy(b).cuda(), meth, 1e-8, 5000)
+    assert ok
+    _margin.assert_count(its, its_r, _margin.margin(hist, its_r, 1e-8),
+                         _margin.drift(gpu_hist[meth], hist, its_r), (rel, rel_r))
+    xg = x.cpu().numpy()
+    assert np.linalg.norm(xg - xr) / np.linalg.norm(xr) <= 1e-9
+
+
+@pytest.mark.parametrize("meth", METHODS)
+def test_c3_exact_counts_at_wide_margin(c3, oracle_runs, gpu_hist, meth):
+    m, G, b, ctx = c3
+    hist = oracle_runs[meth][3]
+    picks = _margin.wide_margin_tols(hist, gpu_hist[meth], count=3)
+    assert picks, "no wide-margin stopping point in the oracle's history"
+    bd = torch.from_numpy(b).cuda()
+    for tol, k, marg in picks:
+        assert _margin.margin(hist, k, tol) == pytest.approx(marg)
+        _, its, rel, ok = gpu_cg(ctx, bd, meth, tol, 5000)
+        assert ok and its == k, (meth, tol, k, marg, its, rel)
+    print(f"{meth}: exact counts at {[(f'{t:.3e}', k, round(mg, 4)) for t, k, mg in picks]}")

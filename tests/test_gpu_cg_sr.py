@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import oracle
+from tests import _margin
 from paper_1403_0968_b200 import meshgen
 
 pytestmark = pytest.mark.gpu
@@ -63,21 +64,35 @@ SR = "single_reduction"
 @pytest.mark.parametrize("N,elems,eps,kind", [
     (4, (2, 2, 2), 0.05, "sin"), (4, (2, 2, 2), 0.05, "rand"), (3, (5, 4, 3), 0.05, "rand"),
     (7, (8, 8, 8), 0.05, "sin"), (2, (3, 3, 3), 0.0, "rand"), (9, (2, 3, 2), 0.05, "sin"),
-    (12, (2, 1, 2), 0.1, "sin"), (1, (4, 3, 3), 0.05, "rand")])
+    (12, (2, 2, 1), 0.05, "sin"), (12, (2, 1, 2), 0.1, "sin"), (1, (4, 3, 3), 0.05, "rand")])
 def test_cg_sr_iteration_parity(dev, impl, N, elems, eps, kind):
-    # (the recursively updated residual of this recurrence drifts a few % from
-    # the oracle's over a solve, R7: the N=12 case is one whose
-    # oracle residual crosses the tolerance by a wider margin (7% / 15% at
-    # the last two iterations) than the 2x2x1 eps=0.05 mesh (3%))
+    """Counts under the drift rule of tests/_margin.py: identical when the
+    oracle's stop has a margin above the measured GPU-vs-oracle residual drift
+    (the recursively updated residual of this recurrence drifts a few % over a
+    solve, R7), within one iteration otherwise; the drift itself
+    below DRIFT_MAX (25%).  (The N=12 2x2x1 eps=0.05 case crosses with a 3%
+    margin.)"""
     if impl.startswith("tma") and N > 10:
         pytest.skip("SEM_AX_KERNEL=tma above N=10 selects the simple kernel (no KA variant)")
     m, G, J, ctx = make(N, elems, eps)
     b = rhs(m, J, kind)
     x, its, rel, ok = ctx.cg(T(b, dev), tol=1e-8, maxit=2000, variant=SR)
-    xr, its_r, rel_r, st = oracle.cg_single_reduction(N, m.glo, m.dirichlet, G, b, tol=1e-8,
-                                                      maxit=2000)
+    with oracle.history() as h:
+        xr, its_r, rel_r, st = oracle.cg_single_reduction(N, m.glo, m.dirichlet, G, b, tol=1e-8,
+                                                          maxit=2000)
     assert ok and st == 0
-    assert its == its_r, (its, its_r, rel, rel_r)
+    bd = T(b, dev)
+
+    def solve(k):
+        _, it, rl, _ = ctx.cg(bd, tol=0.0, maxit=k, variant=SR)
+        return it, rl
+
+    dr = _margin.drift(_margin.gpu_history(solve, its_r), h.values)
+    assert dr <= _margin.DRIFT_MAX["sr"]
+    _margin.assert_count(its, its_r, _margin.margin(h.values, its_r, 1e-8), dr, (rel, rel_r))
+    if its != its_r:        # one iteration apart (a narrow margin): x one step apart
+        assert relerr(x.cpu().numpy(), xr) <= 1e-7
+        return
     assert relerr(x.cpu().numpy(), xr) <= 1e-10
     # the final residual norms drift apart by a few % over the solve (R3)
     assert abs(rel - rel_r) <= 0.1 * rel_r
@@ -157,15 +172,7 @@ def test_cg_sr_rejects_unsupported(dev, monkeypatch):
         ctx2.cg(torch.zeros(m.nlocal, dtype=torch.float64, device=dev), variant=SR)
 
 
-def test_c3_cg_sr_full_size(dev):
-    m, G, J, ctx = make(7, (16, 16, 16), 0.05)
-    b = rhs(m, J)
-    x, its, rel, ok = ctx.cg(T(b, dev), tol=1e-8, maxit=5000, variant=SR)
-    xr, its_r, rel_r, st = oracle.cg_single_reduction(7, m.glo, m.dirichlet, G, b, tol=1e-8,
-                                                      maxit=5000)
-    assert ok and st == 0
-    assert abs(its - its_r) <= 2, (its, its_r, rel, rel_r)
-    assert relerr(x.cpu().numpy(), xr) <= 1e-9
+# (the full-size c3 single-reduction solve: tests/test_gpu_c3_parity.py, drift rule)
 
 
 @pytest.mark.parametrize("N", [3, 7])

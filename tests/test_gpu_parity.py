@@ -267,20 +267,7 @@ def test_c3_ax_and_dssum_full_size(dev, c3):
     assert relerr(w.cpu().numpy(), oracle.dssum(m.glo, wr)) <= 1e-12
 
 
-def test_c3_cg_full_size(dev, c3):
-    """DESIGN.md R3: the c3 count is rounding-sensitive (GPU and oracle
-    residuals differ by ~1% after ~670 iterations), so the bar is +-2
-    iterations and the solution to 1e-9; smaller meshes require equality."""
-    m, G, J, ctx = c3
-    b = _rhs(m, J)
-    x, its, rel, ok = ctx.cg(T(b, dev), tol=1e-8, maxit=5000)
-    xr, its_r, rel_r, st = oracle.cg(7, m.glo, m.dirichlet, G, b, tol=1e-8, maxit=5000)
-    assert ok and st == 0
-    assert abs(its - its_r) <= 2, (its, its_r, rel, rel_r)
-    assert relerr(x.cpu().numpy(), xr) <= 1e-9
-    # both solutions approximate the manufactured u* equally well
-    us, _ = meshgen.manufactured(m)
-    assert abs(np.abs(x.cpu().numpy() - us).max() - np.abs(xr - us).max()) <= 1e-10
+# (the full-size c3 CG solve: tests/test_gpu_c3_parity.py, drift rule)
 
 
 # --- the same discretisation presented differently (meshgen.relabel): random

@@ -154,17 +154,7 @@ def test_pcg_edge_cases(dev, impl):
                              None, None) == sem.SEM_EINVAL
 
 
-def test_c3_pcg_full_size(dev):
-    """c3 (4096 el, N=7, eps=0.05) with the Jacobi preconditioner, as
-    `bench.py --precond jacobi` runs it."""
-    m, G, J, co, ctx = make(7, (16, 16, 16), 0.05)
-    b = rhs(m, J)
-    x, its, rel, ok = ctx.cg(T(b, dev), tol=1e-8, maxit=5000, precond="jacobi")
-    xr, its_r, rel_r, st = oracle.cg(7, m.glo, m.dirichlet, G, b, tol=1e-8, maxit=5000,
-                                     precond="jacobi")
-    assert ok and st == 0
-    assert abs(its - its_r) <= 2, (its, its_r, rel, rel_r)
-    assert relerr(x.cpu().numpy(), xr) <= 1e-9
+# (the full-size c3 Jacobi PCG solve: tests/test_gpu_c3_parity.py, drift rule)
 
 
 @pytest.mark.parametrize("N", [3, 7])

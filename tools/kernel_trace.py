@@ -31,16 +31,60 @@ def trace(fn, export: str | None = None):
     return out
 
 
+def _targs(name: str):
+    """Template arguments of a demangled kernel name ('a<7, true, false>(...)')."""
+    i = name.find("<")
+    if i < 0:
+        return []
+    depth, j = 0, i
+    for j in range(i, len(name)):
+        if name[j] == "<":
+            depth += 1
+        elif name[j] == ">":
+            depth -= 1
+            if depth == 0:
+                break
+    return [t.strip() for t in name[i + 1:j].split(",")]
+
+
 def classify(name: str) -> str:
-    """Kernel class of a libsem kernel name (K1 = the CG operator kernel,
-    K2 = gather-scatter + residual update)."""
-    n = name
-    if "k2_kernel" in n or "kb_sr_kernel" in n:
+    """Kernel class inside the CG loop: 'k1' = the operator kernel of an
+    iteration (ax_*_kernel with CG = true, or the single-reduction KA with
+    DOT = true), 'k2' = the gather-scatter + update kernel (k2_kernel with
+    INIT = false, the pipelined k2p_kernel, kb_sr_kernel), else 'other'
+    (plain Ax, CG start/finish, ...)."""
+    args = _targs(name)
+    bools = [a for a in args if a in ("true", "false")]
+    if "ax_" in name and "_kernel<" in name:
+        # ax_dmma_kernel<CG, MASS, PC, DOT>, ax_tma/hi_kernel<N, CG, MASS, PC, DOT>
+        cg = bools[0] == "true" if bools else False
+        dot = len(bools) >= 4 and bools[3] == "true"
+        return "k1" if (cg or dot) else "other"
+    if "k2_kernel<" in name:
+        return "k2" if len(bools) >= 1 and bools[0] == "false" else "other"
+    if "kb_sr_kernel<" in name or "k2p_kernel<" in name:
         return "k2"
-    if ("ax_dmma_kernel" in n or "ax_tma_kernel" in n or "ax_hi_kernel" in n or
-            "ax_dmmag_kernel" in n or "ax_kernel" in n):
-        return "ax"
     return "other"
+
+
+def per_solve(events, its):
+    """Split a trace of consecutive CG solves at cg_init_kernel / sr_init_kernel
+    and keep, per solve, the first `its` K1 and K2 launches (later launches of
+    the last chunk are no-ops after the stop).  Returns {class: [us, ...]} and
+    the number of solves seen."""
+    out = {"k1": [], "k2": []}
+    nsolve = 0
+    cnt = {"k1": 0, "k2": 0}
+    for name, _, d, _ in events:
+        if "cg_init_kernel" in name or "sr_init_kernel" in name:
+            nsolve += 1
+            cnt = {"k1": 0, "k2": 0}
+            continue
+        c = classify(name)
+        if c in cnt and nsolve > 0 and cnt[c] < its:
+            cnt[c] += 1
+            out[c].append(d)
+    return out, nsolve
 
 
 def summarize(events, ncalls: int = 1):
