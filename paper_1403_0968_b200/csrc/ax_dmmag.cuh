@@ -7,6 +7,12 @@
 // tile (w & 3) of the k-slices of parity w >> 2.  The CUDA-core kernels at these
 // orders are register/latency-bound (c4 fractions 0.68 / 0.70 / 0.44 / 0.43).
 // SLICE: G^ in the slice-major layout [k][6][n^2] of the high-order kernel.
+// DOT: the operator half of the split CG K1 at these orders (k1u_kernel does
+// the x / p update first, sem_kernels.cu): w = A_L p plus per-CTA partials of
+// (p, A_L p) into part1 at the iteration parity, a no-op after the stop.  The
+// partial is accumulated in phase A as sum (D p)^T G^ (D p) = p^T D^T G^ D p
+// (the same quantity as p . w, exactly, up to rounding), so p is not needed
+// in phase B (its stage slot may hold the next element already).
 #pragma once
 #include "ax_tma.cuh"
 #include "ax_dmma.cuh"
@@ -32,7 +38,7 @@ struct DgCfg {
     static_assert(n >= 9 && n <= 16 && NG >= 1, "2 x 2 tiles of 8, one element per stage");
 };
 
-template <int N, bool SLICE>
+template <int N, bool SLICE, bool DOT = false>
 __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
     using C = DgCfg<N>;
     constexpr int n = C::n, n2 = C::n2, n3 = C::n3, KS = C::KS, VL = C::VL, STAGE = C::STAGE;
@@ -126,6 +132,23 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
         if (u0 < nunits) issue(u0, 0);
         if (NS == 2 && u0 + TG < nunits) issue(u0 + TG, 1);
     }
+    int kit = 0;
+    if constexpr (DOT) {
+        __shared__ int done_s;
+        if (tid == 0) {
+            done_s = ld_state(&a.st->done);
+            kit = ld_state(&a.st->k1);
+        }
+        __syncthreads();
+        if (done_s) {       // after the stop: drain the issued copies, no work
+            if (leader) {
+                if (u0 < nunits) mbar_wait(gbar + 0, 0);
+                if (NS == 2 && u0 + TG < nunits) mbar_wait(gbar + 1, 0);
+            }
+            return;
+        }
+    }
+    double pap = 0.0;
 
     // D fragments: B of u_r = D[i][m], A of u_s = D[j][m], B of w_r = D[m][i],
     // A of w_s = D[m][j]; rows / columns beyond n are zero
@@ -190,12 +213,19 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
                     double2 g[6];
 #pragma unroll
                     for (int f = 0; f < 6; ++f) g[f] = *reinterpret_cast<const double2 *>(sG + gidx(f, k, j, i0));
-                    *reinterpret_cast<double2 *>(sG + gidx(0, k, j, i0)) =
-                        make_double2(g[0].x * r0 + g[1].x * s0 + g[2].x * t0, g[0].y * r1 + g[1].y * s1 + g[2].y * t1);
-                    *reinterpret_cast<double2 *>(sG + gidx(1, k, j, i0)) =
-                        make_double2(g[1].x * r0 + g[3].x * s0 + g[4].x * t0, g[1].y * r1 + g[3].y * s1 + g[4].y * t1);
-                    *reinterpret_cast<double2 *>(sG + gidx(2, k, j, i0)) =
-                        make_double2(g[2].x * r0 + g[4].x * s0 + g[5].x * t0, g[2].y * r1 + g[4].y * s1 + g[5].y * t1);
+                    const double2 fr = make_double2(g[0].x * r0 + g[1].x * s0 + g[2].x * t0,
+                                                    g[0].y * r1 + g[1].y * s1 + g[2].y * t1);
+                    const double2 fs = make_double2(g[1].x * r0 + g[3].x * s0 + g[4].x * t0,
+                                                    g[1].y * r1 + g[3].y * s1 + g[4].y * t1);
+                    const double2 ft = make_double2(g[2].x * r0 + g[4].x * s0 + g[5].x * t0,
+                                                    g[2].y * r1 + g[4].y * s1 + g[5].y * t1);
+                    *reinterpret_cast<double2 *>(sG + gidx(0, k, j, i0)) = fr;
+                    *reinterpret_cast<double2 *>(sG + gidx(1, k, j, i0)) = fs;
+                    *reinterpret_cast<double2 *>(sG + gidx(2, k, j, i0)) = ft;
+                    if constexpr (DOT) {   // p^T A p = (D p)^T G^ (D p), node by node (pairs valid: n even)
+                        pap = fma(r0, fr.x, fma(s0, fs.x, fma(t0, ft.x, pap)));
+                        pap = fma(r1, fr.y, fma(s1, fs.y, fma(t1, ft.y, pap)));
+                    }
                 }
                 continue;
             }
@@ -203,17 +233,25 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
                 const double g0 = sG[gidx(0, k, j, i0)], g1 = sG[gidx(1, k, j, i0)];
                 const double g2 = sG[gidx(2, k, j, i0)], g3 = sG[gidx(3, k, j, i0)];
                 const double g4 = sG[gidx(4, k, j, i0)], g5 = sG[gidx(5, k, j, i0)];
-                sG[gidx(0, k, j, i0)] = g0 * r0 + g1 * s0 + g2 * t0;
-                sG[gidx(1, k, j, i0)] = g1 * r0 + g3 * s0 + g4 * t0;
-                sG[gidx(2, k, j, i0)] = g2 * r0 + g4 * s0 + g5 * t0;
+                const double fr = g0 * r0 + g1 * s0 + g2 * t0;
+                const double fs = g1 * r0 + g3 * s0 + g4 * t0;
+                const double ft = g2 * r0 + g4 * s0 + g5 * t0;
+                sG[gidx(0, k, j, i0)] = fr;
+                sG[gidx(1, k, j, i0)] = fs;
+                sG[gidx(2, k, j, i0)] = ft;
+                if constexpr (DOT) pap = fma(r0, fr, fma(s0, fs, fma(t0, ft, pap)));
             }
             if (v1) {
                 const double g0 = sG[gidx(0, k, j, i0 + 1)], g1 = sG[gidx(1, k, j, i0 + 1)];
                 const double g2 = sG[gidx(2, k, j, i0 + 1)], g3 = sG[gidx(3, k, j, i0 + 1)];
                 const double g4 = sG[gidx(4, k, j, i0 + 1)], g5 = sG[gidx(5, k, j, i0 + 1)];
-                sG[gidx(0, k, j, i0 + 1)] = g0 * r1 + g1 * s1 + g2 * t1;
-                sG[gidx(1, k, j, i0 + 1)] = g1 * r1 + g3 * s1 + g4 * t1;
-                sG[gidx(2, k, j, i0 + 1)] = g2 * r1 + g4 * s1 + g5 * t1;
+                const double fr = g0 * r1 + g1 * s1 + g2 * t1;
+                const double fs = g1 * r1 + g3 * s1 + g4 * t1;
+                const double ft = g2 * r1 + g4 * s1 + g5 * t1;
+                sG[gidx(0, k, j, i0 + 1)] = fr;
+                sG[gidx(1, k, j, i0 + 1)] = fs;
+                sG[gidx(2, k, j, i0 + 1)] = ft;
+                if constexpr (DOT) pap = fma(r1, fr, fma(s1, fs, fma(t1, ft, pap)));
             }
         }
         if constexpr (SPLIT) fence_proxy_async();   // generic reads of u, G^ 3..5 done
@@ -256,6 +294,7 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
             double *wo = a.w + e * n3 + k * n2 + j * n + i0;
             if (v0) wo[0] = w0 + t0;
             if (v1) wo[1] = w1 + t1;
+
         }
         fence_proxy_async();
         group_bar(1 + g, GT);
@@ -264,6 +303,11 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
         } else {
             if (leader && e + NS * TG < nunits) issue(e + NS * TG, s);
         }
+    }
+    if constexpr (DOT) {
+        __shared__ double sred[DgCfg<N>::NT / 32];
+        const double bs = block_sum<DgCfg<N>::NT>(pap, sred);
+        if (tid == 0) a.part1[(kit & 1) * a.red.s1 + blockIdx.x] = bs;
     }
 }
 

@@ -51,8 +51,49 @@ bool dmmag_supported(int N) { return N >= 8 && N <= 15; }
     default: break;                                                          \
     }
 
+int dmmag_blocks(int N, int64_t E, int nsm) {
+    int nb = 0;
+    SEM_DG_DISPATCH(N, nb = dmmag_grid<NN>(E, nsm));
+    return nb;
+}
+
+// The split CG K1 at N >= 10 (use_k1ax): the x / p update with the scalar
+// prologue (k1u_kernel), then the tensor-core operator on the new p with the
+// (p, A p) partials (ax_dmmag_kernel DOT) -- 8 B per node more than a fused
+// K1 (p is read twice) but the operator runs on the tensor cores instead of
+// the register-bound CUDA-core high-order kernels.
+cudaError_t launch_ax_cg_dmmag(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne, int pidx0,
+                               cudaStream_t s) {
+    cudaError_t e = launch_k1u(m, v, eb, ne, s);
+    if (e != cudaSuccess) return e;
+    const int64_t o = eb * m.n3;
+    TmaArgs a{};
+    a.E = ne;
+    a.G = m.G + 6 * o;
+    a.u = v.p + o;
+    a.w = v.w + o;
+    a.red = make_red(m, v);
+    a.part1 = v.part1 + pidx0;
+    a.st = v.st;
+    if (m.use_hi) {
+        SEM_DG_DISPATCH(m.N, e = launch_pdl(ax_dmmag_kernel<NN, true, true>, dmmag_grid<NN>(ne, m.nsm),
+                                            DgCfg<NN>::NT, DgCfg<NN>::SMEM, s, a));
+    } else {
+        SEM_DG_DISPATCH(m.N, e = launch_pdl(ax_dmmag_kernel<NN, false, true>, dmmag_grid<NN>(ne, m.nsm),
+                                            DgCfg<NN>::NT, DgCfg<NN>::SMEM, s, a));
+    }
+    return e;
+}
+
 cudaError_t dmmag_prepare(int N) {
     cudaError_t e = cudaSuccess;
+    SEM_DG_DISPATCH(N, (e = cudaFuncSetAttribute(ax_dmmag_kernel<NN, false, true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)DgCfg<NN>::SMEM),
+                        e = (e == cudaSuccess ? cudaFuncSetAttribute(ax_dmmag_kernel<NN, true, true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)DgCfg<NN>::SMEM) : e)));
+    if (e != cudaSuccess) return e;
     SEM_DG_DISPATCH(N, (e = cudaFuncSetAttribute(ax_dmmag_kernel<NN, false>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)DgCfg<NN>::SMEM),

@@ -594,10 +594,12 @@ __global__ void __launch_bounds__(HiCfg<N, CG>::NT, 1) ax_hi_kernel(TmaArgs a) {
 #pragma unroll
             for (int k = 0; k < n; ++k) {
                 const int q = k * n2 + ijc;
-                const double rl = sr[q];
+                // (padding lanes share a real lane's column: they must not
+                // read it while its owner rewrites it -- racecheck r02m)
+                const double rl = lane_on ? sr[q] : 0.0;
                 double pl = rl;
                 if (kit > 0) {
-                    const double po = sp[q];
+                    const double po = lane_on ? sp[q] : 0.0;
                     if (lane_on) a.x[gb + k * n2] = xc[k] + alpha_prev * po;
                     pl = rl + beta * po;
                 }

@@ -551,6 +551,15 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         const char *dg = getenv("SEM_DMMAG");
         const bool dg_on = dg ? dg[0] == '1' : (force_dmma || !impl || !*impl) && N >= 10;
         dm.use_dmmag = dmmag_supported(N) && (dm.use_tma || dm.use_hi) && dg_on;
+        // the split K1 (x / p update + tensor-core operator with (p,Ap)) where
+        // it beats the fused CUDA-core K1: N >= 11 (c4 CG per iteration, r02o:
+        // N=11 544 vs 591 us, 12 679 vs 788, 13 569 vs 668, 14 594 vs 829,
+        // 15 568 vs 671; N=10 586 vs 569).  SEM_K1_AX=fused|split forces.
+        const char *k1ax = getenv("SEM_K1_AX");
+        const bool ax_fused = k1ax && strcmp(k1ax, "fused") == 0;
+        const bool ax_split = k1ax && strcmp(k1ax, "split") == 0;
+        dm.use_k1ax = dm.use_dmmag && !ax_fused && (ax_split || N >= 11);
+        if (dm.H) dm.use_k1ax = false;             // (the tensor-core operator has no mass term)
         if (dm.H && !dm.use_tma && !dm.use_hi) {   // only TMA / hi carry the mass term
             dm.use_hi = hi_supported(N) && N >= hi_min;
             dm.use_tma = !dm.use_hi && tma_supported(N);
@@ -811,7 +820,9 @@ static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
     const int P = ctx->nranks;
     int rc;
     // K1 algorithmic bytes per local node (+8: the mass diagonal, screened operator)
-    const double k1_bpn = (k == 0 ? 72.0 : 96.0) + (ctx->dm.H ? 8.0 : 0.0);
+    // (split K1, use_k1ax: x / p update 40 B (16 at k = 0) + operator 64 B)
+    const double k1_bpn = ctx->dm.use_k1ax ? (k == 0 ? 80.0 : 104.0)
+                                           : (k == 0 ? 72.0 : 96.0) + (ctx->dm.H ? 8.0 : 0.0);
     if (k1_split(ctx->dm)) {
         // boundary elements first; the exchange of their w runs on the side
         // stream while the interior elements' K1 runs here
@@ -819,6 +830,7 @@ static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
         const int64_t nb = m.nbnd, ni = m.E - m.nbnd;
         const int gA = ax_cg_range_blocks(m, nb);
         LAUNCHP(kProfAxCg, k1_bpn * m.n3 * nb, k, launch_ax_cg_range(m, v, 0, nb, 0, s));
+        ctx->launches += m.use_k1ax ? 1 : 0;
         if (P > 1) {
             CU(cudaEventRecord(ctx->fork_ev, s));
             CU(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
@@ -826,6 +838,7 @@ static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
             CU(cudaEventRecord(ctx->join_ev, ctx->side));
         }
         LAUNCHP(kProfAxCg, k1_bpn * m.n3 * ni, k, launch_ax_cg_range(m, v, nb, ni, gA, s));
+        ctx->launches += m.use_k1ax ? 1 : 0;
         if (P > 1) {
             LAUNCH(launch_cg_red_pap(ctx->dm, v, s));
             CU(cudaStreamWaitEvent(s, ctx->join_ev, 0));
@@ -833,6 +846,7 @@ static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
         }
     } else {
         LAUNCHP(kProfAxCg, k1_bpn * ctx->L, k, launch_ax_cg(ctx->dm, v, s));
+        ctx->launches += ctx->dm.use_k1ax ? 1 : 0;
         if (P > 1) {
             if ((rc = exchange_impl(ctx, v.w, s))) return rc;
             LAUNCH(launch_cg_red_pap(ctx->dm, v, s));

@@ -65,6 +65,8 @@ struct DevMesh {
     bool use_hi;                // TMA vector + register-streamed G^ kernels (high N)
     bool use_dmma;              // N = 7: r/s contractions on the FP64 tensor cores (ax_dmma.cuh)
     bool use_dmmag;             // N = 8..11: the plain Ax on the tensor cores (ax_dmmag.cuh)
+    bool use_k1ax;              // CG K1 split in two launches: x / p update (k1u_kernel), then
+                                // the tensor-core operator with (p, A p) partials (use_dmmag, !H)
 };
 
 struct CgVecs {
@@ -153,6 +155,11 @@ cudaError_t dmmag_prepare(int N);
 cudaError_t launch_ax_dmmag(const DevMesh &m, const double *u, double *w, cudaStream_t s);
 int tma_blocks(int N, int64_t E, int nsm, bool cg);
 int dmma_blocks(int64_t E, int nsm, bool cg);   // N = 7 tensor-core kernel grid
+int dmmag_blocks(int N, int64_t E, int nsm);     // N >= 8 tensor-core kernel grid
+// the split K1 (use_k1ax): k1u_kernel over the range, then ax_dmmag_kernel<DOT>
+cudaError_t launch_ax_cg_dmmag(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne, int pidx0,
+                               cudaStream_t s);
+cudaError_t launch_k1u(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne, cudaStream_t s);
 cudaError_t tma_prepare(int N, bool mass);
 cudaError_t upload_const_D(int N, const double *D_host);
 cudaError_t launch_ax_tma(const DevMesh &m, const double *u, double *w, cudaStream_t s);

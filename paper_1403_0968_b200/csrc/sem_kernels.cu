@@ -431,6 +431,53 @@ __global__ void __launch_bounds__(kRedThreads) cg_red_kernel(const double *part,
     if (threadIdx.x == 0) all[(kk & 3) * nranks + rank] = v;
 }
 
+// K1, first half, of the split schedule (use_k1ax, N >= 10 on the tensor
+// cores): the scalar prologue of the iteration (stop, beta_k, alpha_{k-1};
+// cg_device.cuh) and the vector update x += alpha_{k-1} p_{k-1},
+// p = r + beta_k p_{k-1} (z instead of r for Jacobi PCG) over [0, L).  40 B
+// per node (r, p, x read; p, x written; 16 at k = 0).  The second half,
+// ax_dmmag_kernel<DOT>, applies the operator to the new p.
+constexpr int kKuThreads = 256;
+__global__ void __launch_bounds__(kKuThreads) k1u_kernel(const double *__restrict__ src, double *p,
+                                                         double *x, int64_t L, CgRed R, CgState *st) {
+    __shared__ double sred[4 * (kKuThreads / 32)];
+    pdl_wait();
+    const CgStep c = cg_k1_prologue<kKuThreads>(st, R, sred);
+    if (c.done) return;
+    const double beta = c.beta, ap = c.alpha_prev;
+    const int64_t npair = L >> 1;
+    const int64_t stride = int64_t(gridDim.x) * kKuThreads;
+    for (int64_t q = blockIdx.x * int64_t(kKuThreads) + threadIdx.x; q < npair; q += stride) {
+        const double2 rv = __ldcs(reinterpret_cast<const double2 *>(src) + q);
+        double2 *pp = reinterpret_cast<double2 *>(p) + q;
+        if (c.k == 0) {
+            *pp = rv;
+        } else {
+            const double2 pv = *pp;
+            double2 *xp = reinterpret_cast<double2 *>(x) + q;
+            const double2 xv = *xp;
+            *xp = make_double2(xv.x + ap * pv.x, xv.y + ap * pv.y);
+            *pp = make_double2(rv.x + beta * pv.x, rv.y + beta * pv.y);
+        }
+    }
+    if ((L & 1) && blockIdx.x == 0 && threadIdx.x == 0) {     // odd length: the last node
+        const int64_t l = L - 1;
+        if (c.k == 0) {
+            p[l] = src[l];
+        } else {
+            const double pv = p[l];
+            x[l] = x[l] + ap * pv;
+            p[l] = src[l] + beta * pv;
+        }
+    }
+}
+
+cudaError_t launch_k1u(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne, cudaStream_t s) {
+    const int64_t o = eb * m.n3;
+    return launch_pdl(k1u_kernel, m.nsm * 4, kKuThreads, 0, s, k1_src(v) + o, v.p + o, v.xw + o,
+                      ne * m.n3, make_red(m, v), v.st);
+}
+
 // x = xw + alpha_{it-1} p_{it-1}: the update K1 would have applied next.
 __global__ void cg_finish_kernel(int64_t L, double *__restrict__ x, const double *__restrict__ xw,
                                  const double *__restrict__ p, const CgState *st) {
@@ -483,6 +530,7 @@ static int ax_grid(int N, int64_t E, int nsm) {
 
 // grid of K1 over ne elements (range launches: TMA / high-order kernels only)
 int ax_cg_range_blocks(const DevMesh &m, int64_t ne) {
+    if (m.use_k1ax) return dmmag_blocks(m.N, ne, m.nsm);
     if (m.use_dmma) return dmma_blocks(ne, m.nsm, true);
     if (m.use_hi) return hi_blocks(m.N, ne, m.nsm, true);
     return m.use_tma ? tma_blocks(m.N, ne, m.nsm, true) : ax_grid(m.N, ne, m.nsm);
@@ -525,6 +573,7 @@ cudaError_t launch_ax(const DevMesh &m, const double *u, double *w, cudaStream_t
 }
 
 cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
+    if (m.use_k1ax) return launch_ax_cg_dmmag(m, v, 0, m.E, 0, s);
     if (m.use_hi) return launch_ax_cg_hi(m, v, 0, m.E, 0, s);
     if (m.use_tma) return launch_ax_cg_tma(m, v, 0, m.E, 0, s);
     if (m.H) return cudaErrorInvalidValue;
@@ -537,6 +586,7 @@ cudaError_t launch_ax_cg(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
 
 cudaError_t launch_ax_cg_range(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne, int pidx0,
                                cudaStream_t s) {
+    if (m.use_k1ax) return launch_ax_cg_dmmag(m, v, eb, ne, pidx0, s);
     if (m.use_hi) return launch_ax_cg_hi(m, v, eb, ne, pidx0, s);
     if (m.use_tma) return launch_ax_cg_tma(m, v, eb, ne, pidx0, s);
     return cudaErrorInvalidValue;   // the simple kernel covers all elements only
