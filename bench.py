@@ -629,7 +629,7 @@ def main():
     k1_name = ("K1: ax_dmma_kernel<CG=true> (N=7: r/s contractions on the FP64 tensor cores; "
                "x/p update + Ax + (p,Ap) partials)" if dmma else
                "K1: ax_tma_kernel<N,CG=true> (x/p update + Ax + (p,Ap) partials)")
-    traffic = ncu_traffic(("ax_dmma_kernel<1, 0, 0, 0>",) if dmma else
+    traffic = ncu_traffic(("ax_dmma_kernel<1, 0, 0, 0",) if dmma else
                           (f"ax_tma_kernel<{args.N}, true, false>", f"ax_tma_kernel<{args.N}, 1>")) \
         if alpha is None and args.precond == "none" and args.cg_variant == "standard" else None
     # share of the timed solve: per-solve device time of each class inside the
