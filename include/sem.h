@@ -208,6 +208,23 @@ int sem_nccl_get_unique_id(void *id_out);
  * SEM_LOOPBACK_TIMEOUT_MS (default 120000) instead of hanging. */
 int sem_loopback_unique_id(void *id_out);
 
+/* Transport selection (environment, read by sem_setup; all ranks must agree):
+ * SEM_COMM=p2p selects the PEER-MEMORY transport instead of NCCL / the
+ * host-rendezvous loopback: every rank owns a device window (exchange receive
+ * areas, all-gather slots, per-site epoch flags); the interface exchange
+ * stores each partial sum straight into the neighbour's window and the scalar
+ * all-gathers are one-warp kernels that store into every peer's slots,
+ * release a flag at system scope and acquire the peers' -- device work only,
+ * captured into the CUDA graphs (the one-shot
+ * device-side reduction).  Windows are shared as raw pointers inside one
+ * process (the loopback world) and through CUDA IPC across processes
+ * (peer access over NVLink).  Spins time out after SEM_P2P_TIMEOUT_MS
+ * (default 20000) and make the context report SEM_ENCCL.  Caveat for several
+ * ranks on ONE device (the loopback world): a rank that calls a
+ * device-synchronising CUDA function (first allocations, lazy module loading)
+ * while a peer's kernel spins stalls that peer until the timeout; warm up
+ * first (CUDA_MODULE_LOADING=EAGER, allocate before the first collective). */
+
 /* Device timing per kernel class, for the benchmark's roofline report.
  * sem_profile(ctx, 1) resets the accumulators and brackets every later launch
  * with a pair of CUDA events on the context stream (host-side cost only);
@@ -241,6 +258,13 @@ int sem_profile_read(sem_ctx *ctx, int which, double *ms, int64_t *launches, dou
  * SEM_EINVAL (with *nslot set) if cap < *nslot.  For tests and tooling. */
 int sem_exchange_plan(const sem_mesh *mesh, int N, int64_t *counts, int64_t *ids, int64_t cap,
                       int64_t *nslot, int64_t *nglobal);
+
+/* SEM_OK, or the sticky error of the context: SEM_ENCCL after a collective
+ * of the peer-memory transport timed out (a peer never arrived; the
+ * asynchronous work of that collective used stale data), SEM_ECUDA after a
+ * CUDA failure.  Does not synchronise.  Every collective entry point also
+ * reports such an error. */
+int sem_status(sem_ctx *ctx);
 
 /* Number of kernels this context has launched so far (all entry points). */
 int64_t sem_launch_count(const sem_ctx *ctx);

@@ -46,7 +46,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
     inc, lib = nccl_dirs()
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
-    common = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+    common = ["nvcc", *ARCH, *os.environ.get("SEM_NVCC_EXTRA", "").split(), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-O2", "-Xptxas", "-warn-spills",
               "-I", os.path.join(ROOT, "include"), "-I", inc]
     hdr = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "sem.h"),

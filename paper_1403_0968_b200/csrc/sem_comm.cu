@@ -177,8 +177,78 @@ static bool loop_barrier(LoopWorld &w) {
     return true;
 }
 
+// ---------------------------------------------------------------------------
+// peer-memory transport (SEM_COMM=p2p): every rank owns a window -- a header
+// of per-site epoch counters, arrival flags and all-gather slots, then two
+// receive areas for the interface exchange -- that its peers write into
+// directly (device stores to peer memory: the same device for the one-GPU
+// loopback world, CUDA IPC + NVLink peer access across processes).  A
+// collective is device work only, so it is captured into the CUDA graphs:
+//   exchange:   p2p_pack_kernel stores each partial sum straight into the
+//               peer's receive area (parity of the next epoch), then
+//               p2p_sync_kernel (one warp) bumps the epoch, releases a flag
+//               at every neighbour and spins (acquire) until every
+//               neighbour's flag for this epoch has arrived; combine_kernel
+//               reads the local receive area of that parity;
+//   all-gather: p2p_allgather_kernel (one warp) stores this rank's values
+//               into every peer's slots, releases the flags, acquires the
+//               peers' and copies their values out (the one-shot,
+//               fixed-order reduction of SURVEY.md §8(e) step 3).
+// Two parities suffice: a rank can only rewrite a peer's parity-p area at
+// epoch e+2 after that peer signalled e+1, i.e. after it consumed epoch e.
+// Spins time out (SEM_P2P_TIMEOUT_MS) and raise a host-mapped error flag,
+// after which every later spin of the context fails at once.
+// ---------------------------------------------------------------------------
+struct P2PHead {
+    unsigned long long flags[kSites][kMaxRanks];   // flags[site][q]: last epoch rank q signalled here
+    unsigned long long ctr[kSites];                 // this rank's epoch per site
+    double scal[kSites][2][2 * kMaxRanks];          // all-gather slots [site][parity][rank * count + c]
+};
+struct P2PPeers {
+    P2PHead *head[kMaxRanks];                       // every rank's window header (own included)
+    double *recv[2][kMaxRanks];                     // every rank's exchange receive areas
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// spin until *flag >= e (acquire); false on timeout (error flag raised)
+__device__ __forceinline__ bool p2p_wait(const unsigned long long *flag, unsigned long long e,
+                                         unsigned long long timeout_ns, unsigned *err) {
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_sys(flag) < e) {
+        // after a first timeout every later collective fails fast
+        if (*reinterpret_cast<volatile unsigned *>(err)) return false;
+        if (global_ns() - t0 > timeout_ns) {
+            atomicExch(err, 1u);
+            return false;
+        }
+    }
+    return true;
+}
+
 struct Comm {
     ncclComm_t nccl = nullptr;
+    // peer-memory transport (SEM_COMM=p2p)
+    bool p2p = false;
+    char *win = nullptr;                 // own window (cudaMalloc: IPC-exportable)
+    P2PPeers peers{};
+    std::vector<void *> ipc_opened;      // peers' windows opened through CUDA IPC
+    int32_t *slot_rank = nullptr;        // per send slot: destination rank
+    int64_t *slot_off = nullptr;         // ... and offset in its receive area
+    int32_t *plist = nullptr;            // neighbour ranks (device)
+    unsigned *err_h = nullptr, *err_d = nullptr;   // host-mapped timeout flag
+    unsigned long long timeout_ns = 0;
     LoopWorld *lw = nullptr;             // loopback transport (tests) instead of NCCL
     std::string lw_key;
     int rank = 0, nranks = 1;
@@ -191,7 +261,10 @@ struct Comm {
     int32_t *send_group = nullptr, *if_group = nullptr, *if_off = nullptr, *if_src = nullptr;
 };
 
-bool comm_capturable(const Comm *c) { return c && !c->lw; }
+// the host-rendezvous loopback transport cannot be captured; the peer-memory
+// transport (device work only) and NCCL can
+bool comm_capturable(const Comm *c) { return c && (!c->lw || c->p2p); }
+bool comm_device_only(const Comm *c) { return c && c->p2p; }
 
 __device__ __forceinline__ void group_loc(const GsClasses &cls, int g, int &m, int &cnt, int &q,
                                           int &off) {
@@ -223,11 +296,14 @@ __global__ void pack_kernel(const __grid_constant__ GsClasses cls, const int32_t
 
 // total = partials of all sharing ranks in ascending rank order, into the
 // group's first copy; the other copies zeroed
+// (peer-memory transport: recvbuf1 != nullptr, the area of parity ctr & 1)
 __global__ void combine_kernel(const __grid_constant__ GsClasses cls, const int32_t *idx,
                                double *w, const int32_t *if_group, const int32_t *if_off,
-                               const int32_t *if_src, int nif, const double *recvbuf) {
+                               const int32_t *if_src, int nif, const double *recvbuf,
+                               const double *recvbuf1, const unsigned long long *ctr) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nif) return;
+    if (recvbuf1 && (*ctr & 1)) recvbuf = recvbuf1;
     const int g = if_group[i];
     const double local = group_local_sum(cls, idx, w, g);
     double tot = 0.0;
@@ -241,6 +317,59 @@ __global__ void combine_kernel(const __grid_constant__ GsClasses cls, const int3
     const int32_t *ix = idx + off;
     w[__ldg(ix + q)] = tot;
     for (int t = 1; t < m; ++t) w[__ldg(ix + t * cnt + q)] = 0.0;
+}
+
+// exchange, peer-memory transport: partial sums straight into the peers'
+// receive areas (parity of the coming epoch)
+__global__ void p2p_pack_kernel(const __grid_constant__ GsClasses cls, const int32_t *idx,
+                                const double *w, const int32_t *send_group, int64_t nslot,
+                                const int32_t *slot_rank, const int64_t *slot_off,
+                                const __grid_constant__ P2PPeers peers, int me) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < nslot) {
+        const int par = (int)((peers.head[me]->ctr[kSiteExchange] + 1) & 1);
+        peers.recv[par][slot_rank[t]][slot_off[t]] = group_local_sum(cls, idx, w, send_group[t]);
+    }
+    __threadfence_system();     // the stores reach the peers before the flag does
+}
+
+// one warp: epoch of `site` += 1, flag at every rank of plist, wait for theirs
+__global__ void p2p_sync_kernel(const __grid_constant__ P2PPeers peers, int me, int site,
+                                const int32_t *plist, int np, unsigned long long timeout_ns,
+                                unsigned *err) {
+    P2PHead *mine = peers.head[me];
+    const unsigned long long e = mine->ctr[site] + 1;
+    __syncwarp();
+    if (threadIdx.x == 0) mine->ctr[site] = e;
+    __threadfence_system();
+    for (int i = threadIdx.x; i < np; i += 32) st_release_sys(&peers.head[plist[i]]->flags[site][me], e);
+    for (int i = threadIdx.x; i < np; i += 32) p2p_wait(&mine->flags[site][plist[i]], e, timeout_ns, err);
+}
+
+// one warp: this rank's `count` values at slot_base[me * count ..] into every
+// peer's slots, flags, then every peer's values (acquired) into slot_base
+__global__ void p2p_allgather_kernel(const __grid_constant__ P2PPeers peers, int me, int P, int site,
+                                     double *slot_base, int count, unsigned long long timeout_ns,
+                                     unsigned *err) {
+    P2PHead *mine = peers.head[me];
+    const unsigned long long e = mine->ctr[site] + 1;
+    const int par = (int)(e & 1);
+    __syncwarp();
+    if (threadIdx.x == 0) mine->ctr[site] = e;
+    double v[2];
+    for (int c = 0; c < count; ++c) v[c] = slot_base[me * count + c];
+    for (int q = threadIdx.x; q < P; q += 32) {
+        if (q == me) continue;
+        for (int c = 0; c < count; ++c) peers.head[q]->scal[site][par][me * count + c] = v[c];
+    }
+    __threadfence_system();
+    for (int q = threadIdx.x; q < P; q += 32)
+        if (q != me) st_release_sys(&peers.head[q]->flags[site][me], e);
+    for (int q = threadIdx.x; q < P; q += 32) {
+        if (q == me) continue;
+        if (!p2p_wait(&mine->flags[site][q], e, timeout_ns, err)) continue;
+        for (int c = 0; c < count; ++c) slot_base[q * count + c] = mine->scal[site][par][q * count + c];
+    }
 }
 
 #define NC(call)                                                                    \
@@ -346,6 +475,93 @@ static int loop_collective(Comm &c, double *mine, cudaStream_t s, std::string &e
     return SEM_OK;
 }
 
+// Peer-memory transport setup (collective over mesh->allgather): allocate and
+// zero this rank's window, publish its address (the raw pointer inside one
+// process -- the loopback world --, a CUDA IPC handle across processes), the
+// size of its receive area and where in it each peer's slots start; open the
+// peers' windows; per send slot, the destination rank and offset.
+struct P2PInfo {
+    unsigned long long ptr;
+    long long nslot;
+    cudaIpcMemHandle_t h;
+    long long off_to[kMaxRanks];    // offset of the slots shared with rank q (-1: none)
+    long long cnt_to[kMaxRanks];
+};
+
+static int p2p_join(Comm &c, const sem_mesh *mesh, bool same_process, std::string &err) {
+    const int P = c.nranks, me = c.rank;
+    const size_t ns = (size_t)std::max<int64_t>(c.nslot, 1);
+    const size_t bytes = sizeof(P2PHead) + 2 * ns * sizeof(double);
+    CC(cudaMalloc(&c.win, bytes));
+    CC(cudaMemset(c.win, 0, bytes));
+    CC(cudaDeviceSynchronize());
+    P2PInfo mine{};
+    mine.ptr = (unsigned long long)(uintptr_t)c.win;
+    mine.nslot = (long long)ns;
+    if (!same_process) CC(cudaIpcGetMemHandle(&mine.h, c.win));
+    for (int q = 0; q < kMaxRanks; ++q) mine.off_to[q] = mine.cnt_to[q] = -1;
+    for (size_t p = 0; p < c.peer.size(); ++p) {
+        mine.off_to[c.peer[p]] = c.peer_off[p];
+        mine.cnt_to[c.peer[p]] = c.peer_off[p + 1] - c.peer_off[p];
+    }
+    std::vector<P2PInfo> all(P);
+    if (!mesh->allgather || mesh->allgather(mesh->allgather_user, &mine, sizeof mine, all.data()) != 0) {
+        err = "p2p: setup all-gather failed";
+        return SEM_ENCCL;
+    }
+    for (int q = 0; q < P; ++q) {
+        char *base = nullptr;
+        if (q == me) {
+            base = c.win;
+        } else if (same_process) {
+            base = reinterpret_cast<char *>((uintptr_t)all[q].ptr);
+        } else {
+            void *ptr = nullptr;
+            CC(cudaIpcOpenMemHandle(&ptr, all[q].h, cudaIpcMemLazyEnablePeerAccess));
+            c.ipc_opened.push_back(ptr);
+            base = static_cast<char *>(ptr);
+        }
+        c.peers.head[q] = reinterpret_cast<P2PHead *>(base);
+        double *r0 = reinterpret_cast<double *>(base + sizeof(P2PHead));
+        c.peers.recv[0][q] = r0;
+        c.peers.recv[1][q] = r0 + all[q].nslot;
+    }
+    // destinations of my send slots
+    std::vector<int32_t> srank((size_t)ns, 0);
+    std::vector<int64_t> soff((size_t)ns, 0);
+    for (size_t p = 0; p < c.peer.size(); ++p) {
+        const int q = c.peer[p];
+        const long long n = c.peer_off[p + 1] - c.peer_off[p];
+        if (all[q].off_to[me] < 0 || all[q].cnt_to[me] != n) {
+            err = "p2p: asymmetric exchange plan";
+            return SEM_EINVAL;
+        }
+        for (long long t = 0; t < n; ++t) {
+            srank[(size_t)(c.peer_off[p] + t)] = q;
+            soff[(size_t)(c.peer_off[p] + t)] = all[q].off_to[me] + t;
+        }
+    }
+    CC(cudaMalloc(&c.slot_rank, sizeof(int32_t) * ns));
+    CC(cudaMalloc(&c.slot_off, sizeof(int64_t) * ns));
+    CC(cudaMalloc(&c.plist, sizeof(int32_t) * std::max<size_t>(c.peer.size(), 1)));
+    CC(cudaMemcpy(c.slot_rank, srank.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice));
+    CC(cudaMemcpy(c.slot_off, soff.data(), sizeof(int64_t) * ns, cudaMemcpyHostToDevice));
+    if (!c.peer.empty())
+        CC(cudaMemcpy(c.plist, c.peer.data(), sizeof(int32_t) * c.peer.size(), cudaMemcpyHostToDevice));
+    CC(cudaHostAlloc(&c.err_h, sizeof(unsigned), cudaHostAllocMapped));
+    *c.err_h = 0;
+    CC(cudaHostGetDevicePointer(&c.err_d, c.err_h, 0));
+    const char *to = getenv("SEM_P2P_TIMEOUT_MS");
+    c.timeout_ns = (unsigned long long)(to ? atoll(to) : 20000) * 1000000ull;
+    // every rank's window is zeroed before anyone can signal into it
+    int ok = 1, oks[kMaxRanks];
+    if (mesh->allgather(mesh->allgather_user, &ok, sizeof ok, oks) != 0) {
+        err = "p2p: setup all-gather failed";
+        return SEM_ENCCL;
+    }
+    return SEM_OK;
+}
+
 int comm_setup(Comm *&cp, const sem_mesh *mesh, const ExchangePlan &ep, const DevMesh &,
                cudaStream_t s, std::string &err) {
     cp = new Comm;
@@ -357,7 +573,11 @@ int comm_setup(Comm *&cp, const sem_mesh *mesh, const ExchangePlan &ep, const De
     c.nslot = (int64_t)ep.shared_ids.size();
     c.nif = (int)ep.if_group.size();
     const bool loop = std::memcmp(mesh->nccl_id, kLoopMagic, sizeof kLoopMagic) == 0;
-    if (!loop) {
+    {
+        const char *cm = getenv("SEM_COMM");
+        c.p2p = cm && strcmp(cm, "p2p") == 0;
+    }
+    if (!loop && !c.p2p) {
         ncclUniqueId id;
         std::memcpy(&id, mesh->nccl_id, sizeof id);
         NC(ncclCommInitRank(&c.nccl, c.nranks, id, c.rank));
@@ -381,6 +601,7 @@ int comm_setup(Comm *&cp, const sem_mesh *mesh, const ExchangePlan &ep, const De
     CC(cudaMemcpyAsync(c.if_off, ep.if_off.data(), sizeof(int32_t) * (c.nif + 1),
                        cudaMemcpyHostToDevice, s));
     CC(cudaStreamSynchronize(s));
+    if (c.p2p) return p2p_join(c, mesh, loop, err);
     if (loop) return loop_join(c, mesh, err);
     return SEM_OK;
 }
@@ -393,6 +614,26 @@ int comm_exchange(Comm *cp, const DevMesh &m, double *w, cudaStream_t s, int64_t
         return SEM_ESTATE;
     }
     Comm &c = *cp;
+    if (c.p2p) {
+        if (c.nslot) {
+            p2p_pack_kernel<<<(int)((c.nslot + 255) / 256), 256, 0, s>>>(
+                m.cls, m.gs_idx, w, c.send_group, c.nslot, c.slot_rank, c.slot_off, c.peers, c.rank);
+            CC(cudaGetLastError());
+            ++nlaunch;
+        }
+        p2p_sync_kernel<<<1, 32, 0, s>>>(c.peers, c.rank, kSiteExchange, c.plist, (int)c.peer.size(),
+                                         c.timeout_ns, c.err_d);
+        CC(cudaGetLastError());
+        ++nlaunch;
+        if (c.nif) {
+            combine_kernel<<<(c.nif + 255) / 256, 256, 0, s>>>(
+                m.cls, m.gs_idx, w, c.if_group, c.if_off, c.if_src, c.nif, c.peers.recv[0][c.rank],
+                c.peers.recv[1][c.rank], &c.peers.head[c.rank]->ctr[kSiteExchange]);
+            CC(cudaGetLastError());
+            ++nlaunch;
+        }
+        return SEM_OK;
+    }
     if (c.nslot) {
         pack_kernel<<<(int)((c.nslot + 255) / 256), 256, 0, s>>>(m.cls, m.gs_idx, w, c.send_group,
                                                                  c.nslot, c.sendbuf);
@@ -422,27 +663,31 @@ int comm_exchange(Comm *cp, const DevMesh &m, double *w, cudaStream_t s, int64_t
     }
     if (c.nif) {
         combine_kernel<<<(c.nif + 255) / 256, 256, 0, s>>>(m.cls, m.gs_idx, w, c.if_group, c.if_off,
-                                                           c.if_src, c.nif, c.recvbuf);
+                                                           c.if_src, c.nif, c.recvbuf, nullptr,
+                                                           nullptr);
         CC(cudaGetLastError());
         ++nlaunch;
     }
     return SEM_OK;
 }
 
-int comm_allgather_scalar(Comm *cp, double *slot_base, cudaStream_t s, std::string &err) {
-    if (!cp) {
-        err = "no communicator";
-        return SEM_ESTATE;
-    }
-    return comm_allgather(cp, slot_base, 1, s, err);
-}
-
-int comm_allgather(Comm *cp, double *slot_base, int count, cudaStream_t s, std::string &err) {
+int comm_allgather(Comm *cp, double *slot_base, int count, int site, cudaStream_t s,
+                   std::string &err) {
     if (!cp) {
         err = "no communicator";
         return SEM_ESTATE;
     }
     Comm &c = *cp;
+    if (count < 1 || count > 2 || site < 0 || site >= kSites) {
+        err = "comm_allgather: bad count / site";
+        return SEM_EINVAL;
+    }
+    if (c.p2p) {
+        p2p_allgather_kernel<<<1, 32, 0, s>>>(c.peers, c.rank, c.nranks, site, slot_base, count,
+                                              c.timeout_ns, c.err_d);
+        CC(cudaGetLastError());
+        return SEM_OK;
+    }
     if (c.lw) {
         return loop_collective(c, slot_base, s, err, [&]() -> int {
             for (int q = 0; q < c.nranks; ++q) {
@@ -461,6 +706,13 @@ int comm_allgather(Comm *cp, double *slot_base, int count, cudaStream_t s, std::
 // Asynchronous NCCL failure of a peer / the network: polled by
 // the CG drivers while they wait for the device.
 int comm_poll(Comm *cp, std::string &err) {
+    if (cp && cp->p2p) {
+        if (cp->err_h && *reinterpret_cast<volatile unsigned *>(cp->err_h)) {
+            err = "peer-memory transport: a peer did not arrive within SEM_P2P_TIMEOUT_MS";
+            return SEM_ENCCL;
+        }
+        return SEM_OK;
+    }
     if (!cp || cp->lw || !cp->nccl) return SEM_OK;
     ncclResult_t ar = ncclSuccess;
     ncclResult_t r = ncclCommGetAsyncError(cp->nccl, &ar);
@@ -489,6 +741,15 @@ void comm_abort(Comm *cp) {
 void comm_free(Comm *c) {
     if (!c) return;
     if (c->nccl) ncclCommDestroy(c->nccl);
+    if (c->p2p) {
+        cudaDeviceSynchronize();     // no peer kernel may still target a window being freed
+        for (void *ptr : c->ipc_opened) cudaIpcCloseMemHandle(ptr);
+        cudaFree(c->win);
+        cudaFree(c->slot_rank);
+        cudaFree(c->slot_off);
+        cudaFree(c->plist);
+        if (c->err_h) cudaFreeHost(c->err_h);
+    }
     if (c->lw) {
         // the events belong to the world: a peer still leaving its last
         // collective may wait on them after this rank is gone

@@ -49,13 +49,16 @@ int comm_setup(Comm *&c, const sem_mesh *mesh, const ExchangePlan &ep, const Dev
 // copy).  nlaunch receives the kernel count.
 int comm_exchange(Comm *c, const DevMesh &m, double *w, cudaStream_t s, int64_t &nlaunch,
                   std::string &err);
-// In-place all-gather of one double per rank at slot_base[0..nranks).
-int comm_allgather_scalar(Comm *c, double *slot_base, cudaStream_t s, std::string &err);
-// `count` doubles per rank, rank-major at slot_base (in place)
-int comm_allgather(Comm *c, double *slot_base, int count, cudaStream_t s, std::string &err);
+// All-gather sites (one epoch counter and slot set each in the peer-memory
+// transport): the interface exchange and the CG scalars.
+enum { kSiteExchange = 0, kSitePap = 1, kSiteRr = 2, kSiteRz = 3, kSiteSr = 4, kSites = 5 };
+// `count` (<= 2) doubles per rank, rank-major at slot_base (in place)
+int comm_allgather(Comm *c, double *slot_base, int count, int site, cudaStream_t s, std::string &err);
 void comm_free(Comm *c);
 // false for the loopback transport (its host rendezvous cannot be graph-captured)
 bool comm_capturable(const Comm *c);
+// true for the peer-memory transport (its collectives spin on the device)
+bool comm_device_only(const Comm *c);
 // SEM_ENCCL (with a message) if the communicator reported an asynchronous error
 int comm_poll(Comm *c, std::string &err);
 // abort after a failure (cancels pending NCCL work); wakes loopback peers

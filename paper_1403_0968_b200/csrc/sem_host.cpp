@@ -82,6 +82,7 @@ static int fail(sem_ctx *c, int code, const char *fmt, ...) {
 
 struct sem_ctx;
 static cudaEvent_t prof_event(sem_ctx *ctx);
+static int build_cg_graph(sem_ctx *ctx);
 static void prof_fold(sem_ctx *ctx, int iters);
 
 #define CU(call)                                                                     \
@@ -661,6 +662,24 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
             CU(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
             CU(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
         }
+        // peer-memory transport: capture, instantiate and upload the chunk
+        // graphs of every method now, while no collective is in flight -- a
+        // later instantiation could stall on a peer's spinning kernel when
+        // several ranks share a device (include/sem.h)
+        if (ctx->nranks > 1 && comm_device_only(ctx->comm) && ctx->use_graph) {
+            const bool tma_like = dm.use_tma || dm.use_hi;
+            for (int meth = 0; meth < 3; ++meth) {
+                if (meth == 2 && (!tma_like || dm.H)) continue;     // (sem_cg_sr's limits)
+                ctx->method = meth;
+                cv.dinv = (meth == 1) ? ctx->dinv_buf : nullptr;
+                int brc = build_cg_graph(ctx);
+                if (brc) return brc;
+                CU(cudaGraphUpload(ctx->graph_exec[meth], s));
+            }
+            cv.dinv = nullptr;
+            ctx->method = 0;
+            CU(cudaStreamSynchronize(s));
+        }
         return SEM_OK;
     }();
     if (rc) {
@@ -768,8 +787,28 @@ static int dssum_impl(sem_ctx *ctx, double *w, int mode, int k, cudaStream_t s) 
     return SEM_OK;
 }
 
+// A failed collective of the peer-memory transport (a spin that timed out)
+// is sticky: every later collective of the context reports it.
+static int transport_ok(sem_ctx *ctx) {
+    if (ctx->nranks == 1 || !ctx->comm) return SEM_OK;
+    std::string cerr;
+    if (comm_poll(ctx->comm, cerr)) {
+        ctx->broken = true;
+        return fail(ctx, SEM_ENCCL, "%s", cerr.c_str());
+    }
+    return SEM_OK;
+}
+
+extern "C" int sem_status(sem_ctx *ctx) {
+    if (!ctx) return fail(nullptr, SEM_ESTATE, "NULL context");
+    int rc = transport_ok(ctx);
+    if (rc) return rc;
+    return ctx->broken ? SEM_ECUDA : SEM_OK;
+}
+
 extern "C" int sem_dssum(sem_ctx *ctx, double *w) {
     CHECK_CTX();
+    if (int rc = transport_ok(ctx)) return rc;
     if (!w || !aligned16(w)) return fail(ctx, SEM_EINVAL, "sem_dssum: bad pointer");
     return dssum_impl(ctx, w, 0, -1, ctx->stream);
 }
@@ -791,10 +830,12 @@ extern "C" int sem_mass(sem_ctx *ctx, const double *f, double *b) {
 // ---------------------------------------------------------------------------
 // a9: CG driver
 // ---------------------------------------------------------------------------
-static int allgather_scalar(sem_ctx *ctx, double *slot_base, cudaStream_t s) {
+// site: which all-gather of the iteration (kSitePap / kSiteRr / kSiteRz; the
+// peer-memory transport keeps one epoch counter and slot set per site)
+static int allgather_scalar(sem_ctx *ctx, double *slot_base, int site, cudaStream_t s) {
     if (ctx->nranks == 1) return SEM_OK;
     std::string cerr;
-    int rc = comm_allgather_scalar(ctx->comm, slot_base, s, cerr);
+    int rc = comm_allgather(ctx->comm, slot_base, 1, site, s, cerr);
     if (rc) return fail(ctx, rc, "%s", cerr.c_str());
     return SEM_OK;
 }
@@ -842,7 +883,7 @@ static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
         if (P > 1) {
             LAUNCH(launch_cg_red_pap(ctx->dm, v, s));
             CU(cudaStreamWaitEvent(s, ctx->join_ev, 0));
-            if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P, s))) return rc;
+            if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P, kSitePap, s))) return rc;
         }
     } else {
         LAUNCHP(kProfAxCg, k1_bpn * ctx->L, k, launch_ax_cg(ctx->dm, v, s));
@@ -850,16 +891,16 @@ static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
         if (P > 1) {
             if ((rc = exchange_impl(ctx, v.w, s))) return rc;
             LAUNCH(launch_cg_red_pap(ctx->dm, v, s));
-            if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P, s))) return rc;
+            if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P, kSitePap, s))) return rc;
         }
     }
     LAUNCHP(kProfK2, k2_bytes(ctx), k, launch_k2(ctx->dm, v, false, s));
     if (P > 1) {
         LAUNCH(launch_cg_red_rr(ctx->dm, v, s));
-        if ((rc = allgather_scalar(ctx, v.rr_all + ((k + 1) & 3) * P, s))) return rc;
+        if ((rc = allgather_scalar(ctx, v.rr_all + ((k + 1) & 3) * P, kSiteRr, s))) return rc;
         if (v.dinv) {
             LAUNCH(launch_cg_red_rz(ctx->dm, v, s));
-            if ((rc = allgather_scalar(ctx, v.rz_all + ((k + 1) & 3) * P, s))) return rc;
+            if ((rc = allgather_scalar(ctx, v.rz_all + ((k + 1) & 3) * P, kSiteRz, s))) return rc;
         }
     }
     return SEM_OK;
@@ -883,7 +924,7 @@ static int enqueue_iteration_sr(sem_ctx *ctx, int k, cudaStream_t s) {
         if ((rc = exchange_impl(ctx, v.w, s))) return rc;
         LAUNCH(launch_sr_fold(ctx->dm, v, s));
         std::string cerr;
-        rc = comm_allgather(ctx->comm, v.rr_all + (k & 3) * 2 * P, 2, s, cerr);
+        rc = comm_allgather(ctx->comm, v.rr_all + (k & 3) * 2 * P, 2, kSiteSr, s, cerr);
         if (rc) return fail(ctx, rc, "%s", cerr.c_str());
     }
     LAUNCHP(kProfK2, kb_bytes(ctx), k, launch_kb_sr(ctx->dm, v, s));
@@ -1042,6 +1083,7 @@ static int run_chunks(sem_ctx *ctx, int maxit, cudaGraphExec_t gexec, cudaStream
 static int cg_sr_impl(sem_ctx *ctx, const double *b, double *x, double tol, int maxit,
                       int *iters, double *rel_res) {
     if (!b || !x || !aligned16(b) || !aligned16(x)) return fail(ctx, SEM_EINVAL, "sem_cg_sr: bad pointer");
+    if (int rc = transport_ok(ctx)) return rc;
     if (!(tol >= 0.0) || maxit < 0) return fail(ctx, SEM_EINVAL, "sem_cg_sr: tol >= 0 and maxit >= 0 required");
     if (!ctx->dm.use_tma && !ctx->dm.use_hi)
         return fail(ctx, SEM_EINVAL, "sem_cg_sr: needs the TMA / high-order Ax kernels (not SEM_AX_KERNEL=simple)");
@@ -1072,6 +1114,7 @@ static int cg_sr_impl(sem_ctx *ctx, const double *b, double *x, double tol, int 
     CU(cudaMemcpyAsync(&ctx->host_state[0], v.st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     const CgState &hs = ctx->host_state[0];
+    if (int rc = transport_ok(ctx)) return rc;
     if (!hs.done) return fail(ctx, SEM_ECUDA, "sem_cg_sr: device did not reach a stopping decision");
     if (ctx->prof) prof_fold(ctx, hs.iters);
     if (iters) *iters = hs.iters;
@@ -1086,6 +1129,7 @@ static int cg_sr_impl(sem_ctx *ctx, const double *b, double *x, double tol, int 
 static int cg_impl(sem_ctx *ctx, int precond, const double *b, double *x, double tol, int maxit,
                    int *iters, double *rel_res) {
     if (!b || !x || !aligned16(b) || !aligned16(x)) return fail(ctx, SEM_EINVAL, "sem_cg: bad pointer");
+    if (int rc = transport_ok(ctx)) return rc;
     if (!(tol >= 0.0) || maxit < 0) return fail(ctx, SEM_EINVAL, "sem_cg: tol >= 0 and maxit >= 0 required");
     cudaStream_t s = ctx->stream;
     CgVecs &v = ctx->cv;
@@ -1111,10 +1155,10 @@ static int cg_impl(sem_ctx *ctx, int precond, const double *b, double *x, double
     LAUNCH(launch_k2(ctx->dm, v, true, s));
     if (P > 1) {
         LAUNCH(launch_cg_red_rr(ctx->dm, v, s));
-        if ((rc = allgather_scalar(ctx, v.rr_all + 0 * P, s))) return rc;
+        if ((rc = allgather_scalar(ctx, v.rr_all + 0 * P, kSiteRr, s))) return rc;
         if (v.dinv) {
             LAUNCH(launch_cg_red_rz(ctx->dm, v, s));
-            if ((rc = allgather_scalar(ctx, v.rz_all + 0 * P, s))) return rc;
+            if ((rc = allgather_scalar(ctx, v.rz_all + 0 * P, kSiteRz, s))) return rc;
         }
     }
 
@@ -1125,6 +1169,7 @@ static int cg_impl(sem_ctx *ctx, int precond, const double *b, double *x, double
     CU(cudaMemcpyAsync(&ctx->host_state[0], v.st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     const CgState &hs = ctx->host_state[0];
+    if (int rc = transport_ok(ctx)) return rc;
     if (!hs.done) return fail(ctx, SEM_ECUDA, "sem_cg: device did not reach a stopping decision");
     if (ctx->prof) prof_fold(ctx, hs.iters);
     if (iters) *iters = hs.iters;

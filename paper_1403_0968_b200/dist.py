@@ -111,6 +111,12 @@ class LoopbackRank:
     def allgather_fn(self):
         return self.group._allgather_fn(self.rank)
 
+    def barrier(self):
+        """Host rendezvous of all ranks of the group (e.g. after a warm-up,
+        before the first device-side collective of the peer-memory
+        transport)."""
+        self.group._barrier.wait()
+
 
 class LoopbackGroup:
     """P in-process ranks on one device (test transport).  ``run(fn)`` calls

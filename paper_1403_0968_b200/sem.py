@@ -43,7 +43,7 @@ class SemMesh(ctypes.Structure):
 EXPORTS = ["sem_version", "sem_gll", "sem_workspace_bytes", "sem_setup", "sem_sizes",
            "sem_ax", "sem_dssum", "sem_mask", "sem_mass", "sem_cg", "sem_launch_count",
            "sem_free", "sem_strerror", "sem_last_error", "sem_nccl_id_bytes",
-           "sem_nccl_get_unique_id", "sem_loopback_unique_id", "sem_profile", "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan",
+           "sem_nccl_get_unique_id", "sem_loopback_unique_id", "sem_profile", "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan", "sem_status",
            "sem_pcg", "sem_diag", "sem_cg_sr", "fd_weights", "fd2d_step", "fd2d_run", "fd2d_run_ex"]
 
 # preconditioners of sem_pcg (include/sem.h enum sem_precond)
@@ -86,6 +86,8 @@ def lib():
     L.sem_diag.argtypes = [P, P]
     L.sem_cg_sr.argtypes = [P, P, P, ctypes.c_double, ctypes.c_int,
                             ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
+    L.sem_status.argtypes = [P]
+    L.sem_status.restype = ctypes.c_int
     L.sem_launch_count.argtypes = [P]
     L.sem_launch_count.restype = i64
     L.sem_free.argtypes = [P]
@@ -299,6 +301,10 @@ class Context:
         """Enqueue `reps` back-to-back launches of one CG kernel as one graph on
         the context stream (benchmark helper; internal CG state left undefined)."""
         _check(lib().sem_kernel_replay(self._ctx, self.KERNELS[which], int(reps)), self._ctx)
+
+    def status(self):
+        """Raise the context's sticky error (sem_status), if any."""
+        _check(lib().sem_status(self._ctx), self._ctx)
 
     @property
     def launch_count(self) -> int:

@@ -22,7 +22,7 @@ static const fnp exported[] = {
     (fnp)sem_cg, (fnp)sem_pcg, (fnp)sem_cg_sr, (fnp)sem_diag,
     (fnp)sem_nccl_id_bytes, (fnp)sem_nccl_get_unique_id, (fnp)sem_loopback_unique_id,
     (fnp)sem_profile, (fnp)sem_kernel_replay, (fnp)sem_profile_read,
-    (fnp)sem_exchange_plan, (fnp)sem_launch_count, (fnp)sem_free, (fnp)sem_strerror,
+    (fnp)sem_exchange_plan, (fnp)sem_status, (fnp)sem_launch_count, (fnp)sem_free, (fnp)sem_strerror,
     (fnp)sem_last_error, (fnp)fd_weights, (fnp)fd2d_step, (fnp)fd2d_run,
     (fnp)fd2d_run_ex};
 

@@ -19,6 +19,9 @@ Bars:
   every rank reporting the same count, residual and nglobal.
 Inputs: meshgen boxes partitioned as 1x1x2 / 1x2x2 / 2x2x2 blocks (c5's
 partition), the oracle's GLL nodes; no expected value comes from the CUDA path.
+
+The peer-memory transport (SEM_COMM=p2p) runs the same checks in a fresh
+process: tests/test_gpu_p2p.py.
 """
 import numpy as np
 import pytest
@@ -29,6 +32,11 @@ from paper_1403_0968_b200 import meshgen
 pytestmark = pytest.mark.gpu
 
 torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(autouse=True)
+def host_transport(monkeypatch):
+    monkeypatch.delenv("SEM_COMM", raising=False)
 
 
 @pytest.fixture(scope="module")
