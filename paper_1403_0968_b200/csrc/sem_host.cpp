@@ -679,6 +679,11 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
             cv.dinv = nullptr;
             ctx->method = 0;
             CU(cudaStreamSynchronize(s));
+            // no rank leaves setup while another is still capturing (a
+            // device-wide synchronisation elsewhere would invalidate it)
+            int one = 1, all[kMaxRanks];
+            if (mesh->allgather(mesh->allgather_user, &one, sizeof one, all) != 0)
+                return fail(ctx, SEM_ENCCL, "setup all-gather (graph capture) failed");
         }
         return SEM_OK;
     }();

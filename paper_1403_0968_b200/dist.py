@@ -180,7 +180,9 @@ class LoopbackGroup:
             t.start()
         for t in th:
             t.join()
-        for e in errs:
-            if e is not None:
-                raise e
+        # the root cause first: peers of a failed rank see a broken barrier
+        first = [e for e in errs if e is not None and not isinstance(e, threading.BrokenBarrierError)]
+        first += [e for e in errs if e is not None]
+        if first:
+            raise first[0]
         return out
