@@ -122,3 +122,52 @@ def test_c3_exact_counts_at_wide_margin(c3, oracle_runs, gpu_hist, meth):
         _, its, rel, ok = gpu_cg(ctx, bd, meth, tol, 5000)
         assert ok and its == k, (meth, tol, k, marg, its, rel)
     print(f"{meth}: exact counts at {[(f'{t:.3e}', k, round(mg, 4)) for t, k, mg in picks]}")
+
+
+@pytest.mark.parametrize("P", [2, 8])
+def test_c3_partitioned_over_loopback_ranks(c3, oracle_runs, gpu_hist, monkeypatch, P):
+    """The headline mesh split over P in-process ranks (the c5 block partition
+    of the 16^3 element grid, boundary elements first, the K1 split and the
+    interface exchange active; host-rendezvous loopback transport): CG to
+    1e-8 under the same drift rule against the same oracle history, x within
+    1e-9 of the oracle's on every rank."""
+    from paper_1403_0968_b200 import dist as sdist
+    from paper_1403_0968_b200 import sem
+    monkeypatch.delenv("SEM_COMM", raising=False)
+    m, G, b, ctx = c3
+    xr, its_r, _, hist = oracle_runs["cg"]
+    N, n3 = 7, 512
+    xi, _ = oracle.gll(N)
+    parts = meshgen.default_parts(P)
+    ranks = [meshgen.box_mesh(N, xi, elems=(16, 16, 16), eps=0.05, parts=parts, rank=r,
+                              boundary_first=True) for r in range(P)]
+    pos = [mr.eidx[:, 0] + 16 * (mr.eidx[:, 1] + 16 * mr.eidx[:, 2]) for mr in ranks]
+    bfull = b.reshape(-1, n3)
+    xr = xr.reshape(-1, n3)
+
+    picks = _margin.wide_margin_tols(hist, gpu_hist["cg"], count=3)
+
+    def body(lr):
+        c = sem.Context(ranks[lr.rank], N, device=0, loopback=lr)
+        try:
+            bb = torch.from_numpy(bfull[pos[lr.rank]].reshape(-1)).cuda()
+            x, its, rel, ok = c.cg(bb, tol=1e-8, maxit=5000)
+            wide = [c.cg(bb, tol=t, maxit=5000)[1] for t, _, _ in picks]
+            return x.cpu().numpy(), its, rel, ok, wide
+        finally:
+            c.free()
+
+    out = sdist.LoopbackGroup(P, device=0).run(body)
+    # EXACT counts where the oracle's stop has a wide margin
+    for r in range(P):
+        assert out[r][4] == [k for _, k, _ in picks], (r, out[r][4], picks)
+    its0 = out[0][1]
+    for r, (x, its, rel, ok, _) in enumerate(out):
+        assert ok and its == its0 and rel == out[0][2]
+        xe = xr[pos[r]].reshape(-1)
+        assert np.linalg.norm(x - xe) / np.linalg.norm(xe) <= 1e-9
+    # the count under the drift rule: the one-rank GPU history bounds the drift
+    # of the same recurrence; the partitioned solve sums its dot products in
+    # another order, so its own drift is measured at the crossing
+    _margin.assert_count(its0, its_r, _margin.margin(hist, its_r, 1e-8),
+                         max(_margin.C3_DRIFT_MAX["cg"], 0.0), (P,))
