@@ -722,6 +722,12 @@ def main():
                          "kernel": k1_name,
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
+                         # DRAM bytes per launch (ncu, cold cache) over the in-graph
+                         # launch time: frac above 1 means algorithmic bytes served
+                         # from L2 (r written by the previous K2, x / p by the
+                         # previous K1), this is the DRAM side of the same launch
+                         "dram_frac": (traffic / (k1_in_solve_us * 1e-6) / 1e9 / peak
+                                       if traffic and k1_in_solve_us else None),
                          "peak_source": peak_src,
                          "bytes_per_node": f"{bpn_k1:.0f} (x,r,p,G{',H' if alpha is not None else ''} "
                                            "read; x,p,w write)",
