@@ -877,15 +877,16 @@ static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
         const int gA = ax_cg_range_blocks(m, nb);
         LAUNCHP(kProfAxCg, k1_bpn * m.n3 * nb, k, launch_ax_cg_range(m, v, 0, nb, 0, s));
         ctx->launches += m.use_k1ax ? 1 : 0;
-        if (P > 1) {
-            CU(cudaEventRecord(ctx->fork_ev, s));
-            CU(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
-            if ((rc = exchange_impl(ctx, v.w, ctx->side))) return rc;
-            CU(cudaEventRecord(ctx->join_ev, ctx->side));
-        }
+        if (P > 1) CU(cudaEventRecord(ctx->fork_ev, s));
+        // the interior launch is enqueued before the exchange: a transport
+        // whose enqueue blocks the host (the loopback rendezvous) must not
+        // hold it back (profiles/overlap_r02.md)
         LAUNCHP(kProfAxCg, k1_bpn * m.n3 * ni, k, launch_ax_cg_range(m, v, nb, ni, gA, s));
         ctx->launches += m.use_k1ax ? 1 : 0;
         if (P > 1) {
+            CU(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
+            if ((rc = exchange_impl(ctx, v.w, ctx->side))) return rc;
+            CU(cudaEventRecord(ctx->join_ev, ctx->side));
             LAUNCH(launch_cg_red_pap(ctx->dm, v, s));
             CU(cudaStreamWaitEvent(s, ctx->join_ev, 0));
             if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P, kSitePap, s))) return rc;

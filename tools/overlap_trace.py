@@ -74,46 +74,44 @@ def traced():
 
 events = kernel_trace.trace(traced, export=args.out + ".trace.json")
 runner.join()
-# classify, then per rank and iteration: the exchange kernels (pack / sync /
-# combine, on the rank's side branch) against that rank's interior K1.  With
-# CUDA graphs (p2p) CUPTI reports the boundary K1 and the side branch on the
-# rank's stream and the interior K1 on a graph-branch stream; a rank's
-# interior K1 is the first K1 off the main streams that starts when its
-# boundary K1 has ended.
+# classify; each exchange kernel (pack / sync / combine) of an iteration is
+# paired with the interior K1 it was forked beside: the latest LONG K1 launch
+# (the interior range, >= 60% of the longest K1) that started before the
+# rank's pack.  CUPTI's stream ids of graph nodes are not stable enough to
+# tell the ranks apart, but the ranks' iterations alternate on the shared
+# GPU, so "latest interior K1 before this pack" is the same rank's.
 rows = []
 for name, t0, d, sid in events:
     c = kernel_trace.classify(name)
+    nm = name.split("(")[0].replace("sem::", "")
     kind = ("k1" if c == "k1" else
-            "ex" if any(k in name for k in ("pack_kernel", "p2p_sync", "combine_kernel")) else "o")
-    rows.append({"kind": kind, "name": name.split("(")[0].replace("sem::", "")[-30:], "t0": t0,
-                 "t1": t0 + d, "s": sid})
+            "pack" if "pack_kernel" in nm else "sync" if "p2p_sync" in nm else
+            "combine" if "combine_kernel" in nm else "o")
+    rows.append({"kind": kind, "t0": t0, "t1": t0 + d})
 rows.sort(key=lambda r: r["t0"])
 k1s = [r for r in rows if r["kind"] == "k1"]
-cnt = {}
-mains = {}
-for r in k1s:
-    mains[r["s"]] = mains.get(r["s"], 0) + 1
-main_ids = sorted(mains, key=lambda s: -mains[s])[:P]
-n_ex, t_ex, t_in = {}, {}, {}
-for b in [r for r in k1s if r["s"] not in main_ids] or k1s[1::2]:
-    bnd = [r for r in k1s if r["s"] in main_ids and r["t1"] <= b["t0"] + 1.0 and r is not b]
-    if not bnd:
+longest = max(r["t1"] - r["t0"] for r in k1s)
+interior = [r for r in k1s if r["t1"] - r["t0"] >= 0.6 * longest]
+stats = {k: [0, 0.0, 0.0] for k in ("pack", "sync", "combine")}
+for i, r in enumerate(rows):
+    if r["kind"] != "pack":
         continue
-    a = bnd[-1]
-    nxt = [r for r in k1s if r["s"] == a["s"] and r["t0"] > a["t0"] and r is not b]
-    tend = nxt[0]["t0"] if nxt else 1e18
-    for r in rows:
-        if r["kind"] != "ex" or not (a["t1"] - 0.5 <= r["t0"] < tend):
-            continue
-        if r["s"] in main_ids and r["s"] != a["s"]:
-            continue
-        nm = r["name"]
-        n_ex[nm] = n_ex.get(nm, 0) + 1
-        t_ex[nm] = t_ex.get(nm, 0.0) + r["t1"] - r["t0"]
-        t_in[nm] = t_in.get(nm, 0.0) + max(0.0, min(r["t1"], b["t1"]) - max(r["t0"], b["t0"]))
+    cands = [b for b in interior if b["t0"] <= r["t0"] + 0.5]
+    if not cands:
+        continue
+    b = cands[-1]
+    # this pack and the sync / combine that follow it on the same side branch
+    grp = [r] + [q for q in rows[i + 1:i + 12] if q["kind"] in ("sync", "combine")][:2]
+    for q in grp:
+        st = stats[q["kind"]]
+        st[0] += 1
+        st[1] += q["t1"] - q["t0"]
+        st[2] += max(0.0, min(q["t1"], b["t1"]) - max(q["t0"], b["t0"]))
 out = {"config": f"c3 over P={P} loopback ranks on one GPU, transport "
                  f"{os.environ.get('SEM_COMM', 'host')}",
-       "exchange_kernels": {k: {"launches": n_ex[k], "mean_us": t_ex[k] / n_ex[k],
-                                "fraction_inside_interior_k1": t_in[k] / t_ex[k]} for k in n_ex}}
+       "interior_k1_mean_us": sum(b["t1"] - b["t0"] for b in interior) / max(len(interior), 1),
+       "exchange_kernels": {k: {"launches": v[0], "mean_us": v[1] / max(v[0], 1),
+                                "fraction_inside_interior_k1": v[2] / v[1] if v[1] else None}
+                            for k, v in stats.items()}}
 json.dump(out, open(args.out + ".json", "w"), indent=1)
 print(json.dumps(out))
