@@ -18,6 +18,7 @@
 #include <cstring>
 
 #include "cg_device.cuh"
+#include "p2p_dev.cuh"
 #include "sem_internal.h"
 
 namespace sem {
@@ -235,20 +236,30 @@ __global__ void sr_finish_kernel(const __grid_constant__ GsClasses cls, const in
 }
 
 // nranks > 1: this rank's (gamma_k, delta_k) into sr_all[k & 3][rank] before
-// the one all-gather of the iteration (k from KA(k): st->k2)
+// the one all-gather of the iteration (k from KA(k): st->k2); with the
+// peer-memory transport (p2p != nullptr) this kernel also performs the
+// all-gather of the (gamma, delta) pair (warp 0), even after the stop
 constexpr int kFoldThreads = 256;
 __global__ void __launch_bounds__(kFoldThreads) sr_fold_kernel(CgRed R, double *sr_all, const CgState *st,
-                                                               int rank) {
+                                                               int rank, const P2PDev *p2p) {
     __shared__ double sred[2 * (kFoldThreads / 32)];
-    if (ld_state(&st->done)) return;
+    const bool done = ld_state(&st->done);
     const int k = ld_state(&st->k2);
-    double v[2];
-    v[0] = thread_sum<kFoldThreads>(R.part2 + ((k - 1) & 1) * R.s2, R.nb2);
-    v[1] = thread_sum<kFoldThreads>(R.part1 + (k & 1) * R.s1, R.nb1);
-    block_sum_vec<kFoldThreads, 2>(v, sred);
-    if (threadIdx.x == 0) {
-        sr_all[(k & 3) * 2 * R.nranks + 2 * rank] = v[0];
-        sr_all[(k & 3) * 2 * R.nranks + 2 * rank + 1] = v[1];
+    if (!done) {
+        double v[2];
+        v[0] = thread_sum<kFoldThreads>(R.part2 + ((k - 1) & 1) * R.s2, R.nb2);
+        v[1] = thread_sum<kFoldThreads>(R.part1 + (k & 1) * R.s1, R.nb1);
+        block_sum_vec<kFoldThreads, 2>(v, sred);
+        if (threadIdx.x == 0) {
+            sr_all[(k & 3) * 2 * R.nranks + 2 * rank] = v[0];
+            sr_all[(k & 3) * 2 * R.nranks + 2 * rank + 1] = v[1];
+        }
+    } else if (!p2p) {
+        return;
+    }
+    if (p2p) {
+        __syncthreads();
+        if (threadIdx.x < 32) p2p_allgather_warp(*p2p, kSiteSr, sr_all + (k & 3) * 2 * R.nranks, 2);
     }
 }
 
@@ -330,10 +341,10 @@ cudaError_t launch_sr_finish(const DevMesh &m, const CgVecs &v, cudaStream_t s) 
     return cudaGetLastError();
 }
 
-cudaError_t launch_sr_fold(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
+cudaError_t launch_sr_fold(const DevMesh &m, const CgVecs &v, const P2PDev *p2p, cudaStream_t s) {
     CgRed R = make_red(m, v);
     R.nb1 = ka_blocks(m);
-    sr_fold_kernel<<<1, kFoldThreads, 0, s>>>(R, v.rr_all, v.st, m.rank);
+    sr_fold_kernel<<<1, kFoldThreads, 0, s>>>(R, v.rr_all, v.st, m.rank, p2p);
     return cudaGetLastError();
 }
 

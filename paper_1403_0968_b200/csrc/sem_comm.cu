@@ -12,6 +12,7 @@
 #include <thread>
 
 #include "cg_device.cuh"
+#include "p2p_dev.cuh"
 #include "sem_comm.h"
 
 namespace sem {
@@ -199,44 +200,6 @@ static bool loop_barrier(LoopWorld &w) {
 // Spins time out (SEM_P2P_TIMEOUT_MS) and raise a host-mapped error flag,
 // after which every later spin of the context fails at once.
 // ---------------------------------------------------------------------------
-struct P2PHead {
-    unsigned long long flags[kSites][kMaxRanks];   // flags[site][q]: last epoch rank q signalled here
-    unsigned long long ctr[kSites];                 // this rank's epoch per site
-    double scal[kSites][2][2 * kMaxRanks];          // all-gather slots [site][parity][rank * count + c]
-};
-struct P2PPeers {
-    P2PHead *head[kMaxRanks];                       // every rank's window header (own included)
-    double *recv[2][kMaxRanks];                     // every rank's exchange receive areas
-};
-
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long global_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-// spin until *flag >= e (acquire); false on timeout (error flag raised)
-__device__ __forceinline__ bool p2p_wait(const unsigned long long *flag, unsigned long long e,
-                                         unsigned long long timeout_ns, unsigned *err) {
-    const unsigned long long t0 = global_ns();
-    while (ld_acquire_sys(flag) < e) {
-        // after a first timeout every later collective fails fast
-        if (*reinterpret_cast<volatile unsigned *>(err)) return false;
-        if (global_ns() - t0 > timeout_ns) {
-            atomicExch(err, 1u);
-            return false;
-        }
-    }
-    return true;
-}
-
 struct Comm {
     ncclComm_t nccl = nullptr;
     // peer-memory transport (SEM_COMM=p2p)
@@ -248,6 +211,7 @@ struct Comm {
     int64_t *slot_off = nullptr;         // ... and offset in its receive area
     int32_t *plist = nullptr;            // neighbour ranks (device)
     unsigned *err_h = nullptr, *err_d = nullptr;   // host-mapped timeout flag
+    P2PDev *dev = nullptr;               // device copy of peers / rank / timeout (fused folds)
     unsigned long long timeout_ns = 0;
     LoopWorld *lw = nullptr;             // loopback transport (tests) instead of NCCL
     std::string lw_key;
@@ -265,6 +229,7 @@ struct Comm {
 // transport (device work only) and NCCL can
 bool comm_capturable(const Comm *c) { return c && (!c->lw || c->p2p); }
 bool comm_device_only(const Comm *c) { return c && c->p2p; }
+const P2PDev *comm_p2p_dev(const Comm *c) { return (c && c->p2p) ? c->dev : nullptr; }
 
 __device__ __forceinline__ void group_loc(const GsClasses &cls, int g, int &m, int &cnt, int &q,
                                           int &off) {
@@ -346,30 +311,9 @@ __global__ void p2p_sync_kernel(const __grid_constant__ P2PPeers peers, int me, 
     for (int i = threadIdx.x; i < np; i += 32) p2p_wait(&mine->flags[site][plist[i]], e, timeout_ns, err);
 }
 
-// one warp: this rank's `count` values at slot_base[me * count ..] into every
-// peer's slots, flags, then every peer's values (acquired) into slot_base
-__global__ void p2p_allgather_kernel(const __grid_constant__ P2PPeers peers, int me, int P, int site,
-                                     double *slot_base, int count, unsigned long long timeout_ns,
-                                     unsigned *err) {
-    P2PHead *mine = peers.head[me];
-    const unsigned long long e = mine->ctr[site] + 1;
-    const int par = (int)(e & 1);
-    __syncwarp();
-    if (threadIdx.x == 0) mine->ctr[site] = e;
-    double v[2];
-    for (int c = 0; c < count; ++c) v[c] = slot_base[me * count + c];
-    for (int q = threadIdx.x; q < P; q += 32) {
-        if (q == me) continue;
-        for (int c = 0; c < count; ++c) peers.head[q]->scal[site][par][me * count + c] = v[c];
-    }
-    __threadfence_system();
-    for (int q = threadIdx.x; q < P; q += 32)
-        if (q != me) st_release_sys(&peers.head[q]->flags[site][me], e);
-    for (int q = threadIdx.x; q < P; q += 32) {
-        if (q == me) continue;
-        if (!p2p_wait(&mine->flags[site][q], e, timeout_ns, err)) continue;
-        for (int c = 0; c < count; ++c) slot_base[q * count + c] = mine->scal[site][par][q * count + c];
-    }
+// one warp: the all-gather of `site` (p2p_dev.cuh)
+__global__ void p2p_allgather_kernel(const P2PDev *d, int site, double *slot_base, int count) {
+    p2p_allgather_warp(*d, site, slot_base, count);
 }
 
 #define NC(call)                                                                    \
@@ -553,6 +497,16 @@ static int p2p_join(Comm &c, const sem_mesh *mesh, bool same_process, std::strin
     CC(cudaHostGetDevicePointer(&c.err_d, c.err_h, 0));
     const char *to = getenv("SEM_P2P_TIMEOUT_MS");
     c.timeout_ns = (unsigned long long)(to ? atoll(to) : 20000) * 1000000ull;
+    {
+        P2PDev hd{};
+        hd.peers = c.peers;
+        hd.me = me;
+        hd.P = P;
+        hd.timeout_ns = c.timeout_ns;
+        hd.err = c.err_d;
+        CC(cudaMalloc(&c.dev, sizeof(P2PDev)));
+        CC(cudaMemcpy(c.dev, &hd, sizeof hd, cudaMemcpyHostToDevice));
+    }
     // every rank's window is zeroed before anyone can signal into it
     int ok = 1, oks[kMaxRanks];
     if (mesh->allgather(mesh->allgather_user, &ok, sizeof ok, oks) != 0) {
@@ -683,8 +637,7 @@ int comm_allgather(Comm *cp, double *slot_base, int count, int site, cudaStream_
         return SEM_EINVAL;
     }
     if (c.p2p) {
-        p2p_allgather_kernel<<<1, 32, 0, s>>>(c.peers, c.rank, c.nranks, site, slot_base, count,
-                                              c.timeout_ns, c.err_d);
+        p2p_allgather_kernel<<<1, 32, 0, s>>>(c.dev, site, slot_base, count);
         CC(cudaGetLastError());
         return SEM_OK;
     }
@@ -748,6 +701,7 @@ void comm_free(Comm *c) {
         cudaFree(c->slot_rank);
         cudaFree(c->slot_off);
         cudaFree(c->plist);
+        cudaFree(c->dev);
         if (c->err_h) cudaFreeHost(c->err_h);
     }
     if (c->lw) {

@@ -51,7 +51,12 @@ int comm_exchange(Comm *c, const DevMesh &m, double *w, cudaStream_t s, int64_t 
                   std::string &err);
 // All-gather sites (one epoch counter and slot set each in the peer-memory
 // transport): the interface exchange and the CG scalars.
+// all-gather sites (as p2p_dev.cuh)
+#ifndef SEM_P2P_SITES
+#define SEM_P2P_SITES
 enum { kSiteExchange = 0, kSitePap = 1, kSiteRr = 2, kSiteRz = 3, kSiteSr = 4, kSites = 5 };
+#endif
+struct P2PDev;
 // `count` (<= 2) doubles per rank, rank-major at slot_base (in place)
 int comm_allgather(Comm *c, double *slot_base, int count, int site, cudaStream_t s, std::string &err);
 void comm_free(Comm *c);
@@ -59,6 +64,9 @@ void comm_free(Comm *c);
 bool comm_capturable(const Comm *c);
 // true for the peer-memory transport (its collectives spin on the device)
 bool comm_device_only(const Comm *c);
+// the peer-memory transport's device descriptor (nullptr for other transports):
+// rank folds that take it do their all-gather themselves (one kernel)
+const P2PDev *comm_p2p_dev(const Comm *c);
 // SEM_ENCCL (with a message) if the communicator reported an asynchronous error
 int comm_poll(Comm *c, std::string &err);
 // abort after a failure (cancels pending NCCL work); wakes loopback peers

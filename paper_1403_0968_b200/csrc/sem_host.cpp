@@ -845,6 +845,26 @@ static int allgather_scalar(sem_ctx *ctx, double *slot_base, int site, cudaStrea
     return SEM_OK;
 }
 
+// The rank fold of one CG scalar (which: 0 (p,Ap), 1 (r,r), 2 (r,z)) and its
+// all-gather: one kernel with the peer-memory transport (the fold does the
+// all-gather), else the fold, then the transport's all-gather.  wait_ev: an
+// event the all-gather must also wait for (the side-stream exchange).
+static int fold_allgather(sem_ctx *ctx, int which, double *slot_base, cudaStream_t s,
+                          cudaEvent_t wait_ev = nullptr) {
+    const P2PDev *p2p = comm_p2p_dev(ctx->comm);
+    if (which == 0) LAUNCH(launch_cg_red_pap(ctx->dm, ctx->cv, p2p, s));
+    else if (which == 1) LAUNCH(launch_cg_red_rr(ctx->dm, ctx->cv, p2p, s));
+    else LAUNCH(launch_cg_red_rz(ctx->dm, ctx->cv, p2p, s));
+    // (the join: everything after -- the NCCL all-gather, whose order on the
+    // one communicator must follow the exchange's, and K2 -- waits for the
+    // side-stream exchange; the fused p2p fold uses its own flags and runs
+    // concurrently with the exchange)
+    if (wait_ev) CU(cudaStreamWaitEvent(s, wait_ev, 0));
+    if (p2p) return SEM_OK;
+    static const int site[3] = {kSitePap, kSiteRr, kSiteRz};
+    return allgather_scalar(ctx, slot_base, site[which], s);
+}
+
 // Algorithmic bytes of one K2 launch: w copies read + r copies written at
 // surface nodes, r read once per non-Dirichlet group, and r read/write + w
 // read at element-interior nodes.
@@ -887,27 +907,20 @@ static int enqueue_iteration(sem_ctx *ctx, int k, cudaStream_t s) {
             CU(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
             if ((rc = exchange_impl(ctx, v.w, ctx->side))) return rc;
             CU(cudaEventRecord(ctx->join_ev, ctx->side));
-            LAUNCH(launch_cg_red_pap(ctx->dm, v, s));
-            CU(cudaStreamWaitEvent(s, ctx->join_ev, 0));
-            if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P, kSitePap, s))) return rc;
+            if ((rc = fold_allgather(ctx, 0, v.pap_all + (k & 3) * P, s, ctx->join_ev))) return rc;
         }
     } else {
         LAUNCHP(kProfAxCg, k1_bpn * ctx->L, k, launch_ax_cg(ctx->dm, v, s));
         ctx->launches += ctx->dm.use_k1ax ? 1 : 0;
         if (P > 1) {
             if ((rc = exchange_impl(ctx, v.w, s))) return rc;
-            LAUNCH(launch_cg_red_pap(ctx->dm, v, s));
-            if ((rc = allgather_scalar(ctx, v.pap_all + (k & 3) * P, kSitePap, s))) return rc;
+            if ((rc = fold_allgather(ctx, 0, v.pap_all + (k & 3) * P, s))) return rc;
         }
     }
     LAUNCHP(kProfK2, k2_bytes(ctx), k, launch_k2(ctx->dm, v, false, s));
     if (P > 1) {
-        LAUNCH(launch_cg_red_rr(ctx->dm, v, s));
-        if ((rc = allgather_scalar(ctx, v.rr_all + ((k + 1) & 3) * P, kSiteRr, s))) return rc;
-        if (v.dinv) {
-            LAUNCH(launch_cg_red_rz(ctx->dm, v, s));
-            if ((rc = allgather_scalar(ctx, v.rz_all + ((k + 1) & 3) * P, kSiteRz, s))) return rc;
-        }
+        if ((rc = fold_allgather(ctx, 1, v.rr_all + ((k + 1) & 3) * P, s))) return rc;
+        if (v.dinv && (rc = fold_allgather(ctx, 2, v.rz_all + ((k + 1) & 3) * P, s))) return rc;
     }
     return SEM_OK;
 }
@@ -928,10 +941,13 @@ static int enqueue_iteration_sr(sem_ctx *ctx, int k, cudaStream_t s) {
     LAUNCHP(kProfAxCg, 64.0 * ctx->L, k, launch_ax_dot(ctx->dm, v, s));
     if (P > 1) {
         if ((rc = exchange_impl(ctx, v.w, s))) return rc;
-        LAUNCH(launch_sr_fold(ctx->dm, v, s));
-        std::string cerr;
-        rc = comm_allgather(ctx->comm, v.rr_all + (k & 3) * 2 * P, 2, kSiteSr, s, cerr);
-        if (rc) return fail(ctx, rc, "%s", cerr.c_str());
+        const P2PDev *p2p = comm_p2p_dev(ctx->comm);
+        LAUNCH(launch_sr_fold(ctx->dm, v, p2p, s));     // (p2p: the all-gather inside)
+        if (!p2p) {
+            std::string cerr;
+            rc = comm_allgather(ctx->comm, v.rr_all + (k & 3) * 2 * P, 2, kSiteSr, s, cerr);
+            if (rc) return fail(ctx, rc, "%s", cerr.c_str());
+        }
     }
     LAUNCHP(kProfK2, kb_bytes(ctx), k, launch_kb_sr(ctx->dm, v, s));
     return SEM_OK;
@@ -1160,12 +1176,8 @@ static int cg_impl(sem_ctx *ctx, int precond, const double *b, double *x, double
     LAUNCH(launch_cg_init(ctx->dm, v, s));
     LAUNCH(launch_k2(ctx->dm, v, true, s));
     if (P > 1) {
-        LAUNCH(launch_cg_red_rr(ctx->dm, v, s));
-        if ((rc = allgather_scalar(ctx, v.rr_all + 0 * P, kSiteRr, s))) return rc;
-        if (v.dinv) {
-            LAUNCH(launch_cg_red_rz(ctx->dm, v, s));
-            if ((rc = allgather_scalar(ctx, v.rz_all + 0 * P, kSiteRz, s))) return rc;
-        }
+        if ((rc = fold_allgather(ctx, 1, v.rr_all + 0 * P, s))) return rc;
+        if (v.dinv && (rc = fold_allgather(ctx, 2, v.rz_all + 0 * P, s))) return rc;
     }
 
     cudaGraphExec_t gexec = nullptr;

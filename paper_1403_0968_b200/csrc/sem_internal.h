@@ -125,9 +125,12 @@ cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t
 cudaError_t launch_cg_finish(const DevMesh &m, const CgVecs &v, cudaStream_t s);
 // multi-rank: fold this rank's block partials (fixed order) into its slot of
 // pap_all / rr_all before the NCCL all-gather
-cudaError_t launch_cg_red_pap(const DevMesh &m, const CgVecs &v, cudaStream_t s);
-cudaError_t launch_cg_red_rr(const DevMesh &m, const CgVecs &v, cudaStream_t s);
-cudaError_t launch_cg_red_rz(const DevMesh &m, const CgVecs &v, cudaStream_t s);
+// (p2p: the peer-memory transport's descriptor -- the fold then also does the
+// all-gather; nullptr: fold only)
+struct P2PDev;
+cudaError_t launch_cg_red_pap(const DevMesh &m, const CgVecs &v, const P2PDev *p2p, cudaStream_t s);
+cudaError_t launch_cg_red_rr(const DevMesh &m, const CgVecs &v, const P2PDev *p2p, cudaStream_t s);
+cudaError_t launch_cg_red_rz(const DevMesh &m, const CgVecs &v, const P2PDev *p2p, cudaStream_t s);
 // single-reduction (Chronopoulos-Gear) CG, NEXT-3 (cg_update.cu, ax_tma_sr.cu).
 // Global storage: p, s and the x increment live once per global node of the
 // rank -- surface group g at slot g, element-interior node t at ngroups + t --
@@ -140,7 +143,8 @@ int ka_blocks(const DevMesh &m);                  // KA's grid = its partial cou
 cudaError_t launch_kb_sr(const DevMesh &m, const CgVecs &v, cudaStream_t s);    // KB
 cudaError_t launch_sr_init(const DevMesh &m, const CgVecs &v, cudaStream_t s);
 cudaError_t launch_sr_finish(const DevMesh &m, const CgVecs &v, cudaStream_t s);
-cudaError_t launch_sr_fold(const DevMesh &m, const CgVecs &v, cudaStream_t s);  // nranks > 1
+cudaError_t launch_sr_fold(const DevMesh &m, const CgVecs &v, const P2PDev *p2p,
+                           cudaStream_t s);  // nranks > 1
 // Jacobi preconditioner (NEXT-2): d = diag(A_L) per local node (unassembled;
 // kappa-folded G^ + the mass term H); then, after Q Q^T d, dinv = 1 / d
 // (the caller masks it)

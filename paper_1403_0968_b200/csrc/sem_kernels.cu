@@ -10,6 +10,7 @@
 #include <cstdio>
 
 #include "cg_device.cuh"
+#include "p2p_dev.cuh"
 #include "sem_internal.h"
 
 namespace sem {
@@ -416,19 +417,32 @@ __global__ void cg_init_kernel(int64_t L, CgState *st, const double *__restrict_
 
 // Multi-rank: this rank's value = ordered sum of its block partials, into its
 // slot of the all-gather buffer (slot k & 3 for (p,Ap)_k, k_next & 3 for rho).
+// With the peer-memory transport (p2p != nullptr) the same kernel then does
+// the all-gather itself (warp 0, p2p_dev.cuh): the fold and the collective in
+// one launch.  After the stop the fold is skipped but the all-gather still
+// runs (every rank's epochs stay in step).
 constexpr int kRedThreads = 256;
 __global__ void __launch_bounds__(kRedThreads) cg_red_kernel(const double *part, int s, int nb,
                                                              double *all, const CgState *st,
-                                                             int which, int rank, int nranks) {
+                                                             int which, int rank, int nranks,
+                                                             const P2PDev *p2p, int site) {
     __shared__ double sred[kRedThreads / 32];
-    if (ld_state(&st->done)) return;
+    const bool done = ld_state(&st->done);
     // (p,Ap): K1 of iteration k = st->k2.  rho: K2 of iteration k1 - 1 (k1 = k_next).
     const int kk = (which == 0) ? ld_state(&st->k2) : ld_state(&st->k1);
-    const double *src = part + ((which == 0 ? kk : kk - 1) & 1) * s;
-    double v = 0.0;
-    for (int t = threadIdx.x; t < nb; t += kRedThreads) v += __ldcg(src + t);
-    v = block_sum<kRedThreads>(v, sred);
-    if (threadIdx.x == 0) all[(kk & 3) * nranks + rank] = v;
+    if (!done) {
+        const double *src = part + ((which == 0 ? kk : kk - 1) & 1) * s;
+        double v = 0.0;
+        for (int t = threadIdx.x; t < nb; t += kRedThreads) v += __ldcg(src + t);
+        v = block_sum<kRedThreads>(v, sred);
+        if (threadIdx.x == 0) all[(kk & 3) * nranks + rank] = v;
+    } else if (!p2p) {
+        return;
+    }
+    if (p2p) {
+        __syncthreads();
+        if (threadIdx.x < 32) p2p_allgather_warp(*p2p, site, all + (kk & 3) * nranks, 1);
+    }
 }
 
 // K1, first half, of the split schedule (use_k1ax, N >= 10 on the tensor
@@ -627,21 +641,21 @@ cudaError_t launch_cg_init(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_cg_red_pap(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
+cudaError_t launch_cg_red_pap(const DevMesh &m, const CgVecs &v, const P2PDev *p2p, cudaStream_t s) {
     cg_red_kernel<<<1, kRedThreads, 0, s>>>(v.part1, v.s1, v.nb1, v.pap_all, v.st, 0, m.rank,
-                                             m.nranks);
+                                             m.nranks, p2p, kSitePap);
     return cudaGetLastError();
 }
 
-cudaError_t launch_cg_red_rr(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
+cudaError_t launch_cg_red_rr(const DevMesh &m, const CgVecs &v, const P2PDev *p2p, cudaStream_t s) {
     cg_red_kernel<<<1, kRedThreads, 0, s>>>(v.part2, v.s2, v.nb2, v.rr_all, v.st, 1, m.rank,
-                                             m.nranks);
+                                             m.nranks, p2p, kSiteRr);
     return cudaGetLastError();
 }
 
-cudaError_t launch_cg_red_rz(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
+cudaError_t launch_cg_red_rz(const DevMesh &m, const CgVecs &v, const P2PDev *p2p, cudaStream_t s) {
     cg_red_kernel<<<1, kRedThreads, 0, s>>>(v.part3, v.s2, v.nb2, v.rz_all, v.st, 1, m.rank,
-                                             m.nranks);
+                                             m.nranks, p2p, kSiteRz);
     return cudaGetLastError();
 }
 
