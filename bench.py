@@ -60,6 +60,11 @@ def parse():
     ap.add_argument("--fd-radii", type=int, nargs="+", default=[1, 2, 3, 4, 5, 6, 7])
     ap.add_argument("--cpu-its", type=int, default=100,
                     help="oracle CG iterations timed for cpu_baseline (bounded sample)")
+    ap.add_argument("--share-device", action="store_true",
+                    help="HARNESS CHECK, not a measurement: every rank of --gpus N on cuda:0 "
+                         "(gloo process group, the peer-memory transport over CUDA IPC, "
+                         "SEM_COMM=p2p) -- runs the N > 1 code path of this script on a "
+                         "one-GPU box")
     ap.add_argument("--ref-its", type=int, default=10,
                     help="oracle CG iterations per --impl reference step")
     ap.add_argument("--cpu-threads", type=int, default=0,
@@ -431,7 +436,7 @@ def spawn_ranks(args):
 
     import torch
     have = torch.cuda.device_count()
-    if have < args.gpus:
+    if have < args.gpus and not (args.share_device and have >= 1):
         print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible", file=sys.stderr)
         sys.exit(2)
     s = socket.socket()
@@ -466,11 +471,17 @@ def main():
 
     from paper_1403_0968_b200 import meshgen, sem
 
+    if args.share_device:                 # harness check: all ranks on cuda:0
+        local_rank = 0
+        os.environ["SEM_COMM"] = "p2p"
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.share_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
 
     def barrier():
@@ -480,7 +491,7 @@ def main():
     def max_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if args.share_device else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -715,6 +726,8 @@ def main():
                        "partition": "x".join(map(str, parts)), "operator": args.operator,
                        "precond": args.precond, "cg_variant": args.cg_variant,
                        "parallelism": f"element partition over {world} GPU(s)",
+                       **({"harness_check": "--share-device: all ranks time-share cuda:0; "
+                                            "NOT a measurement"} if args.share_device else {}),
                        "l2": f"inputs larger than L2: {ws / 2**20:.0f} MiB resident working set "
                              f"> {L2_BYTES / 2**20:.0f} MiB L2, streamed every iteration"},
             "ax": ax,
