@@ -231,7 +231,9 @@ int sem_loopback_unique_id(void *id_out);
  * sem_profile(ctx, 0) stops.  sem_profile_read synchronises the stream and
  * returns, for class `which` (0 = sem_ax kernel, 1 = CG kernel K1: x/p update
  * + Ax + (w,p), 2 = CG kernel K2: DSSUM + mask fused with the r update and
- * (r,r), 3 = sem_dssum gather-scatter, 4 = other), the summed device
+ * (r,r), 3 = sem_dssum gather-scatter, 4 = other, 5 = the resident CG kernel:
+ * the whole iteration loop of a one-rank N = 7 Poisson sem_cg as one launch,
+ * bytes reported as 0 -- the caller knows the iteration count), the summed device
  * milliseconds, the number of launches that did work (CG launches after the
  * stopping decision are excluded) and their ALGORITHMIC bytes (DESIGN.md:
  * Ax 64 B/node; K1 96 B/node, 72 at k = 0; K2 16 B per surface copy + 8 B per
@@ -248,6 +250,18 @@ int sem_profile(sem_ctx *ctx, int enable);
  * is left undefined until the next sem_cg.  Asynchronous. */
 int sem_kernel_replay(sem_ctx *ctx, int which, int reps);
 int sem_profile_read(sem_ctx *ctx, int which, double *ms, int64_t *launches, double *bytes);
+
+/* Phase clock of the last sem_cg when it ran as the resident kernel (opt-in
+ * with the environment variable SEM_CG_RESIDENT=1, set when the workspace is
+ * sized (its tables add ~12 KB per element) and at sem_cg; one rank, N = 7, Poisson,
+ * no preconditioner, E <= 28 per SM, non-Dirichlet multiplicities <= 8;
+ * DESIGN.md §6 "Resident CG"): us[0..3] =
+ * microseconds per iteration that CTA 0 spent in (0) the x / p update and the
+ * operator of its elements, (1) the first grid barrier and the (p, A p) sum,
+ * (2) the DSSUM + r update of its elements, (3) the second grid barrier and the
+ * (r, r) sum (device %globaltimer).  Synchronises the context stream.
+ * SEM_EINVAL if the last solve did not run resident. */
+int sem_cg_phases(sem_ctx *ctx, double *us);
 
 /* Host-only and collective over mesh->allgather: the interface exchange plan
  * sem_setup builds for nranks > 1, without touching a GPU.

@@ -11,7 +11,7 @@ CSRC = os.path.join(PKG, "csrc")
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libsem.so")
 SOURCES = ["sem_kernels.cu", "ax_tma.cu", "ax_tma_mass.cu", "ax_tma_pc.cu", "cg_update.cu", "sem_host.cpp",
-           "sem_comm.cu", "fd2d.cu", "ax_tma_sr.cu", "cg_sr.cu"]
+           "sem_comm.cu", "fd2d.cu", "ax_tma_sr.cu", "cg_sr.cu", "cg_resident.cu"]
 HEADERS = ["sem_internal.h", "sem_comm.h", "p2p_dev.cuh", "cg_device.cuh", "ax_tma.cuh", "ax_dmma.cuh", "ax_dmmag.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

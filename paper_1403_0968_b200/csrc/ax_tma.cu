@@ -30,6 +30,7 @@ cudaError_t upload_const_D(int N, const double *D_host) {
     cudaError_t e = upload_D_this_tu(N, D_host);
     if (e == cudaSuccess) e = upload_const_D_mass(N, D_host);
     if (e == cudaSuccess) e = upload_const_D_pc(N, D_host);
+    if (e == cudaSuccess) e = upload_const_D_rcg(N, D_host);
     return e == cudaSuccess ? upload_const_D_sr(N, D_host) : e;
 }
 

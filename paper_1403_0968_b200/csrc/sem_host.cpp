@@ -25,7 +25,7 @@
 using namespace sem;
 
 // kernel classes for sem_profile_read (documented in include/sem.h)
-enum { kProfAx = 0, kProfAxCg = 1, kProfK2 = 2, kProfGs = 3, kProfOther = 4, kProfClasses = 5 };
+enum { kProfAx = 0, kProfAxCg = 1, kProfK2 = 2, kProfGs = 3, kProfOther = 4, kProfRcg = 5, kProfClasses = 6 };
 
 struct sem_ctx {
     int N = 0, n = 0, n3 = 0;
@@ -63,6 +63,11 @@ struct sem_ctx {
     // Jacobi preconditioner (NEXT-2): mask / Q Q^T diag(A_L), formed on first use
     double *dinv_buf = nullptr;
     bool dinv_ready = false;
+    // resident CG (cg_resident.cu): eligible mesh / device, and its buffers
+    bool rcg_ok = false;
+    bool rcg_last = false;           // the last sem_cg ran resident (sem_cg_phases)
+    int rcg_iters = 0;
+    RcgBufs rcg{};
 };
 
 static constexpr int kChunk = 8;     // CG iterations per graph launch / poll (multiple of 4)
@@ -224,6 +229,7 @@ static void diff_matrix(int N, const double *x, double *D) {
 namespace {
 struct Layout {
     size_t G, BM, H, r, p, w, xw, z, dinv, D, gs_idx, own, partials, rr_all, pap_all, st, total;
+    size_t rcg_meta, rcg_sbq, rcg_push, rcg_X, rcg_part, rcg_bar;   // resident CG (N = 7, one rank, Poisson)
     int64_t nsurf_cap, partial_cap;
 };
 
@@ -258,6 +264,19 @@ Layout make_layout(int N, int64_t E, int nranks, bool mass) {
     Lo.rr_all = take(sizeof(double) * 2 * kRing * nranks);     // rr_all, then rz_all
     Lo.pap_all = take(sizeof(double) * kRing * nranks);
     Lo.st = take(sizeof(CgState));
+    // the resident CG's tables (opt-in, SEM_CG_RESIDENT=1 when the workspace
+    // is sized and the context set up: ~12 KB per element)
+    const char *rcg_env = getenv("SEM_CG_RESIDENT");
+    if (N == 7 && nranks == 1 && !mass && rcg_env && rcg_env[0] == '1') {
+        // push-based DSSUM: meta per local node, slot bases per node position,
+        // push destinations and receive slots (<= kRcgMaxSlots per element)
+        Lo.rcg_meta = take(sizeof(uint8_t) * L);
+        Lo.rcg_sbq = take(sizeof(int32_t) * n3);
+        Lo.rcg_push = take(sizeof(int32_t) * E * kRcgMaxSlots);
+        Lo.rcg_X = take(sizeof(double) * E * kRcgMaxSlots);
+        Lo.rcg_part = take(sizeof(double) * 2 * Lo.partial_cap);
+        Lo.rcg_bar = take(sizeof(uint32_t) * 64);
+    }
     Lo.total = o;
     return Lo;
 }
@@ -604,6 +623,70 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
             CU(cudaMemcpyAsync((void *)dm.gs_idx, hp.cidx.data(), sizeof(int32_t) * hp.cidx.size(),
                                cudaMemcpyHostToDevice, s));
         CU(cudaMemsetAsync(cv.st, 0, sizeof(CgState), s));
+        // resident CG (cg_resident.cu): the push-based DSSUM tables.  Copy c of
+        // element e at node position q with m copies (ascending c_0 < .. <
+        // c_{m-1}, c = c_pos) receives the values of the m - 1 other copies in
+        // ascending order into X[e S + sb(q) + t], t < m - 1 (S slots per
+        // element, sb(q) = prefix of the per-position reservation R(q) = max
+        // over elements of m - 1); push[e S + sb(q) + t] is where c writes its
+        // own value for the t-th other copy (ascending).  meta = m | pos << 4
+        // (m = 0: Dirichlet copy, never updated).
+        if (Lo.rcg_meta && rcg_supported(dm)) {
+            const int n3 = ctx->n3;
+            const int64_t L = ctx->L;
+            std::vector<uint8_t> meta(L, 1);      // interior / unshared: m = 1, pos = 0
+            std::vector<int32_t> Rq(n3, 0);
+            int mmax = 1;
+            for (int32_t q = 0; q < hp.ngroups; ++q) {
+                const int32_t a0 = hp.off[q], a1 = hp.off[q + 1], mq = a1 - a0;
+                for (int32_t t = a0; t < a1; ++t) {
+                    const int32_t c = hp.idx[t];
+                    if (q < hp.ndir) {
+                        meta[c] = 0;
+                    } else {
+                        meta[c] = (uint8_t)((mq & 15) | ((t - a0) << 4));
+                        Rq[c % n3] = std::max(Rq[c % n3], mq - 1);
+                    }
+                }
+                if (q >= hp.ndir) mmax = std::max(mmax, (int)mq);
+            }
+            std::vector<int32_t> sbq(n3 + 1, 0);
+            for (int q = 0; q < n3; ++q) sbq[q + 1] = sbq[q] + Rq[q];
+            const int64_t S = (sbq[n3] + 3) & ~int64_t(3);      // 16-byte bulk copies (X and push)
+            if (mmax <= kRcgMaxM && S <= kRcgMaxSlots) {
+                std::vector<int32_t> push((size_t)(ctx->E * S), -1);
+                auto xslot = [&](int32_t c, int t) {
+                    return (int64_t)(c / n3) * S + sbq[c % n3] + t;
+                };
+                for (int32_t q = hp.ndir; q < hp.ngroups; ++q) {
+                    const int32_t a0 = hp.off[q], mq = hp.off[q + 1] - a0;
+                    for (int j = 0; j < mq; ++j) {
+                        int t = 0;
+                        for (int i = 0; i < mq; ++i) {
+                            if (i == j) continue;
+                            // c_j's value is c_i's ((j < i) ? j : j - 1)-th other copy
+                            push[xslot(hp.idx[a0 + j], t++)] = (int32_t)xslot(hp.idx[a0 + i], j < i ? j : j - 1);
+                        }
+                    }
+                }
+                std::vector<int32_t> sbh(sbq.begin(), sbq.begin() + n3);
+                RcgBufs &rb = ctx->rcg;
+                rb.S = (int32_t)S;
+                rb.meta = reinterpret_cast<uint8_t *>(ws + Lo.rcg_meta);
+                rb.sbq = reinterpret_cast<int32_t *>(ws + Lo.rcg_sbq);
+                rb.push = reinterpret_cast<int32_t *>(ws + Lo.rcg_push);
+                rb.X = reinterpret_cast<double *>(ws + Lo.rcg_X);
+                rb.part = reinterpret_cast<double *>(ws + Lo.rcg_part);
+                rb.bar = reinterpret_cast<uint32_t *>(ws + Lo.rcg_bar);
+                CU(cudaMemcpyAsync(rb.meta, meta.data(), L, cudaMemcpyHostToDevice, s));
+                CU(cudaMemcpyAsync(rb.sbq, sbh.data(), sizeof(int32_t) * n3, cudaMemcpyHostToDevice, s));
+                CU(cudaMemcpyAsync(rb.push, push.data(), sizeof(int32_t) * push.size(),
+                                   cudaMemcpyHostToDevice, s));
+                CU(rcg_prepare());
+                CU(cudaStreamSynchronize(s));   // (host vectors go out of scope)
+                ctx->rcg_ok = true;
+            }
+        }
         CU(cudaMemsetAsync(cv.rr_all, 0, sizeof(double) * kRing * ctx->nranks, s));
         CU(cudaMemsetAsync(cv.rz_all, 0, sizeof(double) * kRing * ctx->nranks, s));
         CU(cudaMemsetAsync(cv.pap_all, 0, sizeof(double) * kRing * ctx->nranks, s));
@@ -1148,6 +1231,13 @@ static int cg_sr_impl(sem_ctx *ctx, const double *b, double *x, double tol, int 
     return SEM_OK;
 }
 
+// opt-in (SEM_CG_RESIDENT=1): measured slower than the two-kernel schedule at
+// c3 (57.8 vs 44.0 us per iteration, DESIGN.md §6 "Resident CG")
+static bool rcg_enabled() {
+    const char *e = getenv("SEM_CG_RESIDENT");
+    return e && e[0] == '1';
+}
+
 static int cg_impl(sem_ctx *ctx, int precond, const double *b, double *x, double tol, int maxit,
                    int *iters, double *rel_res) {
     if (!b || !x || !aligned16(b) || !aligned16(x)) return fail(ctx, SEM_EINVAL, "sem_cg: bad pointer");
@@ -1180,14 +1270,26 @@ static int cg_impl(sem_ctx *ctx, int precond, const double *b, double *x, double
         if (v.dinv && (rc = fold_allgather(ctx, 2, v.rz_all + 0 * P, s))) return rc;
     }
 
-    cudaGraphExec_t gexec = nullptr;
-    if ((rc = chunk_graph(ctx, gexec))) return rc;
-    if ((rc = run_chunks(ctx, maxit, gexec, s))) return rc;
-    LAUNCH(launch_cg_finish(ctx->dm, v, s));
+    // one rank, N = 7, Poisson CG: the whole solve as one resident kernel
+    // (cg_resident.cu) when SEM_CG_RESIDENT=1
+    const bool resident = ctx->rcg_ok && !v.dinv && P == 1 && rcg_enabled();
+    if (resident) {
+        CU(cudaMemsetAsync(&v.st->rcg_err, 0, sizeof(int32_t), s));
+        LAUNCHP(kProfRcg, 0.0, -1, launch_rcg(ctx->dm, v, ctx->rcg, s));
+    } else {
+        cudaGraphExec_t gexec = nullptr;
+        if ((rc = chunk_graph(ctx, gexec))) return rc;
+        if ((rc = run_chunks(ctx, maxit, gexec, s))) return rc;
+        LAUNCH(launch_cg_finish(ctx->dm, v, s));
+    }
     CU(cudaMemcpyAsync(&ctx->host_state[0], v.st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     const CgState &hs = ctx->host_state[0];
     if (int rc = transport_ok(ctx)) return rc;
+    ctx->rcg_last = resident;
+    ctx->rcg_iters = hs.iters;
+    if (resident && hs.rcg_err)
+        return fail(ctx, SEM_ECUDA, "sem_cg: resident CG grid barrier timed out");
     if (!hs.done) return fail(ctx, SEM_ECUDA, "sem_cg: device did not reach a stopping decision");
     if (ctx->prof) prof_fold(ctx, hs.iters);
     if (iters) *iters = hs.iters;
@@ -1251,6 +1353,18 @@ extern "C" int sem_kernel_replay(sem_ctx *ctx, int which, int reps) {
     CU(e);
     CU(cudaGraphLaunch(ctx->replay_exec, s));
     ctx->launches += (which == 3 ? 2 : 1) * int64_t(reps);
+    return SEM_OK;
+}
+
+extern "C" int sem_cg_phases(sem_ctx *ctx, double *us) {
+    CHECK_CTX();
+    if (!us) return fail(ctx, SEM_EINVAL, "sem_cg_phases: us is NULL");
+    if (!ctx->rcg_last) return fail(ctx, SEM_EINVAL, "sem_cg_phases: the last sem_cg did not run resident");
+    uint64_t ns[4];
+    CU(cudaMemcpyAsync(ns, ctx->rcg.bar + 16, sizeof ns, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    const double it = ctx->rcg_iters > 0 ? ctx->rcg_iters : 1;
+    for (int q = 0; q < 4; ++q) us[q] = 1e-3 * (double)ns[q] / it;
     return SEM_OK;
 }
 

@@ -26,6 +26,8 @@ struct CgState {
     // single-reduction CG (NEXT-3): gamma_k, alpha_k of iteration k in slot k & 1
     double gamma_hist[2];
     double alpha_hist[2];
+    int32_t rcg_err;            // resident CG: 1 = a grid barrier timed out (lost CTA)
+    int32_t pad_;
 };
 
 // Gather-scatter groups are stored by class (Dirichlet flag, multiplicity m):
@@ -150,6 +152,27 @@ cudaError_t launch_sr_fold(const DevMesh &m, const CgVecs &v, const P2PDev *p2p,
 // (the caller masks it)
 cudaError_t launch_diag(const DevMesh &m, double *d, cudaStream_t s);
 cudaError_t launch_recip(const DevMesh &m, const double *d, double *dinv, cudaStream_t s);
+
+// cg_resident.cu: the whole CG solve at N = 7 as one persistent cooperative
+// kernel with x, r in TMEM and p in shared memory (one rank, Poisson, no
+// preconditioner, E <= 28 per SM).  Runs after the CG start (cg_init + K2
+// INIT) and leaves x, the state words and rcg_err behind.
+constexpr int kRcgMaxM = 8;           // largest multiplicity of a non-Dirichlet group
+constexpr int kRcgMaxSlots = 1024;    // receive slots per element (S, even)
+struct RcgBufs {
+    int32_t S;                  // receive slots per element
+    uint8_t *meta;              // [L] m | pos << 4 (m = 0: Dirichlet copy)
+    int32_t *sbq;               // [n^3] first receive slot of each node position
+    int32_t *push;              // [E][S] destination (index into X) of each pushed value
+    double *X;                  // [E][S] receive slots: the other copies' w, ascending
+    double *part;               // [2][kMaxPartials] per-CTA partials
+    uint32_t *bar;              // grid barrier counter; bar + 16: 4 x uint64 phase clocks
+};
+bool rcg_supported(const DevMesh &m);
+int rcg_blocks(const DevMesh &m);
+cudaError_t rcg_prepare();
+cudaError_t upload_const_D_rcg(int N, const double *D_host);
+cudaError_t launch_rcg(const DevMesh &m, const CgVecs &v, const RcgBufs &rb, cudaStream_t s);
 
 // ax_tma.cu
 bool tma_supported(int N);

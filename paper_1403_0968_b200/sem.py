@@ -43,7 +43,7 @@ class SemMesh(ctypes.Structure):
 EXPORTS = ["sem_version", "sem_gll", "sem_workspace_bytes", "sem_setup", "sem_sizes",
            "sem_ax", "sem_dssum", "sem_mask", "sem_mass", "sem_cg", "sem_launch_count",
            "sem_free", "sem_strerror", "sem_last_error", "sem_nccl_id_bytes",
-           "sem_nccl_get_unique_id", "sem_loopback_unique_id", "sem_profile", "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan", "sem_status",
+           "sem_nccl_get_unique_id", "sem_loopback_unique_id", "sem_profile", "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan", "sem_status", "sem_cg_phases",
            "sem_pcg", "sem_diag", "sem_cg_sr", "fd_weights", "fd2d_step", "fd2d_run", "fd2d_run_ex"]
 
 # preconditioners of sem_pcg (include/sem.h enum sem_precond)
@@ -103,11 +103,13 @@ def lib():
     L.sem_nccl_get_unique_id.argtypes = [P]
     L.sem_loopback_unique_id.argtypes = [P]
     L.sem_kernel_replay.argtypes = [P, ctypes.c_int, ctypes.c_int]
+    L.sem_cg_phases.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
     L.sem_exchange_plan.argtypes = [ctypes.POINTER(SemMesh), ctypes.c_int, P, P, i64,
                                     ctypes.POINTER(i64), ctypes.POINTER(i64)]
     for f in ("sem_gll", "sem_workspace_bytes", "sem_setup", "sem_sizes", "sem_ax", "sem_dssum",
               "sem_mask", "sem_mass", "sem_cg", "sem_nccl_get_unique_id", "sem_loopback_unique_id", "sem_profile",
-              "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan", "sem_pcg", "sem_diag", "sem_cg_sr"):
+              "sem_profile_read", "sem_kernel_replay", "sem_exchange_plan", "sem_pcg", "sem_diag", "sem_cg_sr",
+              "sem_cg_phases"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
@@ -280,7 +282,7 @@ class Context:
         self.mask(b)
         return b
 
-    PROF_CLASSES = ("ax", "k1", "k2", "dssum", "other")
+    PROF_CLASSES = ("ax", "k1", "k2", "dssum", "other", "rcg")
 
     def profile(self, enable: bool = True):
         _check(lib().sem_profile(self._ctx, 1 if enable else 0), self._ctx)
@@ -294,6 +296,15 @@ class Context:
                                           ctypes.byref(by)), self._ctx)
             out[nm] = (ms.value, n.value, by.value)
         return out
+
+    CG_PHASES = ("update_operator", "barrier_pap", "dssum_r_update", "barrier_rr")
+
+    def cg_phases(self):
+        """{phase: us per iteration} of CTA 0 in the last sem_cg, which must
+        have run as the resident kernel (include/sem.h sem_cg_phases)."""
+        us = (ctypes.c_double * 4)()
+        _check(lib().sem_cg_phases(self._ctx, us), self._ctx)
+        return dict(zip(self.CG_PHASES, list(us)))
 
     KERNELS = {"ax": 0, "k1": 1, "k2": 2, "ax+dssum": 3}
 
