@@ -117,6 +117,11 @@ int sem_workspace_bytes(const sem_mesh *mesh, int N, size_t *bytes);
  * and for nranks > 1 the NCCL communicator and interface exchange lists.
  * `workspace` is a DEVICE buffer of at least sem_workspace_bytes bytes, 256-byte
  * aligned.  `cuda_stream` is a cudaStream_t (NULL = legacy default stream).
+ * L2 (opt-in): with the environment variable SEM_L2_PERSIST=1, sem_setup raises the
+ * device's persisting-L2 limit (cudaLimitPersistingL2CacheSize, never lowered)
+ * to cover the four CG work vectors r, p, w, x-copy (contiguous in the
+ * workspace, 32 nlocal bytes) and sem_cg's CUDA-graph kernels mark their
+ * accesses to them persisting; sem_free resets the persisting lines.
  * Collective.  Synchronises the stream before returning. */
 int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t bytes,
               void *cuda_stream, sem_ctx **out);

@@ -24,6 +24,10 @@
 
 namespace sem {
 
+#ifndef SEM_DMMA_W4_GROUPS
+#define SEM_DMMA_W4_GROUPS 2
+#endif
+
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(c0), "+d"(c1)
@@ -43,7 +47,7 @@ struct DmmaLayout {
     static constexpr int STAGE = NV * C::VL + 6 * C::n3;        // doubles
     static constexpr int SMEM_MAX = 227 * 1024 - 1024;
     static constexpr int NG_FIT = SMEM_MAX / (2 * STAGE * 8);
-    static constexpr int NG_CAP = W == 2 ? 4 : 2;
+    static constexpr int NG_CAP = W == 2 ? 4 : SEM_DMMA_W4_GROUPS;   // W=4: 2 (3 measured slower, r02)
     static constexpr int NG = NG_FIT > NG_CAP ? NG_CAP : NG_FIT;  // groups per CTA
     static constexpr int NT = NG * GT;
     static constexpr size_t SMEM = size_t(NG) * 2 * STAGE * 8 + 128;

@@ -63,6 +63,10 @@ struct sem_ctx {
     // Jacobi preconditioner (NEXT-2): mask / Q Q^T diag(A_L), formed on first use
     double *dinv_buf = nullptr;
     bool dinv_ready = false;
+    // L2 persistence of the CG work vectors r, p, w, xw (contiguous in the
+    // workspace): access-policy window attached to the CG graph's kernel nodes
+    bool l2_on = false;
+    cudaAccessPolicyWindow l2win{};
     // resident CG (cg_resident.cu): eligible mesh / device, and its buffers
     bool rcg_ok = false;
     bool rcg_last = false;           // the last sem_cg ran resident (sem_cg_phases)
@@ -587,6 +591,38 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         }
         const char *gr = getenv("SEM_CG_GRAPH");
         ctx->use_graph = !(gr && strcmp(gr, "0") == 0);
+        // L2 persistence of the CG work vectors (opt-in, SEM_L2_PERSIST=1):
+        // r, p, w, xw are contiguous in the workspace; the persisting
+        // set-aside is raised to cover them (device-wide limit, only raised).
+        // Off by default: the vectors already stay L2-resident under the
+        // kernels' evict-first G^ / evict-last vector hints (application-replay
+        // ncu r02: K1 reads ~104 MB of DRAM per launch, G^ alone is 100.7) and
+        // c3 measured the same with and without (bench r02f: 48.3-48.5 GDOF/s)
+        const char *lp = getenv("SEM_L2_PERSIST");
+        if (lp && lp[0] == '1') {
+            int maxp = 0, maxw = 0;
+            cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, mesh->device);
+            cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, mesh->device);
+            const size_t span = (size_t)((const char *)(cv.xw + ctx->L) - (const char *)cv.r);
+            const size_t win = std::min(span, (size_t)maxw);
+            size_t cur = 0;
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            const size_t want = std::min(win, (size_t)maxp);
+            if (want > cur) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            if (win > 0 && cur > 0) {
+                ctx->l2win.base_ptr = (void *)cv.r;
+                ctx->l2win.num_bytes = win;
+                ctx->l2win.hitRatio = (float)std::min(1.0, (double)cur / (double)win);
+                ctx->l2win.hitProp = cudaAccessPropertyPersisting;
+                ctx->l2win.missProp = cudaAccessPropertyStreaming;
+                ctx->l2_on = true;
+            }
+            if (getenv("SEM_L2_VERBOSE"))
+                fprintf(stderr, "libsem L2: max persisting %d B, max window %d B, span %zu B, limit %zu B, hitRatio %.3f\n",
+                        maxp, maxw, span, cur, (double)ctx->l2win.hitRatio);
+            cudaGetLastError();   // (attribute queries are best effort)
+        }
     }
     // one rank: SEM_K1_SPLIT=<fraction of E> exercises the boundary/interior
     // K1 split without an exchange (testing only; multi-rank sets nbnd below)
@@ -804,8 +840,9 @@ extern "C" int sem_exchange_plan(const sem_mesh *mesh, int N, int64_t *counts, i
 
 extern "C" void sem_free(sem_ctx *ctx) {
     if (!ctx) return;
-    if (ctx->graph_exec[0] || ctx->graph_exec[1] || ctx->graph_exec[2] || ctx->replay_exec)
+    if (ctx->graph_exec[0] || ctx->graph_exec[1] || ctx->graph_exec[2] || ctx->replay_exec || ctx->l2_on)
         cudaStreamSynchronize(ctx->stream);
+    if (ctx->l2_on) cudaCtxResetPersistingL2Cache();   // the work vectors' lines back to normal
     for (auto &g : ctx->graph_exec)
         if (g) cudaGraphExecDestroy(g);
 
@@ -1055,6 +1092,21 @@ static int build_cg_graph(sem_ctx *ctx) {
         return rc;
     }
     CU(e);
+    if (ctx->l2_on) {
+        // every kernel node of the chunk keeps the work vectors L2-resident
+        size_t nn = 0;
+        CU(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        CU(cudaGraphGetNodes(g, nodes.data(), &nn));
+        cudaKernelNodeAttrValue av{};
+        av.accessPolicyWindow = ctx->l2win;
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType ty;
+            CU(cudaGraphNodeGetType(nd, &ty));
+            if (ty == cudaGraphNodeTypeKernel)
+                CU(cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &av));
+        }
+    }
     e = cudaGraphInstantiate(&ctx->graph_exec[ctx->method], g, 0);
     cudaGraphDestroy(g);
     CU(e);
