@@ -19,6 +19,10 @@
 
 namespace sem {
 
+#ifndef SEM_DMMAG_SWZ
+#define SEM_DMMAG_SWZ 1
+#endif
+
 template <int N>
 struct DgCfg {
     static constexpr int n = N + 1, n2 = n * n, n3 = n2 * n;
@@ -48,6 +52,15 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
     // every staged array (n^2, n^3, VL even, shift 0) -- one conflict-free
     // 128-bit access instead of two 4-way-conflicted 64-bit ones (ncu r01aw)
     constexpr bool VEC = (n % 2) == 0;
+    // n = 16: rows of 128 bytes put a quarter-warp's node pairs (rows j, j+1)
+    // and the DMMA fragments' rows on the same banks (ncu r02hi_n15: 64% of the
+    // shared wavefronts were conflict excess, L1 82% busy).  Each staged row
+    // (u and G^, row index j within its slice) is permuted in place once per
+    // element: 16-byte chunk c -> c ^ sigma(j), sigma(j) = (j & 1) << 2 |
+    // (j >> 1) & 3 -- node pairs, A- and B-fragment loads all conflict-free /
+    // two wavefronts.  Element (row j, column c) then lives at column
+    // c ^ 2 sigma(j) (sc below).
+    constexpr bool SWZ = (n == 16) && SEM_DMMAG_SWZ;
     extern __shared__ __align__(128) double smem[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + size_t(NG) * NS * STAGE);
 
@@ -163,8 +176,11 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
         wsA[ks] = (jb < n && m < n) ? c_D[DO + m * n + jb] : 0.0;
     }
     // G^ factor f of node (k, jj, ii) within the staged element
+    auto sc = [&](int jj, int ii) -> int {
+        return SWZ ? ii ^ ((((jj & 1) << 2) | ((jj >> 1) & 3)) << 1) : ii;
+    };
     auto gidx = [&](int f, int k, int jj, int ii) -> int {
-        return SLICE ? k * 6 * n2 + f * n2 + jj * n + ii : f * n3 + k * n2 + jj * n + ii;
+        return SLICE ? k * 6 * n2 + f * n2 + jj * n + sc(jj, ii) : f * n3 + k * n2 + jj * n + sc(jj, ii);
     };
 
     int t = 0;
@@ -175,12 +191,26 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
         mbar_wait(gbar + s, NS == 2 ? (t >> 1) & 1 : t & 1);
         const double *su = sb + sh;
         double *sG = sb + VL;
+        if constexpr (SWZ) {
+            // in-place row permutation of u (n^2 rows) and G^ (6 n^2 rows):
+            // lane = (row r = 4 warp' + lane / 8 of the step, chunk lane % 8)
+            constexpr int ROWS = n2 + 6 * n2;
+            const int c = lane & 7;
+            for (int r = warp * 4 + (lane >> 3); r < ROWS; r += (GT / 32) * 4) {
+                double *row = (r < n2) ? (sb + sh) + r * n : sG + (r - n2) * n;
+                const int jj = (r < n2 ? r : r - n2) & (n - 1);
+                const double2 v = *reinterpret_cast<const double2 *>(row + 2 * c);
+                __syncwarp();
+                *reinterpret_cast<double2 *>(row + 2 * (c ^ (((jj & 1) << 2) | ((jj >> 1) & 3)))) = v;
+            }
+            group_bar(1 + g, GT);
+        }
 
         double c0v[n], c1v[n];                  // the lane's two input columns
 #pragma unroll
         for (int m = 0; m < n; ++m) {
             if constexpr (VEC) {                // even n: node pairs are 16-byte aligned
-                const double2 c = v0 ? *reinterpret_cast<const double2 *>(su + m * n2 + j * n + i0)
+                const double2 c = v0 ? *reinterpret_cast<const double2 *>(su + m * n2 + j * n + sc(j, i0))
                                      : make_double2(0.0, 0.0);
                 c0v[m] = c.x;
                 c1v[m] = c.y;
@@ -196,8 +226,8 @@ __global__ void __launch_bounds__(DgCfg<N>::NT, 1) ax_dmmag_kernel(TmaArgs a) {
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) {
                 const int m = 4 * ks + tig;
-                const double aa = (jb < n && m < n) ? uk[jb * n + m] : 0.0;   // P_k[j][m]
-                const double bb = (ib < n && m < n) ? uk[m * n + ib] : 0.0;   // P_k[m][i]
+                const double aa = (jb < n && m < n) ? uk[jb * n + sc(jb, m)] : 0.0;   // P_k[j][m]
+                const double bb = (ib < n && m < n) ? uk[m * n + sc(m, ib)] : 0.0;   // P_k[m][i]
                 dmma(r0, r1, aa, urB[ks]);
                 dmma(s0, s1, usA[ks], bb);
             }
