@@ -1,8 +1,8 @@
 """Small invocations of every libsem kernel family, for compute-sanitizer
 (tools/sanitizer_sweep.sh): Ax (element-staged TMA, N=7 DMMA with 2 and 4
 warps per element, high-order slice-streamed, tensor-core high-order, simple),
-K1/K2 CG iterations, the split high-order K1 (x/p update + tensor-core
-operator), Jacobi PCG, single-reduction CG,
+K1/K2 CG iterations, the resident CG kernel (SEM_CG_RESIDENT=1), the split
+high-order K1 (x/p update + tensor-core operator), Jacobi PCG, single-reduction CG,
 the gather-scatter, the boundary/interior K1 split, the multi-rank loopback
 path (pack/combine/rank folds) and the FD stencil (both arithmetic forms).
 Tiny meshes, few iterations: the sanitizers slow kernels down 10-100x.
@@ -116,6 +116,9 @@ def main():
         if N == 7:
             case(N, elems, None, {"SEM_DMMA_W": "2"})
             case(N, elems, None, {"SEM_K1_SPLIT": "0.5"})
+            case(N, elems, None, {"SEM_CG_RESIDENT": "1"})      # the resident CG kernel
+            case(N, (3, 2, 1), None, {"SEM_CG_RESIDENT": "1"})
+            case(N, elems, None, {"SEM_L2_PERSIST": "1"})
         if N >= 10:
             case(N, elems, None, {"SEM_DMMAG": "0"})
             case(N, elems, None, {"SEM_K1_AX": "fused" if N >= 11 else "split"})
