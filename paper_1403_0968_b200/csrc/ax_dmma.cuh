@@ -39,11 +39,13 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
 // elements take 9.22 rounds, the last one 23% full); W = 4: two groups per
 // SM (296: 13.84 rounds, the last one 84% full) with each element done in
 // about half the time.  Stages: two per group, TMA-filled as ax_tma_kernel.
-template <bool CG, int W>
+// PCZ (Jacobi PCG without a mass term): K1 stages r and dinv next to p, x and
+// forms z = dinv r itself, so K2 need not store z at every copy (pcg_z_in_k1).
+template <bool CG, int W, bool PCZ = false>
 struct DmmaLayout {
     using C = TmaCfg<7>;
     static constexpr int GT = 32 * W;
-    static constexpr int NV = CG ? 3 : 1;                       // r,p,x | u
+    static constexpr int NV = CG ? (PCZ ? 4 : 3) : 1;           // r,p,x[,dinv] | u
     static constexpr int STAGE = NV * C::VL + 6 * C::n3;        // doubles
     static constexpr int SMEM_MAX = 227 * 1024 - 1024;
     static constexpr int NG_FIT = SMEM_MAX / (2 * STAGE * 8);
@@ -66,10 +68,11 @@ inline int dmma_w() {
 // the variant does not use, as ax_tma_kernel); PC: Jacobi PCG scalars; DOT:
 // KA of the single-reduction CG (plain apply + (u, w) partials).
 template <bool CG, bool MASS = false, bool PC = false, bool DOT = false, int W = 2>
-__global__ void __launch_bounds__(DmmaLayout<CG, W>::NT, 1) ax_dmma_kernel(TmaArgs a) {
+__global__ void __launch_bounds__(DmmaLayout<CG, W, PC && !MASS>::NT, 1) ax_dmma_kernel(TmaArgs a) {
     constexpr int N = 7;
     using C = TmaCfg<N>;
-    using Lo = DmmaLayout<CG, W>;
+    constexpr bool PCZ = PC && !MASS;     // z = dinv r formed here (a.r = r, a.u = dinv)
+    using Lo = DmmaLayout<CG, W, PCZ>;
     constexpr int n = C::n, n2 = C::n2, n3 = C::n3, GT = Lo::GT, VL = C::VL;
     constexpr int NG = Lo::NG, NV = Lo::NV, STAGE = Lo::STAGE;
     constexpr int KW = n / W;                 // k-slices per warp
@@ -121,11 +124,12 @@ __global__ void __launch_bounds__(DmmaLayout<CG, W>::NT, 1) ax_dmma_kernel(TmaAr
         const VecRange vr = vec_range(first, n3, L);
         const uint32_t vb = (uint32_t)((vr.a1 - vr.a0) * 8);
         double *sb = stage0 + size_t(s) * STAGE;
-        const double *vsrc[3];
+        const double *vsrc[4];
         if constexpr (CG) {
             vsrc[0] = a.r;
             vsrc[1] = a.p;
             vsrc[2] = a.x;
+            if constexpr (PCZ) vsrc[3] = a.u;
         } else {
             vsrc[0] = a.u;
         }
@@ -212,7 +216,7 @@ __global__ void __launch_bounds__(DmmaLayout<CG, W>::NT, 1) ax_dmma_kernel(TmaAr
             for (int kk = 0; kk < KC; ++kk) {
                 const int k = kc0 + kk;
                 const int q = k * n2 + (gt % n2);
-                const double rl = sr[q];
+                const double rl = PCZ ? sb[3 * VL + sh + q] * sr[q] : sr[q];   // z = dinv r
                 double pl;
                 if (kit == 0) {
                     pl = rl;
@@ -342,13 +346,14 @@ static int dmma_grid(int64_t E, int nsm) {
 
 template <bool CG, bool MASS, bool PC, bool DOT>
 static cudaError_t dmma_attr() {
+    constexpr bool PCZ = PC && !MASS;
     cudaError_t e = cudaFuncSetAttribute(ax_dmma_kernel<CG, MASS, PC, DOT, 2>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)DmmaLayout<CG, 2>::SMEM);
+                                         (int)DmmaLayout<CG, 2, PCZ>::SMEM);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(ax_dmma_kernel<CG, MASS, PC, DOT, 4>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)DmmaLayout<CG, 4>::SMEM);
+                                (int)DmmaLayout<CG, 4, PCZ>::SMEM);
 }
 
 // plain apply (MASS: h in a.r)
@@ -366,11 +371,14 @@ static cudaError_t launch_dmma_plain(const TmaArgs &a, int nsm, cudaStream_t s) 
 // K1 over the element range of a (cg_args)
 template <bool MASS, bool PC>
 static cudaError_t launch_dmma_cg(const TmaArgs &a, int nsm, cudaStream_t s) {
+    // (the grid of the plain CG layout: it is the count of (p, A p) partials the
+    // consumers sum, dmma_blocks; the persistent element loop covers any grid)
+    constexpr bool PCZ = PC && !MASS;
     if (dmma_w() == 4)
         return launch_pdl(ax_dmma_kernel<true, MASS, PC, false, 4>, dmma_grid_w<true, 4>(a.E, nsm),
-                          DmmaLayout<true, 4>::NT, DmmaLayout<true, 4>::SMEM, s, a);
+                          DmmaLayout<true, 4, PCZ>::NT, DmmaLayout<true, 4, PCZ>::SMEM, s, a);
     return launch_pdl(ax_dmma_kernel<true, MASS, PC, false, 2>, dmma_grid_w<true, 2>(a.E, nsm),
-                      DmmaLayout<true, 2>::NT, DmmaLayout<true, 2>::SMEM, s, a);
+                      DmmaLayout<true, 2, PCZ>::NT, DmmaLayout<true, 2, PCZ>::SMEM, s, a);
 }
 
 }  // namespace sem

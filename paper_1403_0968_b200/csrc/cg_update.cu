@@ -47,8 +47,9 @@ constexpr int kK2IntU = 4;           // element-interior nodes per thread per ch
 // groups per thread in one chunk, by multiplicity
 // (the PC kernel carries dinv and z as well: half the groups per thread, or
 // its registers spill)
-__host__ __device__ constexpr int k2_upb(int m, bool pc = false) {
-    return pc ? ((m == 1 || m == 2) ? 2 : 1) : ((m == 1 || m == 2) ? 4 : (m == 4 ? 2 : 1));
+// (pc && !zs: dinv but no z stores -- three face groups per thread fit)
+__host__ __device__ constexpr int k2_upb(int m, bool pc = false, bool zs = true) {
+    return pc ? ((m == 1 || m == 2) ? (zs ? 2 : 3) : 1) : ((m == 1 || m == 2) ? 4 : (m == 4 ? 2 : 1));
 }
 
 // One batch of U groups of a class with compile-time multiplicity M (M = 0:
@@ -58,7 +59,7 @@ __device__ __forceinline__ bool k2_owned(const K2Args &a, int g) {
     return !a.own || ((__ldg(a.own + (g >> 5)) >> (g & 31)) & 1u);
 }
 
-template <int M, int U, bool INIT, bool PC>
+template <int M, int U, bool INIT, bool PC, bool ZS = PC>
 __device__ __forceinline__ void k2_groups(const K2Args &a, const int32_t *__restrict__ ix, int m,
                                           int cnt, int q0, int qstride, double alpha, int gstart,
                                           double &part, double &partz) {
@@ -96,9 +97,11 @@ __device__ __forceinline__ void k2_groups(const K2Args &a, const int32_t *__rest
         if (own) part += rn * rn;
         if constexpr (PC) {
             const double zn = dv[u] * rn;
+            if constexpr (ZS) {
 #pragma unroll
-            for (int t = 0; t < MM; ++t)
-                if (t < mm) a.z[li[u][t]] = zn;
+                for (int t = 0; t < MM; ++t)
+                    if (t < mm) a.z[li[u][t]] = zn;
+            }
             if (own) partz += rn * zn;
         }
     }
@@ -141,7 +144,9 @@ __device__ __forceinline__ void k2_interior_idx(int64_t E, int chunk, const int3
     }
 }
 
-template <int N, bool INIT, bool PC>
+// ZS (PC only): store z = dinv r at every copy; false when K1 forms z from r
+// and dinv itself (pcg_z_in_k1: N = 7 tensor-core K1), the (r, z) partial stays
+template <int N, bool INIT, bool PC, bool ZS = PC>
 __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __grid_constant__ K2Args a) {
     constexpr int ni = N - 1;
     constexpr int U = kK2IntU;
@@ -215,7 +220,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
                         part += rn * rn;
                         if constexpr (PC) {
                             const double zn = dv[u] * rn;
-                            a.z[l[u]] = zn;
+                            if constexpr (ZS) a.z[l[u]] = zn;
                             partz += rn * zn;
                         }
                     }
@@ -230,24 +235,24 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
         const int m = a.cls.m[c];
         const int32_t *ix = a.idx + a.cls.idxoff[c];
         const int gs0 = a.cls.start[c];
-        const int base = (cg - a.cchunk[c]) * kK2Threads * k2_upb(m, PC) + threadIdx.x;
+        const int base = (cg - a.cchunk[c]) * kK2Threads * k2_upb(m, PC, ZS) + threadIdx.x;
         if (a.cls.dir[c]) {
             // Dirichlet (INIT only): r0 = 0 at every copy (mask)
-            for (int u = 0; u < k2_upb(m, PC); ++u) {
+            for (int u = 0; u < k2_upb(m, PC, ZS); ++u) {
                 const int q = base + u * kK2Threads;
                 if (q < cnt)
                     for (int t = 0; t < m; ++t) {
                         a.r[__ldg(ix + t * cnt + q)] = 0.0;
-                        if constexpr (PC) a.z[__ldg(ix + t * cnt + q)] = 0.0;
+                        if constexpr (PC && ZS) a.z[__ldg(ix + t * cnt + q)] = 0.0;
                     }
             }
             continue;
         }
         switch (m) {
-        case 1: k2_groups<1, k2_upb(1, PC), INIT, PC>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
-        case 2: k2_groups<2, k2_upb(2, PC), INIT, PC>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
-        case 4: k2_groups<4, k2_upb(4, PC), INIT, PC>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
-        case 8: k2_groups<8, 1, INIT, PC>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
+        case 1: k2_groups<1, k2_upb(1, PC, ZS), INIT, PC, ZS>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
+        case 2: k2_groups<2, k2_upb(2, PC, ZS), INIT, PC, ZS>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
+        case 4: k2_groups<4, k2_upb(4, PC, ZS), INIT, PC, ZS>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
+        case 8: k2_groups<8, 1, INIT, PC, ZS>(a, ix, m, cnt, base, kK2Threads, alpha, gs0, part, partz); break;
         default: {
             const int q = base;
             if (q < cnt) {
@@ -260,7 +265,8 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
                 if (own) part += rn * rn;
                 if constexpr (PC) {
                     const double zn = __ldg(a.dinv + __ldg(ix + q)) * rn;
-                    for (int t = 0; t < m; ++t) a.z[__ldg(ix + t * cnt + q)] = zn;
+                    if constexpr (ZS)
+                        for (int t = 0; t < m; ++t) a.z[__ldg(ix + t * cnt + q)] = zn;
                     if (own) partz += rn * zn;
                 }
             }
@@ -306,6 +312,8 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
 int k2_blocks(const DevMesh &m, bool) { return m.nsm * kK2BlocksPerSM; }
 
 cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t s) {
+    // Jacobi PCG with a K1 that forms z itself (N = 7 tensor cores): no z stores
+    const bool zs = !(v.dinv && pcg_z_in_k1(m) && m.N == 7);
     K2Args a{};
     a.cls = m.cls;
     a.idx = m.gs_idx;
@@ -329,7 +337,7 @@ cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t
     for (int c = 0; c < m.cls.n; ++c) {
         a.cchunk[c] = nch;
         const int cnt = m.cls.start[c + 1] - m.cls.start[c];
-        const int per = kK2Threads * k2_upb(m.cls.m[c], v.dinv != nullptr);
+        const int per = kK2Threads * k2_upb(m.cls.m[c], v.dinv != nullptr, zs);
         if (!m.cls.dir[c] || init) nch += (cnt + per - 1) / per;
     }
     a.cchunk[m.cls.n] = nch;
@@ -337,7 +345,11 @@ cudaError_t launch_k2(const DevMesh &m, const CgVecs &v, bool init, cudaStream_t
     const int nb = k2_blocks(m, init);
     cudaError_t e = cudaSuccess;
     const bool pc = v.dinv != nullptr;
-    if (init && pc) {
+    if (init && pc && !zs) {
+        if (m.N == 7) k2_kernel<7, true, true, false><<<nb, kK2Threads, 0, s>>>(a), e = cudaGetLastError();
+    } else if (pc && !zs) {
+        if (m.N == 7) e = launch_pdl(k2_kernel<7, false, true, false>, nb, kK2Threads, 0, s, a);
+    } else if (init && pc) {
         SEM_K2_DISPATCH(m.N, (k2_kernel<NN, true, true><<<nb, kK2Threads, 0, s>>>(a), e = cudaGetLastError()));
     } else if (init) {
         SEM_K2_DISPATCH(m.N, (k2_kernel<NN, true, false><<<nb, kK2Threads, 0, s>>>(a), e = cudaGetLastError()));

@@ -174,6 +174,9 @@ cudaError_t rcg_prepare();
 cudaError_t upload_const_D_rcg(int N, const double *D_host);
 cudaError_t launch_rcg(const DevMesh &m, const CgVecs &v, const RcgBufs &rb, cudaStream_t s);
 
+// ax_tma_pc.cu: Jacobi PCG whose K1 forms z = dinv r itself (K2 then skips z)
+bool pcg_z_in_k1(const DevMesh &m);
+
 // ax_tma.cu
 bool tma_supported(int N);
 bool dmma_supported(int N);

@@ -1,8 +1,7 @@
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/r02f_smi.txt
-timeout 1800 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/r02f_gputests.log 2>&1; echo "tests rc=$?"
-tail -3 gpurun_out/r02f_gputests.log
-for i in 1 2; do timeout 300 python bench.py --steps 20 --warmup 3 > gpurun_out/r02f_bench$i.json 2> gpurun_out/r02f_bench$i.err; echo "bench rc=$?"; done
-SEM_L2_PERSIST=0 timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/r02f_bench_nol2.json 2> gpurun_out/r02f_bench_nol2.err; echo "bench nol2 rc=$?"
-for f in gpurun_out/r02f_bench1.json gpurun_out/r02f_bench2.json gpurun_out/r02f_bench_nol2.json; do python -c "
-import json,sys; d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', d['value'], d['ms_per_step'], d['roofline']['frac'], d['roofline'].get('kernels_in_solve',{}).get('k2',{}).get('avg_launch_us'), d['e2e']['value'], d.get('clocks'))"; done
+timeout 1200 python -m pytest tests/test_gpu_pcg.py tests/test_gpu_topology.py tests/test_gpu_multirank.py tests/test_gpu_c3_parity.py -x -q -p no:cacheprovider > gpurun_out/pcgz_tests.log 2>&1; echo "tests rc=$?"
+tail -3 gpurun_out/pcgz_tests.log
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --precond jacobi > gpurun_out/pcgz_bench.json 2>/dev/null; echo "bench rc=$?"
+python -c "
+import json; d=json.loads(open('gpurun_out/pcgz_bench.json').read().strip().splitlines()[-1])
+print('value %.2f'%d['value'], 'ms %.3f'%d['ms_per_step'], d['config']['cg_iters'], {k:round(v['avg_launch_us'],2) for k,v in d['roofline']['kernels_in_solve'].items()})"
