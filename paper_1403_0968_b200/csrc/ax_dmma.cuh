@@ -24,6 +24,11 @@
 
 namespace sem {
 
+#ifndef SEM_PDL_LATE
+#define SEM_PDL_LATE 1
+#endif
+constexpr bool PDL_LATE = SEM_PDL_LATE != 0;   // (only with SEM_PDL=1 launches)
+
 #ifndef SEM_DMMA_W4_GROUPS
 #define SEM_DMMA_W4_GROUPS 2
 #endif
@@ -107,7 +112,7 @@ __global__ void __launch_bounds__(DmmaLayout<CG, W, PC && !MASS>::NT, 1) ax_dmma
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if constexpr (CG) pdl_trigger();
+    if constexpr (CG && !PDL_LATE) pdl_trigger();
 
     const uint64_t pol_g = policy_evict_first();
     const uint64_t pol_v = CG ? policy_evict_last() : policy_evict_first();
@@ -327,6 +332,7 @@ __global__ void __launch_bounds__(DmmaLayout<CG, W, PC && !MASS>::NT, 1) ax_dmma
             issue_V(e + 2 * TG, s);
         }
     }
+    if constexpr (CG && PDL_LATE) pdl_trigger();   // dependents launch during the tail
     if constexpr (CG || DOT) {
         const double bs = block_sum<Lo::NT>(pap, sred);
         if (tid == 0) a.part1[(kit & 1) * a.red.s1 + blockIdx.x] = bs;

@@ -37,8 +37,11 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    // off by default: measured slower on c3 (dependents parked at
-    // griddepcontrol.wait hold SM slots the primary's tail could use)
+    // off by default: with the trigger at kernel start measured slower on c3
+    // (dependents parked at griddepcontrol.wait hold SM slots the primary's
+    // tail could use: 46.1 vs 44.4 us/it, r02); with the trigger at the end
+    // of K1's / K2's work (SEM_PDL_LATE, now the placement) within noise
+    // (bench 47.6-47.8 vs 47.4-47.5 GDOF/s; the full GPU suite passes with it)
     static const bool enabled = [] {
         const char *e = getenv("SEM_PDL");
         return e && e[0] == '1';

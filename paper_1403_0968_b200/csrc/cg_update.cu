@@ -40,6 +40,11 @@ struct K2Args {
     int32_t nchunks;
 };
 
+#ifndef SEM_PDL_LATE
+#define SEM_PDL_LATE 1
+#endif
+constexpr bool PDL_LATE_K2 = SEM_PDL_LATE != 0;
+
 constexpr int kK2Threads = 256;
 constexpr int kK2BlocksPerSM = 3;
 constexpr int kK2IntU = 4;           // element-interior nodes per thread per chunk
@@ -152,7 +157,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
     constexpr int U = kK2IntU;
     __shared__ double sred[3 * (kK2Threads / 32)];
     __shared__ int32_t ioff[ni > 0 ? ni * ni * ni : 1];
-    if constexpr (!INIT) pdl_trigger();
+    if constexpr (!INIT && !PDL_LATE_K2) pdl_trigger();
     if constexpr (!INIT) pdl_wait();
     if constexpr (ni > 0) {
         k2_interior_table<N>(ioff);
@@ -274,6 +279,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2BlocksPerSM) k2_kernel(const __
         }
     }
 
+    if constexpr (!INIT && PDL_LATE_K2) pdl_trigger();   // dependents launch during the tail
     // one deterministic partial per block; consumers reduce (cg_device.cuh)
     if constexpr (PC) {
         double v2[2] = {part, partz};
