@@ -67,6 +67,7 @@ cudaError_t launch_ax_cg_dmmag(const DevMesh &m, const CgVecs &v, int64_t eb, in
                                cudaStream_t s) {
     cudaError_t e = launch_k1u(m, v, eb, ne, s);
     if (e != cudaSuccess) return e;
+    if (!m.use_dmmag) return launch_k1dot_range(m, v, eb, ne, pidx0, s);   // CUDA-core operator
     const int64_t o = eb * m.n3;
     TmaArgs a{};
     a.E = ne;

@@ -30,6 +30,45 @@ int ka_blocks(const DevMesh &m) {
     return nb;
 }
 
+// The operator half of the split CG K1 on the CUDA-core TMA / high-order
+// kernels (use_k1ax without the tensor-core Ax): w = A_L p over the element
+// range [eb, eb + ne) plus per-CTA (p, A p) partials into part1[pidx0 ..]
+// at the iteration parity, a no-op after the stop (the DOT flag).
+int k1dot_blocks(const DevMesh &m, int64_t ne) {
+    int nb = 0;
+    if (m.use_hi) {
+        SEM_HI_DISPATCH(m.N, nb = hi_grid<NN, false>(ne, m.nsm));
+    } else if (m.use_tma) {
+        SEM_TMA_DISPATCH(m.N, nb = tma_grid<NN, false>(ne, m.nsm));
+    }
+    return nb;
+}
+
+cudaError_t launch_k1dot_range(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne, int pidx0,
+                               cudaStream_t s) {
+    const int64_t o = eb * m.n3;
+    TmaArgs a{};
+    a.E = ne;
+    a.G = m.G + 6 * o;
+    a.u = v.p + o;
+    a.w = v.w + o;
+    a.red = make_red(m, v);
+    a.part1 = v.part1 + pidx0;
+    a.st = v.st;
+    if (m.use_hi) {
+        SEM_HI_DISPATCH(m.N, (ax_hi_kernel<NN, false, false, false, true>
+                              <<<hi_grid<NN, false>(ne, m.nsm), HiCfg<NN, false>::NT,
+                                 HiCfg<NN, false>::SMEM, s>>>(a)));
+    } else if (m.use_tma) {
+        SEM_TMA_DISPATCH(m.N, (ax_tma_kernel<NN, false, false, false, true>
+                               <<<tma_grid<NN, false>(ne, m.nsm), TmaLayout<NN, false>::NT,
+                                  TmaLayout<NN, false>::SMEM, s>>>(a)));
+    } else {
+        return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_ax_dot(const DevMesh &m, const CgVecs &v, cudaStream_t s) {
     if (m.use_dmma) return launch_dmma_plain<false, true>(sr_args(m, v), m.nsm, s);
     if (m.use_hi) return launch_ax_dot_hi_t(m, v, s);

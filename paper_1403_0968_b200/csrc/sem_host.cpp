@@ -453,6 +453,11 @@ int build_plan(const sem_mesh *m, int N, HostPlan &hp, std::string &err) {
 // ---------------------------------------------------------------------------
 // setup / teardown
 // ---------------------------------------------------------------------------
+// orders where the split K1 with the CUDA-core operator beats the fused K1
+// (c4 CG, r02: N = 9 31.6 vs 28.0 GDOF/s; the fused K1 wins at 3..6 and 8 --
+// 35.2 / 35.3 / 37.4 / 36.9 / 36.5 vs 31.8 / 31.4 / 32.2 / 32.1 / 31.4)
+static bool k1dot_default(int N) { return N == 9; }
+
 extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t bytes,
                          void *cuda_stream, sem_ctx **out) {
     sem_ctx *ctx = nullptr;
@@ -583,6 +588,11 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         const bool ax_fused = k1ax && strcmp(k1ax, "fused") == 0;
         const bool ax_split = k1ax && strcmp(k1ax, "split") == 0;
         dm.use_k1ax = dm.use_dmmag && !ax_fused && (ax_split || N >= 11);
+        // the split with the CUDA-core operator where no tensor-core Ax runs
+        // (SEM_K1_AX=split forces it; default orders below, measured r02)
+        if (!dm.use_dmmag && !dm.use_dmma && (dm.use_tma || dm.use_hi) && !ax_fused &&
+            (ax_split || k1dot_default(N)))
+            dm.use_k1ax = true;
         if (dm.H) dm.use_k1ax = false;             // (the tensor-core operator has no mass term)
         if (dm.H && !dm.use_tma && !dm.use_hi) {   // only TMA / hi carry the mass term
             dm.use_hi = hi_supported(N) && N >= hi_min;

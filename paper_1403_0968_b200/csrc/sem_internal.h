@@ -68,7 +68,8 @@ struct DevMesh {
     bool use_dmma;              // N = 7: r/s contractions on the FP64 tensor cores (ax_dmma.cuh)
     bool use_dmmag;             // N = 8..11: the plain Ax on the tensor cores (ax_dmmag.cuh)
     bool use_k1ax;              // CG K1 split in two launches: x / p update (k1u_kernel), then
-                                // the tensor-core operator with (p, A p) partials (use_dmmag, !H)
+                                // the operator with (p, A p) partials -- the tensor-core one
+                                // (use_dmmag) or the CUDA-core TMA / high-order one; !H
 };
 
 struct CgVecs {
@@ -190,6 +191,10 @@ int dmmag_blocks(int N, int64_t E, int nsm);     // N >= 8 tensor-core kernel gr
 cudaError_t launch_ax_cg_dmmag(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne, int pidx0,
                                cudaStream_t s);
 cudaError_t launch_k1u(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne, cudaStream_t s);
+// the split K1 with the CUDA-core TMA / high-order operator (use_k1ax, !use_dmmag)
+int k1dot_blocks(const DevMesh &m, int64_t ne);
+cudaError_t launch_k1dot_range(const DevMesh &m, const CgVecs &v, int64_t eb, int64_t ne, int pidx0,
+                               cudaStream_t s);
 cudaError_t tma_prepare(int N, bool mass);
 cudaError_t upload_const_D(int N, const double *D_host);
 cudaError_t launch_ax_tma(const DevMesh &m, const double *u, double *w, cudaStream_t s);

@@ -544,7 +544,7 @@ static int ax_grid(int N, int64_t E, int nsm) {
 
 // grid of K1 over ne elements (range launches: TMA / high-order kernels only)
 int ax_cg_range_blocks(const DevMesh &m, int64_t ne) {
-    if (m.use_k1ax) return dmmag_blocks(m.N, ne, m.nsm);
+    if (m.use_k1ax) return m.use_dmmag ? dmmag_blocks(m.N, ne, m.nsm) : k1dot_blocks(m, ne);
     if (m.use_dmma) return dmma_blocks(ne, m.nsm, true);
     if (m.use_hi) return hi_blocks(m.N, ne, m.nsm, true);
     return m.use_tma ? tma_blocks(m.N, ne, m.nsm, true) : ax_grid(m.N, ne, m.nsm);

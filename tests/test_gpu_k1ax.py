@@ -4,7 +4,9 @@ x / p update with the scalar prologue, then the tensor-core operator with the
 here at N = 8..10 -- and the fused CUDA-core K1 (forced at N >= 11 with
 SEM_K1_AX=fused), each against the oracle: CG and Jacobi PCG with identical
 iteration counts, x within 1e-10, on small deformed meshes and on a
-relabelled one (quarter-turned elements, non-compact ids)."""
+relabelled one (quarter-turned elements, non-compact ids).  Also the split
+with the CUDA-core operator (the TMA / high-order Ax kernels with the DOT
+flag; the default at N = 9, forced at other orders without SEM_DMMAG)."""
 import numpy as np
 import pytest
 
@@ -31,12 +33,23 @@ def relerr(a, b):
 
 
 @pytest.mark.parametrize("N,mode", [(8, "split"), (9, "split"), (10, "split"), (11, "fused"),
-                                    (12, "split"), (13, "fused"), (15, "split"), (15, "fused")])
+                                    (12, "split"), (13, "fused"), (15, "split"), (15, "fused"),
+                                    (3, "cudacore-split"), (6, "cudacore-split"), (8, "cudacore-split"),
+                                    (9, "cudacore-default"), (9, "cudacore-fused"),
+                                    (11, "cudacore-split")])
 @pytest.mark.parametrize("relabel", [False, True])
 def test_k1_schedules(dev, monkeypatch, N, mode, relabel):
     from paper_1403_0968_b200 import sem
-    monkeypatch.setenv("SEM_DMMAG", "1")
-    monkeypatch.setenv("SEM_K1_AX", mode)
+    if mode.startswith("cudacore"):
+        monkeypatch.setenv("SEM_DMMAG", "0")
+        sub = mode.split("-")[1]
+        if sub == "default":
+            monkeypatch.delenv("SEM_K1_AX", raising=False)
+        else:
+            monkeypatch.setenv("SEM_K1_AX", sub)
+    else:
+        monkeypatch.setenv("SEM_DMMAG", "1")
+        monkeypatch.setenv("SEM_K1_AX", mode)
     monkeypatch.delenv("SEM_AX_KERNEL", raising=False)
     xi, _ = oracle.gll(N)
     m = meshgen.box_mesh(N, xi, elems=(2, 2, 1) if N >= 12 else (3, 2, 2), eps=0.05)
