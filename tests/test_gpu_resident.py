@@ -90,6 +90,9 @@ def test_resident_cg_parity(dev, monkeypatch, elems, eps, kind, relab):
         xr, its_r, rel_r, st = oracle.cg(7, m.glo, m.dirichlet, G, b, tol=1e-8, maxit=3000)
         assert st == 0
     (x, its, rel, ok), nl = solve(ctx, bd, monkeypatch, True, tol=1e-8, maxit=3000)
+    ph = ctx.cg_phases()           # the resident phase clock of that solve
+    assert set(ph) == set(ctx.CG_PHASES) and all(v >= 0.0 for v in ph.values())
+    assert sum(ph.values()) > 0.0
     (x2, its2, rel2, ok2), nl2 = solve(ctx, bd, monkeypatch, False, tol=1e-8, maxit=3000)
     assert ok and ok2
     # one resident launch replaces ~2 launches per iteration
