@@ -365,7 +365,12 @@ static cudaError_t dmma_attr() {
 // plain apply (MASS: h in a.r)
 template <bool MASS, bool DOT = false>
 static cudaError_t launch_dmma_plain(const TmaArgs &a, int nsm, cudaStream_t s) {
-    if (dmma_w() == 4)
+    // small meshes (config c2: 512 elements): W = 2's three groups per SM need
+    // fewer rounds than W = 4's two -- c2 Ax 8.2 vs 9.1 us (r02); the DOT
+    // variant keeps dmma_w() (its grid is the partial count ka_blocks reads)
+    static const bool w_env = getenv("SEM_DMMA_W") != nullptr;
+    const bool w2 = DOT || w_env ? dmma_w() == 2 : a.E <= int64_t(4) * nsm;
+    if (!w2)
         ax_dmma_kernel<false, MASS, false, DOT, 4>
             <<<dmma_grid_w<false, 4>(a.E, nsm), DmmaLayout<false, 4>::NT, DmmaLayout<false, 4>::SMEM, s>>>(a);
     else
