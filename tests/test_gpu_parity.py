@@ -291,3 +291,20 @@ def test_relabelled_mesh_parity(dev, impl, N, elems):
     xr, its_r, rel_r, st = oracle.cg(N, m.glo, m.dirichlet, G, b, tol=1e-8, maxit=3000)
     assert ok and st == 0 and its == its_r, (its, its_r)
     assert relerr(x.cpu().numpy(), xr) <= 1e-10
+
+
+@pytest.mark.parametrize("extra", [0, 4])
+def test_dmma_plain_w_selection_boundary(dev, monkeypatch, extra):
+    """The N = 7 plain Ax picks two warps per element (three groups per SM) for
+    meshes of at most 4 x SMs elements and four warps above (ax_dmma.cuh
+    launch_dmma_plain): both sides of the boundary against the oracle."""
+    monkeypatch.delenv("SEM_DMMA_W", raising=False)
+    monkeypatch.delenv("SEM_AX_KERNEL", raising=False)
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    E = 4 * nsm + extra
+    m, G, J, ctx = make(7, (E // 4, 4, 1), 0.05)
+    assert m.nelem == E
+    u = meshgen.random_field(m.nlocal, 5)
+    w = ctx.ax(T(u, dev))
+    assert relerr(w.cpu().numpy(), oracle.ax(7, G, u)) <= 1e-12
+    ctx.free()
