@@ -37,6 +37,10 @@ struct sem_ctx {
     int nb_ax = 0;
     CgState *host_state = nullptr;   // pinned, 2 slots for double-buffered polling
     cudaEvent_t ev[2] = {nullptr, nullptr};
+    // chunk polling off the critical path: the state copy runs on its own
+    // stream after an event, so the next chunk's graph does not queue behind it
+    cudaStream_t poll_stream = nullptr;
+    cudaEvent_t chunk_ev[2] = {nullptr, nullptr};
     int64_t launches = 0;
     bool broken = false;
     // optional per-kernel-class device timing (bench roofline), see sem_profile
@@ -661,6 +665,14 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         if (dm.use_hi) CU(hi_prepare(N, dm.H != nullptr));
         if ((dm.use_tma || dm.use_hi) && !dm.H) CU(sr_prepare(dm));
         if (dm.use_dmmag) CU(dmmag_prepare(N));
+        {
+            const char *ps = getenv("SEM_POLL_STREAM");
+            if (!(ps && ps[0] == '0')) {
+                CU(cudaStreamCreateWithFlags(&ctx->poll_stream, cudaStreamNonBlocking));
+                CU(cudaEventCreateWithFlags(&ctx->chunk_ev[0], cudaEventDisableTiming));
+                CU(cudaEventCreateWithFlags(&ctx->chunk_ev[1], cudaEventDisableTiming));
+            }
+        }
         CU(cudaEventCreateWithFlags(&ctx->ev[0], cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&ctx->ev[1], cudaEventDisableTiming));
         CU(cudaMemcpyAsync((void *)dm.D, Dh.data(), sizeof(double) * Dh.size(),
@@ -859,6 +871,12 @@ extern "C" void sem_free(sem_ctx *ctx) {
     if (ctx->replay_exec) cudaGraphExecDestroy(ctx->replay_exec);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->poll_stream) {
+        cudaStreamSynchronize(ctx->poll_stream);
+        cudaStreamDestroy(ctx->poll_stream);
+    }
+    for (auto &e : ctx->chunk_ev)
+        if (e) cudaEventDestroy(e);
     if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
     if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
     if (ctx->comm) comm_free(ctx->comm);
@@ -1232,8 +1250,18 @@ static int run_chunks(sem_ctx *ctx, int maxit, cudaGraphExec_t gexec, cudaStream
                 if (rc) return rc;
             }
         }
-        CU(cudaMemcpyAsync(&ctx->host_state[c & 1], v.st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
-        CU(cudaEventRecord(ctx->ev[c & 1], s));
+        if (ctx->poll_stream) {
+            // (the copy may see a later chunk's state words: done / iters are
+            // sticky once set, which is all the poll reads)
+            CU(cudaEventRecord(ctx->chunk_ev[c & 1], s));
+            CU(cudaStreamWaitEvent(ctx->poll_stream, ctx->chunk_ev[c & 1], 0));
+            CU(cudaMemcpyAsync(&ctx->host_state[c & 1], v.st, sizeof(CgState), cudaMemcpyDeviceToHost,
+                               ctx->poll_stream));
+            CU(cudaEventRecord(ctx->ev[c & 1], ctx->poll_stream));
+        } else {
+            CU(cudaMemcpyAsync(&ctx->host_state[c & 1], v.st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
+            CU(cudaEventRecord(ctx->ev[c & 1], s));
+        }
         if (c > 0) {
             if ((rc = wait_event(ctx, ctx->ev[(c - 1) & 1]))) return rc;
             if (ctx->host_state[(c - 1) & 1].done) break;
@@ -1244,6 +1272,8 @@ static int run_chunks(sem_ctx *ctx, int maxit, cudaGraphExec_t gexec, cudaStream
         }
         ++c;
     }
+    // no poll copy may land after the caller's final state copy
+    if (ctx->poll_stream) CU(cudaStreamSynchronize(ctx->poll_stream));
     return SEM_OK;
 }
 
