@@ -666,8 +666,11 @@ extern "C" int sem_setup(const sem_mesh *mesh, int N, void *workspace, size_t by
         if ((dm.use_tma || dm.use_hi) && !dm.H) CU(sr_prepare(dm));
         if (dm.use_dmmag) CU(dmmag_prepare(N));
         {
+            // one rank only: with several ranks the chunks' exchanges pair up
+            // with the peers', and the harness transports (loopback, p2p on one
+            // GPU) rely on the in-stream copy's pacing (timeouts without it)
             const char *ps = getenv("SEM_POLL_STREAM");
-            if (!(ps && ps[0] == '0')) {
+            if (ctx->nranks == 1 && !(ps && ps[0] == '0')) {
                 CU(cudaStreamCreateWithFlags(&ctx->poll_stream, cudaStreamNonBlocking));
                 CU(cudaEventCreateWithFlags(&ctx->chunk_ev[0], cudaEventDisableTiming));
                 CU(cudaEventCreateWithFlags(&ctx->chunk_ev[1], cudaEventDisableTiming));
